@@ -1,0 +1,206 @@
+"""ctypes wrapper of the fp64 C oracle (oracle/pf_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs, never by the product path
+(paper_1812_01502_b200/).  It shares no code with the CUDA path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "pf_oracle.c")
+_LIB = os.path.join(_HERE, "libpforacle.so")
+
+INIT, MUTATE, RESAMPLE = 1, 2, 3
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (plain -O2, no fast-math: IEEE fp64)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c99", "-D_GNU_SOURCE", "-fPIC", "-shared", "-ffp-contract=off",
+               "-o", _LIB, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+    return _LIB
+
+
+class _Model(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("d", ctypes.c_int), ("dy", ctypes.c_int),
+                ("A", ctypes.c_float * 64), ("LQ", ctypes.c_float * 64), ("H", ctypes.c_float * 64),
+                ("Rinv", ctypes.c_float * 64), ("m0", ctypes.c_float * 8), ("L0", ctypes.c_float * 64),
+                ("sv_phi", ctypes.c_float), ("sv_sigma", ctypes.c_float), ("sv_beta", ctypes.c_float),
+                ("sv_m0", ctypes.c_float), ("sv_s0", ctypes.c_float)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        u64, u32, vp = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p
+        _lib.orc_philox4x32_10.argtypes = [vp, vp, vp]
+        _lib.orc_normal.argtypes = [u64, u32, u32, u64]
+        _lib.orc_normal.restype = ctypes.c_double
+        _lib.orc_init.argtypes = [vp, u64, u64, vp]
+        _lib.orc_mutate.argtypes = [vp, u64, u64, u32, vp, vp]
+        _lib.orc_logweight.argtypes = [vp, u64, vp, vp, vp]
+        _lib.orc_augmented_resample.argtypes = [u64, u64, u64, u32, vp, vp, vp, vp, vp]
+        _lib.orc_augmented_resample_sampled.argtypes = [u64, u64, u64, u32, vp, u64, vp, vp, vp, vp, vp, vp]
+        _lib.orc_estimates.argtypes = [ctypes.c_int, u64, vp, vp, vp, vp, vp, vp]
+        _lib.orc_step.argtypes = [vp, u64, u64, u64, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    return _lib
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def make_model(params: dict) -> _Model:
+    """Build the C model struct from inputs.model_params() (fp32 values)."""
+    m = _Model()
+    m.kind = int(params["kind"])
+    m.d = int(params["d"])
+    m.dy = int(params["dy"])
+    if m.kind == 2:
+        m.sv_phi = float(params["phi"])
+        m.sv_sigma = float(params["sigma"])
+        m.sv_beta = float(params["beta"])
+        m.sv_m0 = float(params["m0"])
+        m.sv_s0 = float(params["s0"])
+    else:
+        for name in ("A", "LQ", "H", "Rinv", "L0", "m0"):
+            arr = np.ascontiguousarray(params[name], dtype=np.float32).ravel()
+            getattr(m, name)[: arr.size] = arr.tolist()
+    return m
+
+
+def philox(ctr, key) -> np.ndarray:
+    c = np.ascontiguousarray(ctr, dtype=np.uint32)
+    k = np.ascontiguousarray(key, dtype=np.uint32)
+    out = np.zeros(4, np.uint32)
+    lib().orc_philox4x32_10(_ptr(c), _ptr(k), _ptr(out))
+    return out
+
+
+def normal(seed: int, domain: int, n: int, c: int) -> float:
+    return lib().orc_normal(seed, domain, n, c)
+
+
+def init(params: dict, N: int, seed: int) -> np.ndarray:
+    mdl = make_model(params)
+    x = np.zeros((N, mdl.d), np.float64)
+    lib().orc_init(ctypes.byref(mdl), N, seed, _ptr(x))
+    return x
+
+
+def mutate(params: dict, seed: int, n: int, xhat: np.ndarray) -> np.ndarray:
+    mdl = make_model(params)
+    xh = np.ascontiguousarray(xhat, dtype=np.float64)
+    x = np.zeros_like(xh)
+    lib().orc_mutate(ctypes.byref(mdl), xh.shape[0], seed, n, _ptr(xh), _ptr(x))
+    return x
+
+
+def logweight(params: dict, y: np.ndarray, x: np.ndarray) -> np.ndarray:
+    mdl = make_model(params)
+    xx = np.ascontiguousarray(x, dtype=np.float64)
+    yy = np.ascontiguousarray(y, dtype=np.float32)
+    lw = np.zeros(xx.shape[0], np.float64)
+    lib().orc_logweight(ctypes.byref(mdl), xx.shape[0], _ptr(yy), _ptr(xx), _ptr(lw))
+    return lw
+
+
+def augmented_resample(lw: np.ndarray, M: int, seed: int, n: int, tables: bool = True) -> dict:
+    """Alg. 3 on log-weights lw (N,). Returns dict(a[S,N], delta[S,N], logV[m-1], A[N])."""
+    lw = np.ascontiguousarray(lw, dtype=np.float64)
+    N = lw.shape[0]
+    m = N // M
+    S = int(round(np.log2(m)))
+    a = np.zeros((S, N), np.int32) if tables else None
+    delta = np.zeros((S, N), np.float32) if tables else None
+    logV = np.zeros(m - 1, np.float64)
+    A = np.zeros(N, np.int64)
+    rc = lib().orc_augmented_resample(N, M, seed, n, _ptr(lw), _ptr(a), _ptr(delta), _ptr(logV), _ptr(A))
+    if rc != 0:
+        raise ValueError(f"orc_augmented_resample rc={rc} (N={N}, M={M})")
+    return dict(a=a, delta=delta, logV=logV, A=A, S=S, m=m)
+
+
+def augmented_resample_sampled(lw: np.ndarray, M: int, seed: int, n: int, outputs: np.ndarray) -> dict:
+    lw = np.ascontiguousarray(lw, dtype=np.float64)
+    N = lw.shape[0]
+    m = N // M
+    S = int(round(np.log2(m)))
+    outs = np.ascontiguousarray(outputs, dtype=np.int64)
+    k = outs.shape[0]
+    path = np.zeros((k, S), np.int64)
+    anc = np.zeros((k, S), np.int64)
+    pdelta = np.zeros((k, S), np.float32)
+    logV = np.zeros(m - 1, np.float64)
+    A = np.zeros(k, np.int64)
+    rc = lib().orc_augmented_resample_sampled(N, M, seed, n, _ptr(lw), k, _ptr(outs), _ptr(path),
+                                              _ptr(anc), _ptr(pdelta), _ptr(logV), _ptr(A))
+    if rc != 0:
+        raise ValueError(f"orc_augmented_resample_sampled rc={rc}")
+    return dict(path=path, anc=anc, delta=pdelta, logV=logV, A=A, S=S, m=m)
+
+
+def level_offset(m: int, s: int) -> int:
+    """Offset of level s (1..S) in the logV table: level s has m/2^s entries."""
+    return m - (m >> (s - 1))
+
+
+def estimates(d: int, lw: np.ndarray, x: np.ndarray, A: Optional[np.ndarray]) -> dict:
+    lw = np.ascontiguousarray(lw, dtype=np.float64)
+    xx = np.ascontiguousarray(x, dtype=np.float64)
+    AA = None if A is None else np.ascontiguousarray(A, dtype=np.int64)
+    f = np.zeros(2 * d)
+    p = np.zeros(2 * d)
+    r = np.zeros(2 * d)
+    lib().orc_estimates(d, lw.shape[0], _ptr(lw), _ptr(xx), _ptr(AA), _ptr(f), _ptr(p), _ptr(r))
+    return dict(filter=f, predict=p, resampled=r if A is not None else None)
+
+
+def step(params: dict, N: int, M: int, seed: int, n: int, y: np.ndarray, xin: np.ndarray,
+         tables: bool = True) -> dict:
+    """One time step from xin (fp32 xhat_{n-1}, or x_0 when n == 0).
+    tables=False skips the per-stage ancestor / delta tables (same draws)."""
+    mdl = make_model(params)
+    d = mdl.d
+    m = N // M
+    S = int(round(np.log2(m)))
+    xin = np.ascontiguousarray(xin, dtype=np.float32).reshape(N, d)
+    yy = np.ascontiguousarray(y, dtype=np.float32)
+    out = dict(x=np.zeros((N, d)), lw=np.zeros(N), a=np.zeros((S, N), np.int32) if tables else None,
+               delta=np.zeros((S, N), np.float32) if tables else None, logV=np.zeros(m - 1), A=np.zeros(N, np.int64),
+               xhat=np.zeros((N, d)), filter=np.zeros(2 * d), predict=np.zeros(2 * d),
+               resampled=np.zeros(2 * d))
+    rc = lib().orc_step(ctypes.byref(mdl), N, M, seed, n, _ptr(yy), _ptr(xin), _ptr(out["x"]),
+                        _ptr(out["lw"]), _ptr(out["a"]), _ptr(out["delta"]), _ptr(out["logV"]),
+                        _ptr(out["A"]), _ptr(out["xhat"]), _ptr(out["filter"]), _ptr(out["predict"]),
+                        _ptr(out["resampled"]))
+    if rc != 0:
+        raise ValueError(f"orc_step rc={rc}")
+    out["S"], out["m"] = S, m
+    return out
+
+
+def run_filter(params: dict, M: int, m: int, seed: int, ys: np.ndarray, x0: Optional[np.ndarray] = None):
+    """Alg. 1 with Alg. 3 for len(ys) steps; returns the per-step filter means (T x d).
+    State is kept in fp32 between steps, as in the configurations (fp32 particles)."""
+    N = M * m
+    d = int(params["d"])
+    x = (init(params, N, seed) if x0 is None else x0).astype(np.float32)
+    means = np.zeros((len(ys), d))
+    for n, y in enumerate(ys):
+        r = step(params, N, M, seed, n, y, x, tables=False)
+        means[n] = r["filter"][:d]
+        x = r["xhat"].astype(np.float32)
+    return means

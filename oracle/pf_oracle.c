@@ -1,0 +1,477 @@
+/*
+ * pf_oracle.c -- plain, slow, fp64 CPU oracle for ONE bootstrap-particle-filter
+ * time step with augmented resampling (arXiv 1812.01502, Heine, Whiteley, Cemgil).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code,
+ * header, table or constant generator with the CUDA path (paper_1812_01502_b200/
+ * csrc); it re-implements the Philox4x32-10 generator independently from its
+ * published definition (Salmon et al., SC'11) and the draw contract of
+ * DESIGN.md §3.
+ *
+ * Every function cites the passage of PAPER.md it follows.  Everything is fp64
+ * except the input particle states and model constants, which the method's
+ * configurations fix as fp32 values (BASELINE.json configs: "fp32 particles");
+ * they are widened to fp64 on entry.
+ *
+ * Pins (what checks this file against something other than itself) are listed in
+ * DESIGN.md §6; every function here has at least one.
+ *
+ * Step, in the paper's order (Alg. 1 with Alg. 3 as RESAMPLE):
+ *   1. mutation   zeta_{n}^i ~ f(zhat_{n-1}^i, .)         (Alg. 1 l.302-303; skipped at n=0)
+ *   2. weighting  V_0^i = g_n(xi_0^i)  (log domain)        (Alg. 3 l.343-344)
+ *   3. for s = 1..S:  V_s = A_s V_{s-1};  xi_s^i ~ (V_s^i)^-1 sum_j A_s^ij V_{s-1}^j delta_{xi_{s-1}^j}
+ *                                                          (Alg. 3 l.346-349; eq. A matrices 357-360)
+ *   4. composition A(i) = a_1(a_2(...a_S(i))), xhat^i = x^{A(i)}  (xi_s^i = xi_{s-1}^{a_s(i)})
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_OK 0
+#define ORC_EINVAL (-1)
+#define ORC_ENOMEM (-2)
+
+/* RNG domains (draw contract). */
+#define ORC_DOMAIN_INIT 1u
+#define ORC_DOMAIN_MUTATE 2u
+#define ORC_DOMAIN_RESAMPLE 3u
+
+/* ------------------------------------------------------------------------- */
+/* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11, "Parallel random numbers:
+ * as easy as 1, 2, 3"): 10 rounds of
+ *   (hi0,lo0) = M0*c0, (hi1,lo1) = M1*c2,
+ *   c' = (hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0),
+ * with the key bumped by the Weyl constants (W0, W1) before every round but the
+ * first.  Pinned against cuRAND's curand_Philox4x32_10 (tests/test_philox.py). */
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4])
+{
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) {
+            k0 += W0;
+            k1 += W1;
+        }
+        uint64_t p0 = (uint64_t)M0 * (uint64_t)c0;
+        uint64_t p1 = (uint64_t)M1 * (uint64_t)c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* One 32-bit word of the draw contract: block counter (c0, n, domain<<24 | sub, 0),
+ * key (seed lo, seed hi), word w in 0..3. */
+static uint32_t rng_word(uint64_t seed, uint32_t c0, uint32_t n, uint32_t domain,
+                         uint32_t sub, int w)
+{
+    uint32_t ctr[4] = {c0, n, (domain << 24) | sub, 0u};
+    uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    uint32_t out[4];
+    orc_philox4x32_10(ctr, key, out);
+    return out[w];
+}
+
+/* u in [0,1): 24 high bits, exact in fp32 and fp64. */
+static double u01(uint32_t r) { return (double)(r >> 8) * 0x1p-24; }
+/* u in (0,1]: used for the Box-Muller radius so log(u) is finite. */
+static double u01_open0(uint32_t r) { return ((double)(r >> 8) + 1.0) * 0x1p-24; }
+
+/* Standard normal for flat coordinate c of the (domain, n) noise field.
+ * Block c/4 gives words (w0,w1,w2,w3); Box-Muller on (w0,w1) gives coordinates
+ * 4j, 4j+1 (cos, sin) and on (w2,w3) coordinates 4j+2, 4j+3. */
+double orc_normal(uint64_t seed, uint32_t domain, uint32_t n, uint64_t c)
+{
+    uint32_t ctr[4] = {(uint32_t)(c >> 2), n, domain << 24, 0u};
+    uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    uint32_t out[4];
+    orc_philox4x32_10(ctr, key, out);
+    int w = (int)(c & 3u);
+    int pair = w >> 1;
+    double radius = sqrt(-2.0 * log(u01_open0(out[2 * pair])));
+    double theta = 2.0 * M_PI * u01(out[2 * pair + 1]);
+    return (w & 1) ? radius * sin(theta) : radius * cos(theta);
+}
+
+/* ------------------------------------------------------------------------- */
+/* The HMM of eq. HMM for the two model families of
+ * BASELINE.json: linear-Gaussian (LG) and stochastic volatility (SV). */
+typedef struct {
+    int kind; /* 1 = LG, 2 = SV */
+    int d, dy;
+    float A[64], LQ[64], H[64], Rinv[64], m0[8], L0[64]; /* row-major */
+    float sv_phi, sv_sigma, sv_beta, sv_m0, sv_s0;
+} orc_model;
+
+/* Alg. 1 l.296-298: zeta_0^i iid pi_0.  LG: m0 + L0 z; SV: m0 + s0 z. */
+void orc_init(const orc_model* mdl, uint64_t N, uint64_t seed, double* x0)
+{
+    int d = mdl->d;
+    for (uint64_t i = 0; i < N; ++i) {
+        double z[8];
+        for (int k = 0; k < d; ++k)
+            z[k] = orc_normal(seed, ORC_DOMAIN_INIT, 0u, i * (uint64_t)d + (uint64_t)k);
+        for (int k = 0; k < d; ++k) {
+            double v;
+            if (mdl->kind == 2) {
+                v = (double)mdl->sv_m0 + (double)mdl->sv_s0 * z[k];
+            } else {
+                v = (double)mdl->m0[k];
+                for (int j = 0; j < d; ++j) v += (double)mdl->L0[k * d + j] * z[j];
+            }
+            x0[i * d + k] = v;
+        }
+    }
+}
+
+/* Alg. 1 l.302-303: zeta_n^i ~ f(zhat_{n-1}^i, .).
+ * LG: x = A xhat + LQ z;  SV: x = phi xhat + sigma z.  z from the MUTATE field at n. */
+void orc_mutate(const orc_model* mdl, uint64_t N, uint64_t seed, uint32_t n,
+                const double* xhat, double* x)
+{
+    int d = mdl->d;
+    for (uint64_t i = 0; i < N; ++i) {
+        double z[8];
+        for (int k = 0; k < d; ++k)
+            z[k] = orc_normal(seed, ORC_DOMAIN_MUTATE, n, i * (uint64_t)d + (uint64_t)k);
+        for (int k = 0; k < d; ++k) {
+            double v;
+            if (mdl->kind == 2) {
+                v = (double)mdl->sv_phi * xhat[i] + (double)mdl->sv_sigma * z[0];
+            } else {
+                v = 0.0;
+                for (int j = 0; j < d; ++j) v += (double)mdl->A[k * d + j] * xhat[i * d + j];
+                for (int j = 0; j < d; ++j) v += (double)mdl->LQ[k * d + j] * z[j];
+            }
+            x[i * d + k] = v;
+        }
+    }
+}
+
+/* g_n(x) = g(x, y_n), in the log domain with normalising constants
+ * dropped (reading R9).
+ * LG: log g = -1/2 (y - Hx)^T Rinv (y - Hx).
+ * SV: y | x ~ N(0, beta^2 e^x)  =>  log g = -x/2 - y^2 e^{-x} / (2 beta^2).
+ * A non-finite result (non-finite x) is -inf. */
+void orc_logweight(const orc_model* mdl, uint64_t N, const float* y, const double* x,
+                   double* lw)
+{
+    int d = mdl->d, dy = mdl->dy;
+    for (uint64_t i = 0; i < N; ++i) {
+        double v;
+        if (mdl->kind == 2) {
+            double xv = x[i];
+            double yv = (double)y[0];
+            double beta = (double)mdl->sv_beta;
+            v = -0.5 * xv - yv * yv * exp(-xv) / (2.0 * beta * beta);
+        } else {
+            double r[8];
+            for (int k = 0; k < dy; ++k) {
+                double hx = 0.0;
+                for (int j = 0; j < d; ++j) hx += (double)mdl->H[k * d + j] * x[i * d + j];
+                r[k] = (double)y[k] - hx;
+            }
+            double q = 0.0;
+            for (int k = 0; k < dy; ++k)
+                for (int j = 0; j < dy; ++j) q += r[k] * (double)mdl->Rinv[k * dy + j] * r[j];
+            v = -0.5 * q;
+        }
+        lw[i] = isfinite(v) ? v : -INFINITY;
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* Augmented resampling, Alg. 3 with A_s of eq. A matrices
+ * (PAPER.md:357-360).  Groups are 0-based; group g holds particles g*M..g*M+M-1.
+ *
+ * By Lemma `facts about A`, at stage s group g interacts with
+ * exactly one other group, h = g XOR 2^{s-1}; block (g,h) of A_s is (1/2M) 1.
+ * By eq. V_defn_proofs, V_s^i = (1/2M) sum over the pair's 2M
+ * particles of V_{s-1}^j, so V_s is constant over blocks of 2^s groups; we store
+ * it per block:  logV[off(s) + b], b = g >> s, off(s) = m - m/2^{s-1}.
+ *
+ * Draw law: P(xi_s^i = xi_{s-1}^j) = A_s^ij V_{s-1}^j / V_s^i.
+ *   s = 1: the 2M pool (lower group first) with weights g(xi_0^j): inverse CDF,
+ *          u = U(RESAMPLE, n, s=1, i); a_1(i) = base + #{k < 2M-1 : C_k <= u C_{2M-1}}
+ *          (readings R1-R4).
+ *   s >= 2: V_{s-1} is constant over each of the two groups, so the law is
+ *          "side L w.p. p = V_L/(V_L+V_R), then uniform index": with M = 2^b and
+ *          r = RESAMPLE word, side = L iff (r >> b) < floor(p 2^{32-b}),
+ *          index = r & (M-1) (reading R1).
+ * RESAMPLE word for (s, i): word i%4 of block (i/4, n, RESAMPLE<<24 | s).
+ *
+ * Outputs (any may be NULL):
+ *   a[(s-1)*N + i]     = a_s(i), the stage-(s-1) position of the stage-s particle i;
+ *   delta[(s-1)*N + i] = distance of draw (s,i) to its nearest decision boundary in
+ *                        uniform units (stage 1: min_k |u - C_k/C_{2M-1}|;
+ *                        s >= 2: |p - ((r>>b)+1)/2^{32-b}|);
+ *   logV[m-1]          = all levels s = 1..S (see off(s));
+ *   A[N]               = composed ancestor A(i) = a_1(a_2(...a_S(i))).
+ */
+static int ilog2_exact(uint64_t v)
+{
+    if (v == 0 || (v & (v - 1)) != 0) return -1;
+    int k = 0;
+    while ((1ull << k) < v) ++k;
+    return k;
+}
+
+static uint64_t level_offset(uint64_t m, int s) { return m - (m >> (s - 1)); }
+
+/* log((e^a + e^b)/2): the pair average of eq. V_defn_proofs in the log domain. */
+static double log_pair_mean(double a, double b)
+{
+    double c = a > b ? a : b;
+    if (c == -INFINITY) return -INFINITY;
+    return c + log((exp(a - c) + exp(b - c)) / 2.0);
+}
+
+/* Stage-1 draw for output i of the pool starting at `base` (2M entries, CDF C). */
+static void stage1_draw(uint64_t M, uint64_t seed, uint32_t n, uint64_t base, const double* C,
+                        uint64_t i, int64_t* a_out, double* delta_out)
+{
+    uint64_t twoM = 2 * M;
+    double u = u01(rng_word(seed, (uint32_t)(i >> 2), n, ORC_DOMAIN_RESAMPLE, 1u, (int)(i & 3u)));
+    double total = C[twoM - 1];
+    double t = u * total;
+    uint64_t k = 0;
+    for (uint64_t kk = 0; kk + 1 < twoM; ++kk)
+        if (C[kk] <= t) ++k;
+    *a_out = (int64_t)(base + k);
+    if (delta_out) {
+        double dmin = INFINITY;
+        for (uint64_t kk = 0; kk + 1 < twoM; ++kk) {
+            double dd = fabs(u - C[kk] / total);
+            if (dd < dmin) dmin = dd;
+        }
+        *delta_out = dmin;
+    }
+}
+
+/* Stage-s (s >= 2) draw for output i, given the level-(s-1) table. */
+static void stage_s_draw(uint64_t M, int b, int s, uint64_t seed, uint32_t n, const double* lv_prev,
+                         uint64_t i, int64_t* a_out, double* delta_out)
+{
+    uint64_t g = i / M;
+    uint64_t h = g ^ (1ull << (s - 1));
+    uint64_t gl = g < h ? g : h, gr = g < h ? h : g;
+    double vl = lv_prev[gl >> (s - 1)], vr = lv_prev[gr >> (s - 1)];
+    /* p = V_L / (V_L + V_R) */
+    double p = 1.0 / (1.0 + exp(vr - vl));
+    if (vl == -INFINITY && vr == -INFINITY) p = 0.5; /* both zero: undefined; never happens for g > 0 */
+    double scale = ldexp(1.0, 32 - b);
+    uint64_t P = (uint64_t)floor(p * scale);
+    uint32_t r = rng_word(seed, (uint32_t)(i >> 2), n, ORC_DOMAIN_RESAMPLE, (uint32_t)s, (int)(i & 3u));
+    uint64_t hi = (uint64_t)(r >> b);
+    uint64_t idx = (uint64_t)r & (M - 1);
+    uint64_t chosen = (hi < P) ? gl : gr;
+    *a_out = (int64_t)(chosen * M + idx);
+    if (delta_out) *delta_out = fabs(p - (double)(hi + 1) / scale);
+}
+
+/* Stage-1 CDF of the pair starting at base: C_k = sum_{j<=k} exp(lw_j - mx),
+ * sequential.  Returns mx. */
+static double pair_cdf(const double* lw, uint64_t base, uint64_t twoM, double* C)
+{
+    double mx = -INFINITY;
+    for (uint64_t j = 0; j < twoM; ++j)
+        if (lw[base + j] > mx) mx = lw[base + j];
+    double acc = 0.0;
+    for (uint64_t j = 0; j < twoM; ++j) {
+        acc += (mx == -INFINITY) ? 1.0 : exp(lw[base + j] - mx);
+        C[j] = acc;
+    }
+    return mx;
+}
+
+int orc_augmented_resample(uint64_t N, uint64_t M, uint64_t seed, uint32_t n, const double* lw,
+                           int32_t* a, float* delta, double* logV, int64_t* A)
+{
+    if (M == 0 || N % M != 0) return ORC_EINVAL;
+    uint64_t m = N / M;
+    int S = ilog2_exact(m);
+    int b = ilog2_exact(M);
+    if (S < 1 || b < 0) return ORC_EINVAL;
+    uint64_t twoM = 2 * M;
+    double* lv = (double*)malloc(sizeof(double) * (m - 1));
+    double* C = (double*)malloc(sizeof(double) * twoM);
+    int32_t* as = (int32_t*)malloc(sizeof(int32_t) * N * (uint64_t)S);
+    if (!lv || !C || !as) {
+        free(lv); free(C); free(as);
+        return ORC_ENOMEM;
+    }
+
+    /* Stage s = 1 (Alg. 3 l.346-349 with A_1: pairs (2p, 2p+1)). */
+    for (uint64_t p = 0; p < m / 2; ++p) {
+        uint64_t base = 2 * p * M;
+        double mx = pair_cdf(lw, base, twoM, C);
+        /* V_1 = (1/2M) sum_pool g  (eq. V_defn_proofs) */
+        lv[level_offset(m, 1) + p] = (mx == -INFINITY) ? -INFINITY : mx + log(C[twoM - 1]) - log((double)twoM);
+        for (uint64_t j = 0; j < twoM; ++j) {
+            uint64_t i = base + j;
+            int64_t ai;
+            double dl;
+            stage1_draw(M, seed, n, base, C, i, &ai, &dl);
+            as[i] = (int32_t)ai;
+            if (delta) delta[i] = (float)dl;
+        }
+    }
+    /* Stages s = 2..S (Alg. 3 l.346-349). */
+    for (int s = 2; s <= S; ++s) {
+        const double* prev = lv + level_offset(m, s - 1);
+        double* cur = lv + level_offset(m, s);
+        /* V_s = A_s V_{s-1}: block b of level s is the pair mean of blocks 2b, 2b+1. */
+        for (uint64_t bk = 0; bk < (m >> s); ++bk) cur[bk] = log_pair_mean(prev[2 * bk], prev[2 * bk + 1]);
+        for (uint64_t i = 0; i < N; ++i) {
+            int64_t ai;
+            double dl;
+            stage_s_draw(M, b, s, seed, n, prev, i, &ai, &dl);
+            as[(uint64_t)(s - 1) * N + i] = (int32_t)ai;
+            if (delta) delta[(uint64_t)(s - 1) * N + i] = (float)dl;
+        }
+    }
+    /* Composition: xi_S^i = xi_0^{a_1(a_2(...a_S(i)))}. */
+    if (A) {
+        for (uint64_t i = 0; i < N; ++i) {
+            uint64_t j = i;
+            for (int s = S; s >= 1; --s) j = (uint64_t)as[(uint64_t)(s - 1) * N + j];
+            A[i] = (int64_t)j;
+        }
+    }
+    if (a) memcpy(a, as, sizeof(int32_t) * N * (uint64_t)S);
+    if (logV) memcpy(logV, lv, sizeof(double) * (m - 1));
+    free(lv); free(C); free(as);
+    return ORC_OK;
+}
+
+/* Same draws, evaluated only along the ancestral paths of `nsamp` sampled outputs
+ * (for full-size configurations where S x N tables do not fit).  The V tables are
+ * computed in full, exactly as above.  For each sample k and stage s:
+ *   path[k*S + (s-1)]  = the stage-s position on the path (path[k*S+S-1] = output),
+ *   anc[k*S + (s-1)]   = a_s(path position),  pdelta likewise;  A_out[k] = A(output). */
+int orc_augmented_resample_sampled(uint64_t N, uint64_t M, uint64_t seed, uint32_t n,
+                                   const double* lw, uint64_t nsamp, const int64_t* outputs,
+                                   int64_t* path, int64_t* anc, float* pdelta, double* logV,
+                                   int64_t* A_out)
+{
+    if (M == 0 || N % M != 0) return ORC_EINVAL;
+    uint64_t m = N / M;
+    int S = ilog2_exact(m);
+    int b = ilog2_exact(M);
+    if (S < 1 || b < 0) return ORC_EINVAL;
+    uint64_t twoM = 2 * M;
+    double* lv = (double*)malloc(sizeof(double) * (m - 1));
+    double* C = (double*)malloc(sizeof(double) * twoM);
+    if (!lv || !C) {
+        free(lv); free(C);
+        return ORC_ENOMEM;
+    }
+    for (uint64_t p = 0; p < m / 2; ++p) {
+        double mx = pair_cdf(lw, 2 * p * M, twoM, C);
+        lv[level_offset(m, 1) + p] = (mx == -INFINITY) ? -INFINITY : mx + log(C[twoM - 1]) - log((double)twoM);
+    }
+    for (int s = 2; s <= S; ++s) {
+        const double* prev = lv + level_offset(m, s - 1);
+        double* cur = lv + level_offset(m, s);
+        for (uint64_t bk = 0; bk < (m >> s); ++bk) cur[bk] = log_pair_mean(prev[2 * bk], prev[2 * bk + 1]);
+    }
+    for (uint64_t k = 0; k < nsamp; ++k) {
+        uint64_t j = (uint64_t)outputs[k];
+        for (int s = S; s >= 1; --s) {
+            int64_t aj;
+            double dl;
+            if (s >= 2) {
+                stage_s_draw(M, b, s, seed, n, lv + level_offset(m, s - 1), j, &aj, &dl);
+            } else {
+                uint64_t base = (j / twoM) * twoM;
+                pair_cdf(lw, base, twoM, C);
+                stage1_draw(M, seed, n, base, C, j, &aj, &dl);
+            }
+            if (path) path[k * S + (uint64_t)(s - 1)] = (int64_t)j;
+            if (anc) anc[k * S + (uint64_t)(s - 1)] = aj;
+            if (pdelta) pdelta[k * S + (uint64_t)(s - 1)] = (float)dl;
+            j = (uint64_t)aj;
+        }
+        if (A_out) A_out[k] = (int64_t)j;
+    }
+    if (logV) memcpy(logV, lv, sizeof(double) * (m - 1));
+    free(lv); free(C);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Estimates of one step (reading R8):
+ *   filter   pi_hat_n(phi) = sum_i g_n(x^i) phi(x^i) / sum_i g_n(x^i)
+ *   predict  pi_n^N(phi)   = N^-1 sum_i phi(x^i)
+ *   resampled N^-1 sum_i phi(xhat^i)
+ * for phi = x_k (out[0..d)) and phi = x_k^2 (out[d..2d)), sequential fp64 sums. */
+void orc_estimates(int d, uint64_t N, const double* lw, const double* x, const int64_t* A,
+                   double* filt, double* pred, double* resamp)
+{
+    double L = -INFINITY;
+    for (uint64_t i = 0; i < N; ++i)
+        if (lw[i] > L) L = lw[i];
+    double sw = 0.0;
+    double s1[8] = {0}, s2[8] = {0}, p1[8] = {0}, p2[8] = {0}, r1[8] = {0}, r2[8] = {0};
+    for (uint64_t i = 0; i < N; ++i) {
+        double w = exp(lw[i] - L);
+        sw += w;
+        for (int k = 0; k < d; ++k) {
+            double v = x[i * d + k];
+            s1[k] += w * v;
+            s2[k] += w * v * v;
+            p1[k] += v;
+            p2[k] += v * v;
+            if (A) {
+                double vr = x[(uint64_t)A[i] * d + k];
+                r1[k] += vr;
+                r2[k] += vr * vr;
+            }
+        }
+    }
+    for (int k = 0; k < d; ++k) {
+        if (filt) { filt[k] = s1[k] / sw; filt[d + k] = s2[k] / sw; }
+        if (pred) { pred[k] = p1[k] / (double)N; pred[d + k] = p2[k] / (double)N; }
+        if (resamp && A) { resamp[k] = r1[k] / (double)N; resamp[d + k] = r2[k] / (double)N; }
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* A whole step of Alg. 1 deploying Alg. 3, from a given xhat_{n-1} (or x_0 when
+ * n == 0, when no mutation happens: DESIGN.md reading R7).  Outputs x (N*d), lw,
+ * per-stage tables, estimates, and xhat_n (N*d).  Returns an ORC_* code. */
+int orc_step(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t seed, uint32_t n,
+             const float* y, const float* xin, double* x, double* lw, int32_t* a, float* delta,
+             double* logV, int64_t* A, double* xhat_out, double* filt, double* pred, double* resamp)
+{
+    int d = mdl->d;
+    double* xprev = (double*)malloc(sizeof(double) * N * (uint64_t)d);
+    int64_t* Aloc = (int64_t*)malloc(sizeof(int64_t) * N);
+    if (!xprev || !Aloc) {
+        free(xprev); free(Aloc);
+        return ORC_ENOMEM;
+    }
+    for (uint64_t i = 0; i < N * (uint64_t)d; ++i) xprev[i] = (double)xin[i];
+    if (n == 0) memcpy(x, xprev, sizeof(double) * N * (uint64_t)d);
+    else orc_mutate(mdl, N, seed, n, xprev, x);
+    orc_logweight(mdl, N, y, x, lw);
+    int rc = orc_augmented_resample(N, M, seed, n, lw, a, delta, logV, Aloc);
+    if (rc == ORC_OK) {
+        if (A) memcpy(A, Aloc, sizeof(int64_t) * N);
+        if (xhat_out)
+            for (uint64_t i = 0; i < N; ++i)
+                for (int k = 0; k < d; ++k) xhat_out[i * d + k] = x[(uint64_t)Aloc[i] * d + k];
+        orc_estimates(d, N, lw, x, Aloc, filt, pred, resamp);
+    }
+    free(xprev); free(Aloc);
+    return rc;
+}
