@@ -1,0 +1,144 @@
+/*
+ * pf.h -- C-ABI of the B200-native bootstrap particle filter step with augmented
+ * resampling (arXiv 1812.01502, Heine, Whiteley and Cemgil).
+ *
+ * The method (PAPER.md line numbers; DESIGN.md §1-§3 for the readings):
+ *   - HMM  X_0 ~ pi_0, X_n | X_{n-1} ~ f, Y_n | X_n ~ g            (eq. HMM)
+ *   - Alg. 1 (BPF): mutate, then RESAMPLE with potentials g_n(.) = g(., y_n)
+ *
+ *   - Alg. 3 (augmented resampling) with A_s of eq. `A matrices`: N = m M particles in
+ *     m = 2^S groups of M; at stage s = 1..S group g is paired with g XOR 2^{s-1}
+ *     and each particle redraws its ancestor from the pair's 2M particles with
+ *     probability A_s^{ij} V_{s-1}^j / V_s^i
+ *
+ * One pf_step(y_n) = [mutate x_hat_{n-1} -> x_n (n >= 1)] + weight g_n + S butterfly
+ * stages + composition of the stage ancestors, leaving x_hat_n on the device.
+ *
+ * Conventions (all calls):
+ *   - Return value: PF_OK (0) or a negative PF_E* code; pf_last_error() describes it.
+ *     No C++ exception crosses this ABI.
+ *   - "host" pointers are read (or written) before the call returns; "device"
+ *     pointers must stay valid until the work enqueued on the handle's stream is done.
+ *   - The library never allocates device memory: the caller passes one device
+ *     workspace of pf_workspace_bytes() bytes (256-byte aligned), and a CUDA stream.
+ *   - Determinism: the same (model, N, M, seed, flags, y_0..y_n) give bitwise
+ *     identical results (counter-based RNG, fixed reduction trees).
+ */
+#ifndef PF_H_
+#define PF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define PF_OK 0
+#define PF_EINVAL (-1)     /* bad topology / model / argument */
+#define PF_EWORKSPACE (-2) /* workspace too small or misaligned */
+#define PF_ECUDA (-3)      /* a CUDA runtime error (message in pf_last_error) */
+#define PF_EOBS (-4)       /* non-finite observation */
+#define PF_ESTATE (-5)     /* call not valid in the current state (e.g. no step yet) */
+
+/* model kinds */
+#define PF_LG 1 /* x_n = A x_{n-1} + LQ z,  y_n = H x_n + N(0, R),  x_0 = m0 + L0 z */
+#define PF_SV 2 /* x_n = phi x_{n-1} + sigma z, y_n = beta exp(x_n/2) N(0,1), x_0 = sv_m0 + sv_s0 z */
+
+/* Model description (HOST pointers, copied by pf_init; the caller keeps ownership).
+ * All matrices row-major fp32: A, LQ, L0 are d x d (LQ, L0 lower Cholesky factors of
+ * Q and P0), H is dy x d, Rinv is dy x dy (R^{-1}), m0 has d entries.  d, dy in 1..8.
+ * PF_SV uses only the sv_* scalars (d = dy = 1).  The oracle widens the same fp32
+ * values to fp64. */
+typedef struct pf_model {
+    int kind;
+    int d, dy;
+    const float *A, *LQ, *H, *Rinv, *m0, *L0;
+    float sv_phi, sv_sigma, sv_beta, sv_m0, sv_s0;
+} pf_model;
+
+typedef struct pf_handle pf_handle;
+
+/* pf_init flags */
+#define PF_FLAG_DEBUG 1u /* keep x_n, log-weights and every stage's ancestor table
+                            (S x N int32) for pf_debug_get; test-only, costs HBM */
+
+/* Bytes of device workspace pf_init needs for this problem (0 if invalid). */
+size_t pf_workspace_bytes(const pf_model* model, uint64_t N, uint32_t M, uint32_t flags);
+
+/* Validate and set up one filter on the current CUDA device, and enqueue the draw of
+ * x_0^i ~ pi_0 (Alg. 1 l.1-3) on `cuda_stream` (a cudaStream_t; NULL
+ * = legacy default stream).
+ * Topology (Assumption A1; reading R5): m = N/M must be an
+ * integer power of two with m >= 2 (S = log2 m >= 1); M must be a power of two in
+ * [2, 8192] and a stage-1 pool of 2M particles must fit one SM's shared memory
+ * (2M (4d + 5) bytes <= 227 KB: M <= 8192 for d = 1, M <= 4096 for d = 4);
+ * N < 2^31; d in {1, 2, 4, 8}.  Errors: PF_EINVAL, PF_EWORKSPACE, PF_ECUDA.
+ * dev_ws: DEVICE pointer, >= pf_workspace_bytes(), 256-byte aligned, owned by the
+ * caller and not touched by anyone else until pf_destroy. */
+int pf_init(const pf_model* model, uint64_t N, uint32_t M, uint64_t seed, uint32_t flags,
+            void* dev_ws, size_t ws_bytes, void* cuda_stream, pf_handle** out);
+
+/* Enqueue one time step n (n = 0, 1, 2, ... counted by the handle) with observation
+ * y_n (HOST pointer, dy floats, copied into the launch parameters before return).
+ * n = 0 weights and resamples x_0 (no mutation); n >= 1 first mutates x_hat_{n-1}
+ * (reading R7).  Asynchronous.  Errors: PF_EOBS (non-finite y), PF_ECUDA. */
+int pf_step(pf_handle* h, const float* y_host);
+
+/* Same as pf_step with y_n read by the kernels from DEVICE memory (dy floats), so a
+ * caller can keep the whole observation sequence resident in HBM.  Non-finite
+ * device observations are not detected. */
+int pf_step_dev(pf_handle* h, const float* y_dev);
+
+/* estimates (phi) */
+#define PF_PHI_X 1  /* phi(x) = x_k, k = 0..d-1 */
+#define PF_PHI_X2 2 /* phi(x) = x_k^2 */
+/* estimate kinds (reading R8) */
+#define PF_EST_FILTER 1  /* sum_i g_n(x^i) phi(x^i) / sum_i g_n(x^i): pi_hat_n */
+#define PF_EST_PREDICT 2 /* N^-1 sum_i phi(x^i): pi_n^N */
+
+/* Synchronise the handle's stream and write the d estimates of the last completed
+ * step into out (HOST, d doubles).  Errors: PF_ESTATE before the first step,
+ * PF_EINVAL, PF_ECUDA. */
+int pf_estimate(pf_handle* h, int phi, int kind, double* out);
+
+/* Release the handle (not the workspace, not the stream). NULL is a no-op. */
+void pf_destroy(pf_handle* h);
+
+/* Human-readable description of the last error on h (or of the last failed pf_init
+ * when h is NULL).  Valid until the next call on h. */
+const char* pf_last_error(const pf_handle* h);
+
+/* --- debug / test exports (parity harness) ------------------------------------ */
+#define PF_DBG_X 1         /* x_n before resampling, N x d fp32 (needs PF_FLAG_DEBUG) */
+#define PF_DBG_LOGW 2      /* log g_n(x_n^i), N fp32 (needs PF_FLAG_DEBUG) */
+#define PF_DBG_ANC_STAGE 3 /* a_s(i), N int32, stage = s in 1..S (needs PF_FLAG_DEBUG) */
+#define PF_DBG_ANC_FINAL 4 /* A(i) = a_1(...a_S(i)), N int32 (needs PF_FLAG_DEBUG) */
+#define PF_DBG_XHAT 5      /* x_hat_n = x_n[A(i)], N x d fp32 */
+#define PF_DBG_LOGV 6      /* log V_s per block, all levels s = 1..S, m-1 fp64
+                              (level s at offset m - m/2^{s-1}, m/2^s entries) */
+#define PF_DBG_THRESH 7    /* stage s >= 2 side thresholds floor(p 2^{32-b}), m-1 uint32,
+                              same layout (stage s at offset m - m/2^{s-1}); entry 0.. of
+                              level 1 unused */
+
+/* Copy one debug table of the last completed step to HOST memory (bytes = capacity of
+ * host_out).  Synchronises.  Errors: PF_ESTATE (no step / not in debug mode), PF_EINVAL. */
+int pf_debug_get(pf_handle* h, int what, int stage, void* host_out, size_t bytes);
+
+/* DEVICE pointer of a debug table (same `what`/`stage`), for on-device sampling of
+ * large tables; valid until the next pf_step.  PF_DBG_XHAT is materialised on demand. */
+int pf_debug_ptr(pf_handle* h, int what, int stage, void** dev_out);
+
+/* Replace the filter state: the next pf_step is time step n and starts from
+ * x_hat_{n-1} = host_xhat (N x d fp32, HOST) -- or from x_0 = host_xhat when n = 0.
+ * Used by single-step parity tests with seeded synthetic particle clouds. */
+int pf_debug_set_state(pf_handle* h, const float* host_xhat, uint32_t n);
+
+/* Number of kernel launches the last pf_step enqueued (bench accounting). */
+int pf_last_step_launches(const pf_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PF_H_ */

@@ -1,0 +1,222 @@
+"""Thin Python binding of the C-ABI in include/pf.h (argument marshalling only).
+
+Every step of the filter runs in the CUDA kernels of libpf.so; there is no CPU or
+PyTorch fallback: importing this module without the built library raises.
+PyTorch is used only for device memory (the workspace tensor) and streams.
+
+The functions carry the C names (pf_init, pf_step, pf_step_dev, pf_estimate,
+pf_debug_get, pf_debug_set_state, ...); ParticleFilter wraps them for convenience.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpf.so")
+
+PF_OK, PF_EINVAL, PF_EWORKSPACE, PF_ECUDA, PF_EOBS, PF_ESTATE = 0, -1, -2, -3, -4, -5
+PF_LG, PF_SV = 1, 2
+PF_FLAG_DEBUG = 1
+PF_PHI_X, PF_PHI_X2 = 1, 2
+PF_EST_FILTER, PF_EST_PREDICT = 1, 2
+PF_DBG_X, PF_DBG_LOGW, PF_DBG_ANC_STAGE, PF_DBG_ANC_FINAL, PF_DBG_XHAT, PF_DBG_LOGV, PF_DBG_THRESH = 1, 2, 3, 4, 5, 6, 7
+
+
+class PFError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"pf error {code}: {msg}")
+        self.code = code
+
+
+class pf_model(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("d", ctypes.c_int), ("dy", ctypes.c_int),
+                ("A", ctypes.c_void_p), ("LQ", ctypes.c_void_p), ("H", ctypes.c_void_p),
+                ("Rinv", ctypes.c_void_p), ("m0", ctypes.c_void_p), ("L0", ctypes.c_void_p),
+                ("sv_phi", ctypes.c_float), ("sv_sigma", ctypes.c_float), ("sv_beta", ctypes.c_float),
+                ("sv_m0", ctypes.c_float), ("sv_s0", ctypes.c_float)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libpf.so; raises if it has not been built (no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with "
+                              "`python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, u64, u32, sz = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_size_t
+        L.pf_workspace_bytes.argtypes = [vp, u64, u32, u32]
+        L.pf_workspace_bytes.restype = sz
+        L.pf_init.argtypes = [vp, u64, u32, u64, u32, vp, sz, vp, ctypes.POINTER(vp)]
+        L.pf_step.argtypes = [vp, vp]
+        L.pf_step_dev.argtypes = [vp, vp]
+        L.pf_estimate.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp]
+        L.pf_destroy.argtypes = [vp]
+        L.pf_destroy.restype = None
+        L.pf_last_error.argtypes = [vp]
+        L.pf_last_error.restype = ctypes.c_char_p
+        L.pf_debug_get.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, sz]
+        L.pf_debug_ptr.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
+        L.pf_debug_set_state.argtypes = [vp, vp, u32]
+        L.pf_last_step_launches.argtypes = [vp]
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["pf_workspace_bytes", "pf_init", "pf_step", "pf_step_dev", "pf_estimate", "pf_destroy",
+            "pf_last_error", "pf_debug_get", "pf_debug_ptr", "pf_debug_set_state", "pf_last_step_launches"]
+
+
+def _check(rc: int, h=None):
+    if rc != PF_OK:
+        msg = lib().pf_last_error(h)
+        raise PFError(rc, msg.decode() if msg else "")
+
+
+def make_model(params: dict):
+    """pf_model from inputs.model_params(); returns (struct, keepalive arrays)."""
+    keep = []
+    m = pf_model()
+    m.kind = int(params["kind"])
+    m.d = int(params["d"])
+    m.dy = int(params["dy"])
+    if m.kind == PF_SV:
+        m.sv_phi, m.sv_sigma, m.sv_beta = float(params["phi"]), float(params["sigma"]), float(params["beta"])
+        m.sv_m0, m.sv_s0 = float(params["m0"]), float(params["s0"])
+    else:
+        for name in ("A", "LQ", "H", "Rinv", "m0", "L0"):
+            arr = np.ascontiguousarray(params[name], dtype=np.float32)
+            keep.append(arr)
+            setattr(m, name, arr.ctypes.data)
+    return m, keep
+
+
+def pf_workspace_bytes(params: dict, N: int, M: int, flags: int = 0) -> int:
+    m, keep = make_model(params)
+    return int(lib().pf_workspace_bytes(ctypes.byref(m), N, M, flags))
+
+
+def pf_init(params: dict, N: int, M: int, seed: int, flags: int, ws_ptr: int, ws_bytes: int, stream_ptr: int):
+    m, keep = make_model(params)
+    h = ctypes.c_void_p()
+    _check(lib().pf_init(ctypes.byref(m), N, M, seed, flags, ws_ptr, ws_bytes, stream_ptr, ctypes.byref(h)))
+    return h
+
+
+def pf_step(h, y: np.ndarray):
+    yy = np.ascontiguousarray(y, dtype=np.float32)
+    _check(lib().pf_step(h, yy.ctypes.data), h)
+
+
+def pf_step_dev(h, y_dev_ptr: int):
+    _check(lib().pf_step_dev(h, y_dev_ptr), h)
+
+
+def pf_estimate(h, d: int, phi: int = PF_PHI_X, kind: int = PF_EST_FILTER) -> np.ndarray:
+    out = np.zeros(d, np.float64)
+    _check(lib().pf_estimate(h, phi, kind, out.ctypes.data), h)
+    return out
+
+
+def pf_destroy(h):
+    lib().pf_destroy(h)
+
+
+def pf_debug_ptr(h, what: int, stage: int = 0) -> int:
+    p = ctypes.c_void_p()
+    _check(lib().pf_debug_ptr(h, what, stage, ctypes.byref(p)), h)
+    return int(p.value)
+
+
+def pf_debug_set_state(h, xhat: np.ndarray, n: int):
+    x = np.ascontiguousarray(xhat, dtype=np.float32)
+    _check(lib().pf_debug_set_state(h, x.ctypes.data, n), h)
+
+
+class ParticleFilter:
+    """One filter on one GPU: workspace in a torch uint8 tensor, work on a torch stream."""
+
+    def __init__(self, params: dict, N: int, M: int, seed: int, debug: bool = False, device: str = "cuda",
+                 stream=None):
+        import torch
+
+        self.torch = torch
+        self.params = params
+        self.N, self.M, self.seed = int(N), int(M), int(seed)
+        self.d = int(params["d"])
+        self.dy = int(params["dy"])
+        self.m = self.N // self.M
+        self.S = int(round(np.log2(self.m)))
+        self.flags = PF_FLAG_DEBUG if debug else 0
+        self.device = torch.device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        nbytes = pf_workspace_bytes(params, self.N, self.M, self.flags)
+        if nbytes == 0:
+            raise PFError(PF_EINVAL, "invalid model/topology (pf_workspace_bytes returned 0)")
+        self.ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        base = self.ws.data_ptr()
+        self._off = (-base) % 256
+        self.ws_ptr = base + self._off
+        self.ws_bytes = nbytes
+        self.h = pf_init(params, self.N, self.M, self.seed, self.flags, self.ws_ptr, nbytes, self.stream.cuda_stream)
+
+    def close(self):
+        if getattr(self, "h", None) is not None:
+            pf_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, y: np.ndarray):
+        pf_step(self.h, y)
+
+    def step_dev(self, y_dev):
+        """y_dev: a CUDA tensor (float32, dy entries, contiguous)."""
+        pf_step_dev(self.h, y_dev.data_ptr())
+
+    def estimate(self, phi: int = PF_PHI_X, kind: int = PF_EST_FILTER) -> np.ndarray:
+        return pf_estimate(self.h, self.d, phi, kind)
+
+    def launches(self) -> int:
+        return int(lib().pf_last_step_launches(self.h))
+
+    def debug_tensor(self, what: int, stage: int = 0):
+        """Device view (torch tensor into the workspace) of a debug table."""
+        torch = self.torch
+        ptr = pf_debug_ptr(self.h, what, stage)
+        off = ptr - self.ws.data_ptr()
+        if what in (PF_DBG_X, PF_DBG_XHAT):
+            n, dt, shape = self.N * self.d * 4, torch.float32, (self.N, self.d)
+        elif what == PF_DBG_LOGW:
+            n, dt, shape = self.N * 4, torch.float32, (self.N,)
+        elif what in (PF_DBG_ANC_STAGE, PF_DBG_ANC_FINAL):
+            n, dt, shape = self.N * 4, torch.int32, (self.N,)
+        elif what == PF_DBG_LOGV:
+            n, dt, shape = (self.m - 1) * 8, torch.float64, (self.m - 1,)
+        elif what == PF_DBG_THRESH:
+            n, dt, shape = (self.m - 1) * 4, torch.int32, (self.m - 1,)
+        else:
+            raise ValueError(what)
+        return self.ws[off: off + n].view(dt).view(shape)
+
+    def debug_get(self, what: int, stage: int = 0) -> np.ndarray:
+        t = self.debug_tensor(what, stage)
+        self.stream.synchronize()
+        out = t.cpu().numpy()
+        if what == PF_DBG_THRESH:
+            out = out.view(np.uint32)
+        return out
+
+    def set_state(self, xhat: np.ndarray, n: int):
+        pf_debug_set_state(self.h, np.asarray(xhat, np.float32).reshape(self.N, self.d), n)

@@ -1,0 +1,68 @@
+"""The C-ABI library loads without a GPU and exports every symbol include/pf.h declares;
+host-side validation (topology / model) works without a device."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1812_01502_b200 import inputs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def pfb():
+    from paper_1812_01502_b200 import build, pf
+    build.build()
+    return pf
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "pf.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pf_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(pfb):
+    names = _declared()
+    assert "pf_init" in names and "pf_step" in names and "pf_estimate" in names
+    L = pfb.lib()
+    for n in names:
+        assert hasattr(L, n), n
+    assert sorted(pfb.EXPORTED) == names
+
+
+@pytest.mark.parametrize("N,M,ok", [(1024, 64, True), (1 << 28, 64, True), (64, 64, False), (96, 32, False),
+                                    (1024, 1, False), (1024, 3, False), (1 << 14, 4096, True), (1 << 14, 8192, False), (1 << 14, 16384, False),
+                                    (4, 2, True), (1 << 31, 64, False)])
+def test_topology_validation(pfb, N, M, ok):
+    p = inputs.model_params(inputs.CONFIGS["C4"])
+    nbytes = pfb.pf_workspace_bytes(p, N, M)
+    assert (nbytes > 0) == ok
+
+
+def test_model_validation(pfb):
+    p = dict(inputs.model_params(inputs.CONFIGS["C4"]))
+    assert pfb.pf_workspace_bytes(p, 1 << 16, 64) > 0
+    bad = dict(p)
+    LQ = p["LQ"].copy()
+    LQ[0, 1] = 1.0  # not lower triangular
+    bad["LQ"] = LQ
+    assert pfb.pf_workspace_bytes(bad, 1 << 16, 64) == 0
+    bad = dict(p)
+    bad["d"] = 3
+    assert pfb.pf_workspace_bytes(bad, 1 << 16, 64) == 0
+    sv = inputs.model_params(inputs.CONFIGS["C3"])
+    assert pfb.pf_workspace_bytes(sv, 1 << 16, 32) > 0
+    assert pfb.pf_workspace_bytes(sv, 1 << 26, 8192) > 0  # C5's largest group (d = 1)
+
+
+def test_workspace_scales(pfb):
+    p = inputs.model_params(inputs.CONFIGS["C4"])
+    a = pfb.pf_workspace_bytes(p, 1 << 20, 64)
+    b = pfb.pf_workspace_bytes(p, 1 << 21, 64)
+    assert 1.9 < b / a < 2.1
+    dbg = pfb.pf_workspace_bytes(p, 1 << 20, 64, pfb.PF_FLAG_DEBUG)
+    assert dbg > a + (1 << 20) * 14 * 4

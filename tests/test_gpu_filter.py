@@ -1,0 +1,108 @@
+"""Whole-filter behaviour of the CUDA path through the public C-ABI (multi-step runs):
+statistical agreement with the exact Kalman posterior mean, determinism, pf_step vs
+pf_step_dev equivalence, error codes."""
+import numpy as np
+import pytest
+
+from paper_1812_01502_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+from oracle import kalman  # noqa: E402
+from paper_1812_01502_b200 import pf as pfb  # noqa: E402
+
+
+def _run(params, N, M, seed, ys, dev=False):
+    f = pfb.ParticleFilter(params, N, M, seed)
+    d = int(params["d"])
+    means = np.zeros((len(ys), d))
+    yd = torch.tensor(np.asarray(ys, np.float32), device="cuda")
+    for n, y in enumerate(ys):
+        if dev:
+            f.step_dev(yd[n])
+        else:
+            f.step(y)
+        means[n] = f.estimate(pfb.PF_PHI_X, pfb.PF_EST_FILTER)
+    xhat = f.debug_get(pfb.PF_DBG_XHAT)
+    f.close()
+    return means, xhat
+
+
+def test_c1_vs_kalman():
+    cfg = inputs.CONFIGS["C1"]
+    p = inputs.model_params(cfg)
+    _, ys = inputs.simulate(cfg)
+    km, _ = kalman.kalman_filter(p["A"], p["Q"], p["H"], p["R"], p["m0"], p["P0"], ys)
+    J = 32
+    runs = np.array([_run(p, cfg.N, cfg.M, 500 + j, ys)[0][:, 0] for j in range(J)])
+    mean = runs.mean(axis=0)
+    se = runs.std(axis=0, ddof=1) / np.sqrt(J)
+    z = (mean - km[:, 0]) / se
+    assert np.all(np.abs(z) < 5.0), z
+
+
+@pytest.mark.parametrize("name,N,M", [("C4", 1 << 20, 64), ("C2", 1 << 18, 256)])
+def test_lg_large_vs_kalman(name, N, M):
+    """A single large-N run: per-step filter-mean error below 6 x the posterior sd / sqrt(N/S)."""
+    cfg = inputs.CONFIGS[name]
+    p = inputs.model_params(cfg)
+    _, ys = inputs.simulate(cfg, T=20)
+    km, kc = kalman.kalman_filter(p["A"], p["Q"], p["H"], p["R"], p["m0"], p["P0"], ys)
+    means, _ = _run(p, N, M, 3, ys)
+    S = np.log2(N // M)
+    sd = np.sqrt(np.diagonal(kc, axis1=1, axis2=2))
+    assert np.all(np.abs(means - km) < 6 * sd * np.sqrt(S / N) * 10 + 1e-6)
+
+
+def test_determinism_and_step_dev():
+    cfg = inputs.CONFIGS["C4"]
+    p = inputs.model_params(cfg)
+    _, ys = inputs.simulate(cfg, T=5)
+    m1, x1 = _run(p, 1 << 16, 64, 9, ys)
+    m2, x2 = _run(p, 1 << 16, 64, 9, ys)
+    m3, x3 = _run(p, 1 << 16, 64, 9, ys, dev=True)
+    assert np.array_equal(m1, m2) and np.array_equal(x1, x2)
+    assert np.array_equal(m1, m3) and np.array_equal(x1, x3)
+    m4, _ = _run(p, 1 << 16, 64, 10, ys)
+    assert not np.array_equal(m1, m4)
+
+
+def test_error_codes():
+    cfg = inputs.CONFIGS["C1"]
+    p = inputs.model_params(cfg)
+    f = pfb.ParticleFilter(p, 1024, 64, 1)
+    with pytest.raises(pfb.PFError) as e:
+        f.estimate()
+    assert e.value.code == pfb.PF_ESTATE
+    with pytest.raises(pfb.PFError) as e:
+        f.step(np.array([np.nan], np.float32))
+    assert e.value.code == pfb.PF_EOBS
+    with pytest.raises(pfb.PFError) as e:
+        f.debug_get(pfb.PF_DBG_X)
+    assert e.value.code == pfb.PF_ESTATE
+    f.step(np.array([0.3], np.float32))
+    with pytest.raises(pfb.PFError) as e:
+        f.debug_get(pfb.PF_DBG_X)  # not a debug handle
+    assert e.value.code == pfb.PF_ESTATE
+    f.close()
+    with pytest.raises(pfb.PFError) as e:
+        pfb.ParticleFilter(p, 1024, 1024, 1)  # m = 1
+    assert e.value.code == pfb.PF_EINVAL
+
+
+def test_init_distribution():
+    """x_0 ~ pi_0: the predictive mean/second moment at n = 0 match the prior."""
+    cfg = inputs.CONFIGS["C4"]
+    p = inputs.model_params(cfg)
+    N = 1 << 20
+    f = pfb.ParticleFilter(p, N, 64, 4)
+    f.step(np.zeros(4, np.float32))
+    m1 = f.estimate(pfb.PF_PHI_X, pfb.PF_EST_PREDICT)
+    m2 = f.estimate(pfb.PF_PHI_X2, pfb.PF_EST_PREDICT)
+    f.close()
+    assert np.all(np.abs(m1) < 5 / np.sqrt(N))
+    assert np.all(np.abs(m2 - 1.0) < 5 * np.sqrt(2.0 / N))
