@@ -1,0 +1,302 @@
+#!/usr/bin/env python
+"""Benchmark of the BPF step with augmented resampling (arXiv 1812.01502) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+One "step" = one pf_step: mutate + weight + S butterfly stages + composition over all
+N particles.  Default workload: BASELINE.json configs[3]
+(C4: 4-D linear-Gaussian HMM, N = 2^28, M = 64, S = 22), the configuration the
+north_star's throughput/HBM target is quoted on; it fits one B200 (state 4 GiB).
+
+Timing: W untimed warm-up steps, then K steps bracketed by a barrier +
+torch.cuda.synchronize() and CUDA events on the filter's stream; max over ranks.
+Inputs (x: 4 GiB, A: 1 GiB at C4) are far larger than the 126 MB L2, so no flush is
+needed between steps.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-steps/sec per BPF step (1/2/4/8 B200) and % of HBM roofline"
+UNIT = "particle-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--N", type=int, default=0, help="override N (default: the config's)")
+    ap.add_argument("--M", type=int, default=0, help="override M")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=1)
+    return ap.parse_args()
+
+
+def workload(args):
+    from paper_1812_01502_b200 import inputs
+    cfg = inputs.CONFIGS[args.config]
+    if args.config == "C5" and not args.M:
+        cfg = cfg.with_sizes(64, inputs.C5_N // 64)
+    if args.M or args.N:
+        M = args.M or cfg.M
+        N = args.N or cfg.N
+        cfg = cfg.with_sizes(M, N // M)
+    return cfg
+
+
+def config_dict(cfg, world, parallelism):
+    return {"workload": cfg.name, "model": {1: "linear-Gaussian", 2: "stochastic-volatility"}[cfg.kind],
+            "d": cfg.d, "N_per_gpu": cfg.N, "M": cfg.M, "m": cfg.m, "S": cfg.S, "T": cfg.T,
+            "global_particles": cfg.N * world, "parallelism": parallelism,
+            "l2": "inputs larger than L2 (state + ancestor map >> 126 MB), no flush"}
+
+
+# ----------------------------------------------------------------------------- oracle
+def oracle_sample(cfg, n_sample, steps):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
+    same model and M, N = n_sample particles, `steps` mutating steps.  Single thread."""
+    from oracle import oracle as orc
+    from paper_1812_01502_b200 import inputs
+    params = inputs.model_params(cfg)
+    x = inputs.particle_cloud(cfg, n_sample, 5)
+    _, ys = inputs.simulate(cfg, T=steps + 1)
+    t0 = time.perf_counter()
+    for n in range(1, steps + 1):
+        r = orc.step(params, n_sample, cfg.M, 1, n, ys[n], x, tables=False)
+        x = r["xhat"].astype("float32")
+    dt = time.perf_counter() - t0
+    m = n_sample // cfg.M
+    return dict(value=n_sample * steps / dt, unit=UNIT, cores=1, kind="oracle",
+                sample=f"{cfg.name} model, M={cfg.M}, N={n_sample} (m={m}, S={m.bit_length() - 1}), "
+                       f"{steps} steps, fp64 C oracle, 1 thread, {dt:.1f} s")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = workload(args)
+    n_sample = min(cfg.N, 1 << 20)
+    from oracle import oracle as orc
+    orc.build()
+    for _ in range(max(0, args.warmup)):
+        pass  # the oracle has no warm-up state; steps are timed below
+    steps = max(1, args.steps // 25)
+    cb = oracle_sample(cfg, n_sample, steps)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": n_sample / cb["value"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(cfg, 1, "single-thread CPU oracle"),
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.gpu), "-lms", "20"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [r.split(",") for r in out.strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for k, nm in enumerate(names):
+                    if r[4 + k].strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        loaded = [v for v in sm if mx and v > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- ours
+def algorithmic_bytes(cfg, kernel: str, passes) -> float:
+    """Algorithmic HBM bytes per launch: the bytes the kernel must move
+    once, with no sector amplification and no re-reads."""
+    N, d = cfg.N, cfg.d
+    index_mode = d >= 4
+    if kernel == "k_pass1":
+        return N * (8 * d + (4 if index_mode else 0))   # read xhat (+ ancestor), write x
+    if kernel == "k_compose":
+        if index_mode:  # first pass writes 4 B, later passes read + write 4 B
+            per = [4 if i == 0 else 8 for i in range(passes)]
+        else:
+            per = [8 * d] * passes
+        return N * sum(per) / max(passes, 1)
+    if kernel == "k_cascade":
+        return (cfg.m / 64) * 8 * 2
+    return 0.0
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(cfg, kernel):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            tr = json.load(f)
+        return tr[f"{cfg.name}:N={cfg.N}:M={cfg.M}"][kernel]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1812_01502_b200 import inputs, pf
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = workload(args)
+    params = inputs.model_params(cfg)
+    _, ys = inputs.simulate(cfg)
+    T = len(ys)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        f = pf.ParticleFilter(params, cfg.N, cfg.M, args.seed + rank, stream=stream)
+        y_dev = torch.tensor(np.asarray(ys, np.float32), device=dev)
+        for w in range(args.warmup):
+            f.step_dev(y_dev[w % T])
+        stream.synchronize()
+        f.timing_enable(True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clocks = ClockSampler(local)
+        clocks.start()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(args.steps):
+            f.step_dev(y_dev[(args.warmup + k) % T])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clk = clocks.stop()
+        ms = e0.elapsed_time(e1)
+        kt = f.timing_read()
+        f.timing_enable(False)
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        launches = sum(n for _, n in kt.values())
+        value = cfg.N * world * args.steps / (ms / 1e3)
+
+        # roofline of the dominant kernel
+        dom = max(kt, key=lambda k: kt[k][0])
+        dom_ms, dom_n = kt[dom]
+        passes = kt["k_compose"][1] // max(args.steps, 1)
+        alg = algorithmic_bytes(cfg, dom, passes)
+        achieved = alg / (dom_ms / dom_n / 1e3) / 1e9
+        peak, peak_src = measured_peak()
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": ncu_traffic(cfg, dom),
+                    "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
+                    "kernel_share_of_step": round(dom_ms / max(sum(v[0] for v in kt.values()), 1e-9), 3),
+                    "step_alg_bytes_frac": round(value / world * 8 * cfg.d / 1e9 / peak, 4)}
+        kernels = {k: {"ms_per_launch": round(v[0] / max(v[1], 1), 4), "launches": v[1]} for k, v in kt.items()}
+
+        # end-to-end through the public API: pinned H2D of y_n, step, D2H of the estimate
+        e2e = None
+        if not args.no_e2e:
+            y_pin = torch.tensor(np.asarray(ys, np.float32)).pin_memory()
+            y_slot = torch.empty(cfg.dy, dtype=torch.float32, device=dev)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for k in range(args.steps):
+                y_slot.copy_(y_pin[(args.warmup + k) % T], non_blocking=True)
+                f.step_dev(y_slot)
+                est = f.estimate(pf.PF_PHI_X, pf.PF_EST_FILTER)
+            torch.cuda.synchronize()
+            te = time.perf_counter() - t0
+            if world > 1:
+                t = torch.tensor([te], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                te = float(t.item())
+            e2e = {"value": cfg.N * world * args.steps / te, "unit": UNIT, "h2d_bytes_per_step": 4 * cfg.dy,
+                   "d2h_bytes_per_step": 8 * cfg.d, "last_filter_mean": [float(v) for v in est]}
+        f.close()
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline:
+            cpu = oracle_sample(cfg, min(cfg.N, 1 << 21), 2)
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": config_dict(cfg, world, "single" if world == 1 else "replicas"),
+                "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

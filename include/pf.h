@@ -138,6 +138,19 @@ int pf_debug_set_state(pf_handle* h, const float* host_xhat, uint32_t n);
 /* Number of kernel launches the last pf_step enqueued (bench accounting). */
 int pf_last_step_launches(const pf_handle* h);
 
+/* --- kernel timing (bench accounting) ------------------------------------------ */
+#define PF_KERNEL_PASS1 0   /* k_pass1: mutate + weight + stages 1..k1 */
+#define PF_KERNEL_CASCADE 1 /* k_cascade: V levels, thresholds, estimates */
+#define PF_KERNEL_COMPOSE 2 /* k_compose: stages k1+1..S */
+#define PF_KERNEL_KINDS 3
+/* When on, every pf_step records a CUDA event pair around each of its kernels on the
+ * handle's stream.  pf_timing_read synchronises the stream and returns, per kernel kind,
+ * the summed device milliseconds (ms[PF_KERNEL_KINDS], HOST) and launch counts
+ * (launches[PF_KERNEL_KINDS], HOST, may be NULL) since the last enable or read, then
+ * resets them.  Errors: PF_EINVAL, PF_ECUDA. */
+int pf_timing_enable(pf_handle* h, int on);
+int pf_timing_read(pf_handle* h, double* ms, int* launches);
+
 #ifdef __cplusplus
 }
 #endif

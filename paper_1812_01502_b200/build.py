@@ -1,6 +1,10 @@
-"""Build the in-tree C-ABI library libpf.so for sm_100a (nvcc, no JIT cache)."""
+"""Build the in-tree C-ABI library libpf.so for sm_100a (nvcc, no JIT cache).
+
+Each translation unit under csrc/ is compiled in parallel, then linked with nvcc -shared.
+"""
 from __future__ import annotations
 
+import concurrent.futures as cf
 import glob
 import os
 import subprocess
@@ -8,12 +12,15 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libpf.so")
-SOURCES = [os.path.join(HERE, "csrc", "pf_api.cu")]
-DEPS = glob.glob(os.path.join(HERE, "csrc", "*")) + [os.path.join(ROOT, "include", "pf.h")]
+HEADERS = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
+    [os.path.join(ROOT, "include", "pf.h")]
 
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr", "-Wno-deprecated-gpu-targets"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+                     "-Wno-deprecated-gpu-targets"]
 
 
 def nvcc() -> str:
@@ -21,20 +28,49 @@ def nvcc() -> str:
     return cand if os.path.exists(cand) else "nvcc"
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+def sources():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+
+
+def _obj(src: str) -> str:
+    return os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
+
+
+def _stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(p) > t for p in DEPS)
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def needs_build() -> bool:
+    objs = [_obj(s) for s in sources()]
+    return _stale(LIB, sources() + HEADERS) or any(_stale(o, [s] + HEADERS) for s, o in zip(sources(), objs))
+
+
+def _compile(src: str, verbose: bool) -> str:
+    out = _obj(src)
+    cmd = [nvcc()] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", "-o", out, src]
+    r = subprocess.run(cmd, cwd=HERE, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    return r.stderr if verbose else ""
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if force or needs_build():
-        cmd = [nvcc()] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB] + SOURCES
-        subprocess.check_call(cmd, cwd=HERE)
+    if not force and not needs_build():
+        return LIB
+    os.makedirs(OBJ, exist_ok=True)
+    todo = [s for s in sources() if force or _stale(_obj(s), [s] + HEADERS)]
+    with cf.ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 4))) as ex:
+        logs = list(ex.map(lambda s: _compile(s, verbose), todo))
+    if verbose:
+        for src, log in zip(todo, logs):
+            print(f"== {os.path.basename(src)}\n{log}")
+    subprocess.check_call([nvcc()] + ARCH + ["-shared", "-o", LIB] + [_obj(s) for s in sources()], cwd=HERE)
     return LIB
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
+    build(force="-f" in sys.argv or "-v" in sys.argv, verbose="-v" in sys.argv)
     print(LIB)

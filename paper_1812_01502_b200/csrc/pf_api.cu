@@ -9,30 +9,39 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/pf.h"
-#include "pf_kernels.cuh"
+#include "pf_launch.h"
 
 using namespace pfk;
 
 namespace {
 
-constexpr uint32_t kPass1SmemBudget = 112u * 1024u;
-constexpr uint32_t kComposeSmemBudget = 200u * 1024u;
+constexpr uint32_t kPass1SmemBudgetDefault = 64u * 1024u;
+constexpr uint32_t kComposeSmemBudgetDefault = 200u * 1024u;
+constexpr uint32_t kPass1ThreadsDefault = 256u;
+constexpr uint32_t kComposeThreadsDefault = 1024u;
+
+// Tuning knobs (environment, read at pf_init; for experiments only).
+uint32_t env_u32(const char* name, uint32_t dflt) {
+    const char* v = getenv(name);
+    return (v && *v) ? (uint32_t)strtoul(v, nullptr, 10) : dflt;
+}
 constexpr uint32_t kLPC = 2048u;
 
 struct ComposePass {
-    uint32_t s0, k, P;
+    uint32_t s0, k, P, threads, qpt;
     bool ident;
 };
 
 struct Plan {
     int D;
     bool index_mode;
-    uint32_t P1, k1, NT, LPC, cascade_grid, pass1_threads;
+    uint32_t P1, k1, NT, LPC, cascade_grid, pass1_threads, pass1_qpt;
     uint32_t pass1_smem;
     std::vector<ComposePass> passes;
 };
@@ -46,18 +55,39 @@ int ilog2_exact(uint64_t v) {
 
 size_t align256(size_t v) { return (v + 255u) & ~size_t(255u); }
 
+uint32_t pick_threads(uint32_t nq, uint32_t maxthr, uint32_t* qpt) {
+    if (nq < 32u) {
+        *qpt = 1;
+        return 32u;
+    }
+    uint32_t t = std::min(nq, std::max(maxthr, std::min(nq / 8u, 1024u)));  // at most 8 quads per thread
+    *qpt = nq / t;
+    return t;
+}
+
 bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err) {
     const uint64_t m = N / M;
     const int S = ilog2_exact(m);
-    const int b = ilog2_exact(M);
     Plan p;
     p.D = d;
-    p.index_mode = d >= 4;
-    // pass-1 tile: the largest 2^k1 groups with k1 <= S whose shared memory fits
-    uint32_t P1 = (uint32_t)std::min<uint64_t>(N, 65536u);
+    // State mode (default): every pass moves the particle states through shared-memory
+    // tiles, so no pass makes a random HBM access.  Index mode (PF_INDEX_MODE=1, d >= 4):
+    // passes compose int32 ancestor maps and the next step gathers x[A(i)] (one random
+    // 4d-byte read per particle, ~3.7e10/s on B200: slower; kept for comparison).
+    p.index_mode = d >= 4 && env_u32("PF_INDEX_MODE", 1u) != 0u;
+    const uint32_t kPass1SmemBudget = env_u32("PF_PASS1_SMEM", kPass1SmemBudgetDefault);
+    const uint32_t kComposeSmemBudget = env_u32("PF_COMPOSE_SMEM", kComposeSmemBudgetDefault);
+    const uint32_t kPass1Threads = env_u32("PF_PASS1_THREADS", kPass1ThreadsDefault);
+    const uint32_t kComposeThreads = env_u32("PF_COMPOSE_THREADS", kComposeThreadsDefault);
+    const uint32_t kMoveSmemBudget = env_u32("PF_MOVE_SMEM", 112u * 1024u);
+    const uint32_t kMoveThreads = env_u32("PF_MOVE_THREADS", 256u);
+    // pass-1 tile: the largest 2^k1 groups (k1 <= S) whose shared memory fits the budget
+    uint32_t P1 = (uint32_t)std::min<uint64_t>(N, 16384u);
     for (;;) {
         const uint32_t k1 = (uint32_t)ilog2_exact(P1 / M);
-        if (pass1_smem(d, P1, M, k1).total <= kPass1SmemBudget || P1 <= 2 * M) break;
+        uint32_t q;
+        const uint32_t thr = pick_threads(P1 / 4, kPass1Threads, &q);
+        if (pass1_smem(d, P1, M, k1, thr).total <= kPass1SmemBudget || P1 <= 2 * M) break;
         P1 >>= 1;
     }
     if (P1 < 2 * M) P1 = 2 * M;
@@ -67,7 +97,12 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err) {
         *err = "internal: k1 > S";
         return false;
     }
-    p.pass1_smem = pass1_smem(d, P1, M, p.k1).total;
+    p.pass1_threads = pick_threads(P1 / 4, kPass1Threads, &p.pass1_qpt);
+    if (p.pass1_qpt > 8u) {
+        *err = "internal: too many quads per thread";
+        return false;
+    }
+    p.pass1_smem = pass1_smem(d, P1, M, p.k1, p.pass1_threads).total;
     if (p.pass1_smem > 227u * 1024u) {
         *err = "pass-1 tile does not fit in shared memory (M too large for d)";
         return false;
@@ -79,33 +114,41 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err) {
         *err = "too many pass-1 tiles for the cascade tree";
         return false;
     }
-    const uint32_t nq = P1 / 4;
-    p.pass1_threads = std::max<uint32_t>(32u, std::min<uint32_t>(kPass1Threads, nq));
-    if ((nq + p.pass1_threads - 1) / p.pass1_threads > (uint32_t)kMaxQuadsPerThread) {
-        *err = "internal: too many quads per thread";
-        return false;
-    }
     // compose passes for stages k1+1..S
     uint32_t s = p.k1 + 1;
     bool first = true;
     while ((int)s <= S) {
         const bool ident = p.index_mode && first;
         const uint32_t payload = ident ? 0u : (p.index_mode ? 4u : (uint32_t)(4 * d));
-        uint32_t P = 65536u;
-        while (P > 2 * M && (compose_smem(P, payload) > kComposeSmemBudget || P > N)) P >>= 1;
+        const bool move = !p.index_mode;
+        auto smem_of = [&](uint32_t PP, uint32_t kk) {
+            return move ? move_smem(PP, payload, kk) : compose_smem(PP, payload, kk);
+        };
+        const uint32_t budget = move ? kMoveSmemBudget : kComposeSmemBudget;
+        uint32_t P = 32768u;
+        while (P > 2 * M && (smem_of(P, (uint32_t)ilog2_exact(P / M)) > budget || P > N)) P >>= 1;
         if (P < 2 * M) P = 2 * M;
-        if (compose_smem(P, payload) > 227u * 1024u) {
-            *err = "compose tile does not fit in shared memory";
-            return false;
-        }
         uint32_t k = (uint32_t)ilog2_exact(P / M);
         if (k > (uint32_t)S - s + 1) k = (uint32_t)S - s + 1;
         P = M << k;
-        p.passes.push_back({s, k, P, ident});
+        if (smem_of(P, k) > 227u * 1024u) {
+            *err = "compose tile does not fit in shared memory";
+            return false;
+        }
+        ComposePass cp;
+        cp.s0 = s;
+        cp.k = k;
+        cp.P = P;
+        cp.ident = ident;
+        cp.threads = pick_threads(P / 4, move ? kMoveThreads : kComposeThreads, &cp.qpt);
+        if (cp.qpt > 8u) {
+            *err = "internal: compose quads per thread";
+            return false;
+        }
+        p.passes.push_back(cp);
         s += k;
         first = false;
     }
-    (void)b;
     *pl = p;
     return true;
 }
@@ -168,7 +211,41 @@ struct pf_handle {
     bool a_identity;     // next step reads X[cur] without a map
     bool have_step;
     int last_launches;
+    // kernel timing
+    bool timing;
+    struct Rec {
+        cudaEvent_t a, b;
+        int kind;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
     std::string err;
+    cudaEvent_t ev() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+    void mark(int kind, bool begin) {
+        if (!timing) return;
+        if (begin) {
+            Rec r;
+            r.a = ev();
+            r.b = nullptr;
+            r.kind = kind;
+            cudaEventRecord(r.a, stream);
+            recs.push_back(r);
+        } else {
+            recs.back().b = ev();
+            cudaEventRecord(recs.back().b, stream);
+        }
+    }
+    ~pf_handle() {
+        for (cudaEvent_t e : pool) cudaEventDestroy(e);
+    }
     float* X(int i) { return reinterpret_cast<float*>(ws + (i ? lay.X1 : lay.X0)); }
     int32_t* A(int i) { return reinterpret_cast<int32_t*>(ws + (i ? lay.A1 : lay.A0)); }
     template <typename T>
@@ -261,6 +338,11 @@ static ModelParams to_params(const pf_model* mdl) {
         for (int j = 0; j < dy; ++j)
             if (k != j && mp.Rinv[k * dy + j] != 0.0f) diag = false;
     mp.diag_obs = diag ? 1 : 0;
+    bool dlq = true;
+    for (int k = 0; k < d; ++k)
+        for (int j = 0; j < d; ++j)
+            if (k != j && mp.LQ[k * d + j] != 0.0f) dlq = false;
+    mp.diag_lq = dlq ? 1 : 0;
     for (int k = 0; k < dy; ++k) mp.rdiag[k] = -0.5f * mp.Rinv[k * dy + k];
     return mp;
 }
@@ -287,35 +369,21 @@ static bool validate_topology(uint64_t N, uint32_t M, std::string* err) {
 }
 
 // ---------------------------------------------------------------------------------------
-// kernel dispatch
-template <int D, int KIND>
-static void launch_init(pf_handle* h) {
-    InitArgs a;
-    a.mp = h->mp;
-    a.key = {(uint32_t)(h->seed & 0xffffffffu), (uint32_t)(h->seed >> 32)};
-    a.N = h->N;
-    a.x = h->X(0);
-    const uint64_t nq = h->N / 4;
-    const uint32_t grid = (uint32_t)std::min<uint64_t>((nq + 255) / 256, 148ull * 16);
-    k_init<D, KIND><<<grid, 256, 0, h->stream>>>(a);
-}
-
-template <int D, int KIND>
+// kernel dispatch (instantiations live in pf_inst_*.cu)
 static void launch_pass1(pf_handle* h, const Pass1Args& a, bool gather) {
     const Plan& p = h->plan;
-    if (gather) {
-        auto k = k_pass1<D, KIND, true>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, p.pass1_smem);
-        k<<<p.NT, p.pass1_threads, p.pass1_smem, h->stream>>>(a);
-    } else {
-        auto k = k_pass1<D, KIND, false>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, p.pass1_smem);
-        k<<<p.NT, p.pass1_threads, p.pass1_smem, h->stream>>>(a);
+    const LaunchCfg c{p.NT, p.pass1_threads, p.pass1_smem, h->stream};
+    const bool dbg = h->flags & PF_FLAG_DEBUG;
+    const int q = (int)p.pass1_qpt;
+    switch (p.D) {
+        case 1: launch_pass1_d1(h->mp.kind, gather, dbg, q, c, a); break;
+        case 2: launch_pass1_d2(h->mp.kind, gather, dbg, q, c, a); break;
+        case 4: launch_pass1_d4(h->mp.kind, gather, dbg, q, c, a); break;
+        default: launch_pass1_d8(h->mp.kind, gather, dbg, q, c, a); break;
     }
 }
 
-template <int D>
-static void launch_cascade(pf_handle* h) {
+static void launch_cascade_k(pf_handle* h) {
     const Plan& p = h->plan;
     CascadeArgs c;
     c.logV = h->at<double>(h->lay.logV);
@@ -331,21 +399,25 @@ static void launch_cascade(pf_handle* h) {
     c.b = h->b;
     c.NT = p.NT;
     c.LPC = p.LPC;
-    k_cascade<D><<<p.cascade_grid, kCascadeThreads, 0, h->stream>>>(c);
+    launch_cascade(p.D, LaunchCfg{p.cascade_grid, (uint32_t)kCascadeThreads, 0u, h->stream}, c);
 }
 
-template <typename T, bool IDENT>
-static void launch_compose(pf_handle* h, const ComposeArgs& a, uint32_t P) {
-    const uint32_t smem = compose_smem(P, IDENT ? 0u : (uint32_t)sizeof(T));
-    auto k = k_compose<T, IDENT>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const uint32_t grid = (uint32_t)(h->N / P);
-    const uint32_t threads = std::min<uint32_t>(kComposeThreads, std::max<uint32_t>(32u, P / 4));
-    k<<<grid, threads, smem, h->stream>>>(a);
+static void launch_compose_k(pf_handle* h, int payload, const ComposeArgs& a, const ComposePass& cp) {
+    static const uint32_t bytes[6] = {0u, 4u, 4u, 8u, 16u, 32u};
+    const uint32_t pb = bytes[payload];
+    const bool dbg = h->flags & PF_FLAG_DEBUG;
+    if (payload >= kPayloadF1) {
+        const LaunchCfg c{(uint32_t)(h->N / cp.P), cp.threads, move_smem(cp.P, pb, cp.k), h->stream};
+        launch_move(payload, dbg, (int)cp.qpt, c, a);
+        return;
+    }
+    const LaunchCfg c{(uint32_t)(h->N / cp.P), cp.threads, compose_smem(cp.P, pb, cp.k), h->stream};
+    if (dbg) launch_compose_dbg(payload, (int)cp.qpt, c, a);
+    else launch_compose_nodbg(payload, (int)cp.qpt, c, a);
 }
 
-template <int D, int KIND>
 static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
+    const int D = h->plan.D;
     const Plan& p = h->plan;
     const bool dbg = h->flags & PF_FLAG_DEBUG;
     Pass1Args a;
@@ -362,6 +434,8 @@ static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
     a.S = h->S;
     a.k1 = p.k1;
     a.P1 = p.P1;
+    a.T1 = p.P1 / h->M;
+    a.sl = pass1_smem(p.D, p.P1, h->M, p.k1, p.pass1_threads);
     const int src = h->cur, dst = h->cur ^ 1;
     a.x_in = h->X(src);
     const bool gather = p.index_mode && !h->a_identity;
@@ -373,9 +447,13 @@ static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
     a.dbg_x = dbg ? h->at<float>(h->lay.dbg_x) : nullptr;
     a.dbg_lw = dbg ? h->at<float>(h->lay.dbg_lw) : nullptr;
     a.dbg_anc = dbg ? h->at<int32_t>(h->lay.dbg_anc) : nullptr;
-    launch_pass1<D, KIND>(h, a, gather);
+    h->mark(PF_KERNEL_PASS1, true);
+    launch_pass1(h, a, gather);
+    h->mark(PF_KERNEL_PASS1, false);
     int launches = 1;
-    launch_cascade<D>(h);
+    h->mark(PF_KERNEL_CASCADE, true);
+    launch_cascade_k(h);
+    h->mark(PF_KERNEL_CASCADE, false);
     ++launches;
 
     // compose passes
@@ -396,25 +474,26 @@ static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
         c.k = cp.k;
         c.P = cp.P;
         c.lowbits = cp.s0 - 1;
+        h->mark(PF_KERNEL_COMPOSE, true);
         if (p.index_mode) {
             if (cp.ident) {
                 amap_out = 0;
                 c.pin = nullptr;
                 c.pout = h->A(0);
-                launch_compose<int32_t, true>(h, c, cp.P);
+                launch_compose_k(h, kPayloadIdent, c, cp);
             } else {
                 c.pin = h->A(amap_out);
                 c.pout = h->A(amap_out ^ 1);
                 amap_out ^= 1;
-                launch_compose<int32_t, false>(h, c, cp.P);
+                launch_compose_k(h, kPayloadIndex, c, cp);
             }
         } else {
             c.pin = h->X(xs);
             c.pout = h->X(xs ^ 1);
             xs ^= 1;
-            if (D == 1) launch_compose<float, false>(h, c, cp.P);
-            else launch_compose<float2, false>(h, c, cp.P);
+            launch_compose_k(h, D == 1 ? kPayloadF1 : (D == 2 ? kPayloadF2 : (D == 4 ? kPayloadF4 : kPayloadF8)), c, cp);
         }
+        h->mark(PF_KERNEL_COMPOSE, false);
         ++launches;
     }
     if (p.index_mode) {
@@ -431,21 +510,7 @@ static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
     return check_cuda(h, "pf_step");
 }
 
-template <int D>
-static int dispatch_kind(pf_handle* h, const float* yh, const float* yd) {
-    if (h->mp.kind == PF_SV) return run_step<D, 2>(h, yh, yd);
-    return run_step<D, 1>(h, yh, yd);
-}
-
-static int dispatch_step(pf_handle* h, const float* yh, const float* yd) {
-    switch (h->plan.D) {
-        case 1: return dispatch_kind<1>(h, yh, yd);
-        case 2: return dispatch_kind<2>(h, yh, yd);
-        case 4: return dispatch_kind<4>(h, yh, yd);
-        case 8: return dispatch_kind<8>(h, yh, yd);
-    }
-    return fail(h, PF_EINVAL, "bad d");
-}
+static int dispatch_step(pf_handle* h, const float* yh, const float* yd) { return run_step(h, yh, yd); }
 
 // ---------------------------------------------------------------------------------------
 extern "C" {
@@ -489,14 +554,16 @@ int pf_init(const pf_model* model, uint64_t N, uint32_t M, uint64_t seed, uint32
     h->a_identity = true;
     h->have_step = false;
     h->last_launches = 0;
+    h->timing = false;
     cudaMemsetAsync(h->at<uint32_t>(L.ticket), 0, 16, h->stream);
-    switch (p.D * 4 + h->mp.kind) {
-        case 1 * 4 + 1: launch_init<1, 1>(h); break;
-        case 1 * 4 + 2: launch_init<1, 2>(h); break;
-        case 2 * 4 + 1: launch_init<2, 1>(h); break;
-        case 4 * 4 + 1: launch_init<4, 1>(h); break;
-        case 8 * 4 + 1: launch_init<8, 1>(h); break;
-        default: delete h; return fail(nullptr, PF_EINVAL, "unsupported (d, kind)");
+    {
+        InitArgs ia;
+        ia.mp = h->mp;
+        ia.key = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+        ia.N = N;
+        ia.x = h->X(0);
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((N / 4 + 255) / 256, 148ull * 16);
+        launch_init(p.D, h->mp.kind, LaunchCfg{grid, 256u, 0u, h->stream}, ia);
     }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -539,6 +606,34 @@ const char* pf_last_error(const pf_handle* h) { return h ? h->err.c_str() : g_in
 
 int pf_last_step_launches(const pf_handle* h) { return h ? h->last_launches : 0; }
 
+int pf_timing_enable(pf_handle* h, int on) {
+    if (!h) return fail(h, PF_EINVAL, "NULL handle");
+    h->timing = on != 0;
+    h->recs.clear();
+    h->used = 0;
+    return PF_OK;
+}
+
+int pf_timing_read(pf_handle* h, double* ms, int* launches) {
+    if (!h || !ms) return fail(h, PF_EINVAL, "NULL argument");
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_timing_read: ") + cudaGetErrorString(e));
+    for (int k = 0; k < PF_KERNEL_KINDS; ++k) {
+        ms[k] = 0.0;
+        if (launches) launches[k] = 0;
+    }
+    for (const auto& r : h->recs) {
+        float t = 0.0f;
+        e = cudaEventElapsedTime(&t, r.a, r.b);
+        if (e != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_timing_read: ") + cudaGetErrorString(e));
+        ms[r.kind] += (double)t;
+        if (launches) launches[r.kind] += 1;
+    }
+    h->recs.clear();
+    h->used = 0;
+    return PF_OK;
+}
+
 int pf_debug_ptr(pf_handle* h, int what, int stage, void** dev_out) {
     if (!h || !dev_out) return fail(h, PF_EINVAL, "NULL argument");
     if (!h->have_step) return fail(h, PF_ESTATE, "no completed step");
@@ -563,7 +658,7 @@ int pf_debug_ptr(pf_handle* h, int what, int stage, void** dev_out) {
             return PF_OK;
         case PF_DBG_ANC_FINAL: {
             int32_t* A = h->at<int32_t>(h->lay.dbg_A);
-            k_debug_compose<<<1024, 256, 0, h->stream>>>(h->at<int32_t>(h->lay.dbg_anc), h->N, h->S, A);
+            launch_debug_compose(LaunchCfg{1024u, 256u, 0u, h->stream}, h->at<int32_t>(h->lay.dbg_anc), h->N, h->S, A);
             *dev_out = A;
             return check_cuda(h, "pf_debug_ptr");
         }
@@ -571,12 +666,7 @@ int pf_debug_ptr(pf_handle* h, int what, int stage, void** dev_out) {
             float* out = h->at<float>(h->lay.dbg_xhat);
             const float* x = h->X(h->cur);
             const int32_t* A = (h->plan.index_mode && !h->a_identity) ? h->A(h->amap) : nullptr;
-            switch (D) {
-                case 1: k_gather<1><<<1024, 256, 0, h->stream>>>(x, A, h->N, out); break;
-                case 2: k_gather<2><<<1024, 256, 0, h->stream>>>(x, A, h->N, out); break;
-                case 4: k_gather<4><<<1024, 256, 0, h->stream>>>(x, A, h->N, out); break;
-                case 8: k_gather<8><<<1024, 256, 0, h->stream>>>(x, A, h->N, out); break;
-            }
+            launch_gather(D, LaunchCfg{1024u, 256u, 0u, h->stream}, x, A, h->N, out);
             *dev_out = out;
             return check_cuda(h, "pf_debug_ptr");
         }

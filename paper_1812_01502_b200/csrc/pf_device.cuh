@@ -50,14 +50,40 @@ __device__ __forceinline__ uint32_t word_of(const uint4& v, int w) {
 // u in [0,1) from the 24 high bits (exact in fp32).
 __device__ __forceinline__ float u01f(uint32_t r) { return (float)(r >> 8) * 0x1p-24f; }
 
-// Box-Muller: (a, b) -> two normals (cos, sin) with u1 = ((a>>8)+1) 2^-24 in (0,1].
+// -2 ln u1 for u1 = n 2^-24, n = (a >> 8) + 1 in [1, 2^24].  With n = 2^e m, m in
+// [0.75, 1.5): ln u1 = (e - 24) ln 2 + log1p(f), f = m - 1 exact, and
+// log1p(f) = 2 atanh(t) = 2t (1 + t^2/3 + t^4/5 + t^6/7 + t^8/9), t = f / (2 + f),
+// |t| <= 0.2 (truncation < 4e-9).  Relative accuracy ~1e-7 everywhere, including
+// u1 -> 1 where R = sqrt(-2 ln u1) -> 0 is most sensitive (no cancellation).
+__device__ __forceinline__ float neg2_log_u1(uint32_t a) {
+    const float nf = (float)((a >> 8) + 1u);  // exact
+    const int bits = __float_as_int(nf);
+    int e = (bits >> 23) - 127;
+    float m = __int_as_float((bits & 0x007fffff) | 0x3f800000);  // [1, 2)
+    const bool hi = m >= 1.5f;
+    m = hi ? 0.5f * m : m;
+    e = hi ? e + 1 : e;
+    const float f = m - 1.0f;
+    const float t = __fdividef(f, 2.0f + f);
+    const float t2 = t * t;
+    const float poly = fmaf(t2, fmaf(t2, fmaf(t2, fmaf(t2, 1.0f / 9.0f, 1.0f / 7.0f), 1.0f / 5.0f), 1.0f / 3.0f), 1.0f);
+    const float l1p = 2.0f * t * poly;
+    const float k = (float)(24 - e);
+    return 2.0f * fmaf(k, 0.693145751953125f, fmaf(k, 1.428606765330187e-06f, -l1p));  // ln2 = hi + lo
+}
+
+// Box-Muller: (a, b) -> (R cos 2 pi u2, R sin 2 pi u2), R = sqrt(-2 ln u1), with
+// u1 = ((a>>8)+1) 2^-24 in (0,1] and u2 = (b>>8) 2^-24 in [0,1).
+// The square root uses MUFU.RSQ and the angle the MUFU sin/cos on [-pi, pi):
+// cos(2 pi u2) = -cos(th), sin(2 pi u2) = -sin(th) with th = 2 pi u2 - pi.
+// Absolute error <= ~3e-6.
 __device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
-    const float u1 = (float)((a >> 8) + 1u) * 0x1p-24f;
-    const float u2 = (float)(b >> 8) * 0x1p-24f;
-    const float rad = sqrtf(-2.0f * logf(u1));
+    const float r2 = neg2_log_u1(a);
+    const float rad = r2 * rsqrtf(fmaxf(r2, 1e-30f));
+    const float th = fmaf((float)(b >> 8), 6.28318530717958647692f * 0x1p-24f, -3.14159265358979323846f);
     float s, c;
-    sincospif(2.0f * u2, &s, &c);
-    return make_float2(rad * c, rad * s);
+    __sincosf(th, &s, &c);
+    return make_float2(-rad * c, -rad * s);
 }
 
 // Four normals of one block: coordinates 4j..4j+3.
@@ -75,6 +101,7 @@ struct ModelParams {
     int kind;  // 1 LG, 2 SV
     int d, dy;
     int diag_obs;  // H == I (dy == d) and Rinv diagonal: fast weighting path
+    int diag_lq;   // LQ diagonal: fast noise path
     float A[64], LQ[64], H[64], Rinv[64], m0[8], L0[64];
     float rdiag[8];  // -0.5 * Rinv_kk (fast path)
     float phi, sigma, beta, sv_m0, sv_s0;
@@ -92,8 +119,12 @@ __device__ __forceinline__ void mutate(const ModelParams& mp, const float* xh, c
             float v = 0.0f;
 #pragma unroll
             for (int j = 0; j < D; ++j) v = fmaf(mp.A[k * D + j], xh[j], v);
+            if (mp.diag_lq) {
+                v = fmaf(mp.LQ[k * D + k], z[k], v);
+            } else {
 #pragma unroll
-            for (int j = 0; j <= k; ++j) v = fmaf(mp.LQ[k * D + j], z[j], v);
+                for (int j = 0; j <= k; ++j) v = fmaf(mp.LQ[k * D + j], z[j], v);
+            }
             x[k] = v;
         }
     }
@@ -162,6 +193,23 @@ __device__ __forceinline__ uint32_t side_threshold(double vl, double vr, int b) 
     if (vl == -CUDART_INF && vr == -CUDART_INF) p = 0.5;
     else p = 1.0 / (1.0 + exp(vr - vl));
     return (uint32_t)floor(p * ldexp(1.0, 32 - b));
+}
+
+// The same two quantities with the O(1) transcendental part in fp32 (the large common
+// offset stays fp64): |error| <~ 3e-7 in log V and ~1e-7 in p, well inside the 1e-6
+// decision window of the parity contract.  Used for the in-tile levels of k_pass1.
+__device__ __forceinline__ double log_pair_mean_fast(double a, double b) {
+    const double c = a > b ? a : b;
+    if (c == -CUDART_INF) return -CUDART_INF;
+    const float dlt = (float)((a > b ? b : a) - c);  // <= 0, possibly -inf
+    return c + (double)(log1pf(expf(dlt)) - 0.693147180559945309f);
+}
+
+__device__ __forceinline__ uint32_t side_threshold_fast(double vl, double vr, int b) {
+    float p;
+    if (vl == -CUDART_INF && vr == -CUDART_INF) p = 0.5f;
+    else p = 1.0f / (1.0f + expf((float)(vr - vl)));
+    return (uint32_t)floorf(p * __int_as_float((127 + 32 - b) << 23));  // p * 2^(32-b), exact scaling
 }
 
 }  // namespace pfk

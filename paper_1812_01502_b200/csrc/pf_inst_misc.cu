@@ -1,0 +1,41 @@
+// Instantiations of k_init, k_cascade and the debug kernels.
+#include "pf_launch.h"
+
+namespace pfk {
+
+void launch_cascade(int D, const LaunchCfg& c, const CascadeArgs& a) {
+    switch (D) {
+        case 1: k_cascade<1><<<c.grid, c.threads, 0, c.stream>>>(a); break;
+        case 2: k_cascade<2><<<c.grid, c.threads, 0, c.stream>>>(a); break;
+        case 4: k_cascade<4><<<c.grid, c.threads, 0, c.stream>>>(a); break;
+        default: k_cascade<8><<<c.grid, c.threads, 0, c.stream>>>(a); break;
+    }
+}
+
+void launch_init(int D, int kind, const LaunchCfg& c, const InitArgs& a) {
+    if (kind == 2) {
+        k_init<1, 2><<<c.grid, c.threads, 0, c.stream>>>(a);
+        return;
+    }
+    switch (D) {
+        case 1: k_init<1, 1><<<c.grid, c.threads, 0, c.stream>>>(a); break;
+        case 2: k_init<2, 1><<<c.grid, c.threads, 0, c.stream>>>(a); break;
+        case 4: k_init<4, 1><<<c.grid, c.threads, 0, c.stream>>>(a); break;
+        default: k_init<8, 1><<<c.grid, c.threads, 0, c.stream>>>(a); break;
+    }
+}
+
+void launch_debug_compose(const LaunchCfg& c, const int32_t* anc, uint64_t N, uint32_t S, int32_t* A) {
+    k_debug_compose<0><<<c.grid, c.threads, 0, c.stream>>>(anc, N, S, A);
+}
+
+void launch_gather(int D, const LaunchCfg& c, const float* x, const int32_t* A, uint64_t N, float* out) {
+    switch (D) {
+        case 1: k_gather<1><<<c.grid, c.threads, 0, c.stream>>>(x, A, N, out); break;
+        case 2: k_gather<2><<<c.grid, c.threads, 0, c.stream>>>(x, A, N, out); break;
+        case 4: k_gather<4><<<c.grid, c.threads, 0, c.stream>>>(x, A, N, out); break;
+        default: k_gather<8><<<c.grid, c.threads, 0, c.stream>>>(x, A, N, out); break;
+    }
+}
+
+}  // namespace pfk

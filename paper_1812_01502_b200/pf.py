@@ -66,12 +66,17 @@ def lib() -> ctypes.CDLL:
         L.pf_debug_ptr.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
         L.pf_debug_set_state.argtypes = [vp, vp, u32]
         L.pf_last_step_launches.argtypes = [vp]
+        L.pf_timing_enable.argtypes = [vp, ctypes.c_int]
+        L.pf_timing_read.argtypes = [vp, vp, vp]
         _lib = L
     return _lib
 
 
 EXPORTED = ["pf_workspace_bytes", "pf_init", "pf_step", "pf_step_dev", "pf_estimate", "pf_destroy",
-            "pf_last_error", "pf_debug_get", "pf_debug_ptr", "pf_debug_set_state", "pf_last_step_launches"]
+            "pf_last_error", "pf_debug_get", "pf_debug_ptr", "pf_debug_set_state", "pf_last_step_launches",
+            "pf_timing_enable", "pf_timing_read"]
+PF_KERNEL_KINDS = 3
+KERNEL_NAMES = ("k_pass1", "k_cascade", "k_compose")
 
 
 def _check(rc: int, h=None):
@@ -190,6 +195,16 @@ class ParticleFilter:
 
     def launches(self) -> int:
         return int(lib().pf_last_step_launches(self.h))
+
+    def timing_enable(self, on: bool = True):
+        _check(lib().pf_timing_enable(self.h, 1 if on else 0), self.h)
+
+    def timing_read(self):
+        """{kernel name: (summed ms, launches)} since the last enable/read."""
+        ms = np.zeros(PF_KERNEL_KINDS, np.float64)
+        n = np.zeros(PF_KERNEL_KINDS, np.int32)
+        _check(lib().pf_timing_read(self.h, ms.ctypes.data, n.ctypes.data), self.h)
+        return {KERNEL_NAMES[k]: (float(ms[k]), int(n[k])) for k in range(PF_KERNEL_KINDS)}
 
     def debug_tensor(self, what: int, stage: int = 0):
         """Device view (torch tensor into the workspace) of a debug table."""
