@@ -79,7 +79,7 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err) {
     const uint32_t kComposeSmemBudget = env_u32("PF_COMPOSE_SMEM", kComposeSmemBudgetDefault);
     const uint32_t kPass1Threads = env_u32("PF_PASS1_THREADS", kPass1ThreadsDefault);
     const uint32_t kComposeThreads = env_u32("PF_COMPOSE_THREADS", kComposeThreadsDefault);
-    const uint32_t kMoveSmemBudget = env_u32("PF_MOVE_SMEM", 112u * 1024u);
+    const uint32_t kMoveSmemBudget = env_u32("PF_MOVE_SMEM", 118000u);
     const uint32_t kMoveThreads = env_u32("PF_MOVE_THREADS", 256u);
     // pass-1 tile: the largest 2^k1 groups (k1 <= S) whose shared memory fits the budget
     uint32_t P1 = (uint32_t)std::min<uint64_t>(N, 16384u);

@@ -737,6 +737,21 @@ __host__ __device__ inline uint32_t compose_smem(uint32_t P, uint32_t payload_by
     return P * payload_bytes + 4u * P + 4u * (1u << k);
 }
 
+// Thresholds of a tile for stages s0..s0+k-1 into shared memory: stage st has
+// 2^{k-st-1} entries at offset 2^k - 2^{k-st}.  One flat index space, so every thread's
+// loads are independent (a per-stage loop would serialise k global-load latencies).
+__device__ __forceinline__ void load_tile_thresholds(const ComposeArgs& a, const TileGeom& G, uint32_t k,
+                                                     uint32_t* ths) {
+    const uint32_t E = (1u << k) - 1u;
+    for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
+        const uint32_t u = (1u << k) - e;                    // in (2^{k-st-1}, 2^{k-st}]
+        const uint32_t st = k - (32u - __clz(u - 1u));       // k - ceil(log2 u)
+        const uint32_t off = (1u << k) - (1u << (k - st));
+        const uint32_t s = a.s0 + st;
+        ths[e] = __ldg(a.thr + level_offset(a.m, (int)s) + (G.thi >> s) + (e - off));
+    }
+}
+
 template <typename T>
 struct __align__(4 * sizeof(T) <= 16 ? 4 * sizeof(T) : 16) Vec4 {
     T v[4];
@@ -762,12 +777,7 @@ __global__ void __launch_bounds__(1024) k_compose(const __grid_constant__ Compos
     const T* pin = reinterpret_cast<const T*>(a.pin);
     T* pout = reinterpret_cast<T*>(a.pout);
 
-    // thresholds of this tile for stages s0..s0+k-1: stage st has 2^{k-st-1} entries
-    for (uint32_t st = 0; st < k; ++st) {
-        const uint32_t s = a.s0 + st, cnt = 1u << (k - st - 1), off = (1u << k) - (1u << (k - st));
-        const uint64_t g0 = level_offset(a.m, (int)s) + (G.thi >> s);
-        for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) ths[off + i] = __ldg(a.thr + g0 + i);
-    }
+    load_tile_thresholds(a, G, k, ths);
 #pragma unroll
     for (int it = 0; it < QPT; ++it) {
         const uint32_t q = threadIdx.x + it * blockDim.x;
@@ -870,12 +880,7 @@ __global__ void __launch_bounds__(1024) k_move(const __grid_constant__ ComposeAr
     } else {
         for (uint32_t l = threadIdx.x; l < P; l += blockDim.x) pin_s[l] = pin[G.gpos(l)];
     }
-    // thresholds of this tile for stages s0..s0+k-1: stage st has 2^{k-st-1} entries
-    for (uint32_t st = 0; st < k; ++st) {
-        const uint32_t s = a.s0 + st, cnt = 1u << (k - st - 1), off = (1u << k) - (1u << (k - st));
-        const uint64_t g0 = level_offset(a.m, (int)s) + (G.thi >> s);
-        for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) ths[off + i] = __ldg(a.thr + g0 + i);
-    }
+    load_tile_thresholds(a, G, k, ths);
     __syncthreads();
 
     // B: all stages' draws
