@@ -59,8 +59,8 @@ def workload(args):
 
 def config_dict(cfg, world, parallelism):
     return {"workload": cfg.name, "model": {1: "linear-Gaussian", 2: "stochastic-volatility"}[cfg.kind],
-            "d": cfg.d, "N_per_gpu": cfg.N, "M": cfg.M, "m": cfg.m, "S": cfg.S, "T": cfg.T,
-            "global_particles": cfg.N * world, "parallelism": parallelism,
+            "d": cfg.d, "N": cfg.N, "N_per_gpu": cfg.N // world, "M": cfg.M, "m": cfg.m, "S": cfg.S, "T": cfg.T,
+            "parallelism": parallelism,
             "l2": "inputs larger than L2 (state + ancestor map >> 126 MB), no flush"}
 
 
@@ -148,11 +148,10 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- ours
-def algorithmic_bytes(cfg, kernel: str, passes) -> float:
+def algorithmic_bytes(cfg, kernel: str, passes, index_mode: bool) -> float:
     """Algorithmic HBM bytes per launch: the bytes the kernel must move
-    once, with no sector amplification and no re-reads."""
+    once, with no sector amplification and no re-reads.  cfg: this rank's shard."""
     N, d = cfg.N, cfg.d
-    index_mode = d >= 4
     if kernel == "k_pass1":
         return N * (8 * d + (4 if index_mode else 0))   # read xhat (+ ancestor), write x
     if kernel == "k_compose":
@@ -161,7 +160,9 @@ def algorithmic_bytes(cfg, kernel: str, passes) -> float:
         else:
             per = [8 * d] * passes
         return N * sum(per) / max(passes, 1)
-    if kernel == "k_cascade":
+    if kernel == "k_cross":
+        return N * 8 * d + N * 4 * d  # own read + write, partner half on average
+    if kernel in ("k_cascade", "k_top"):
         return (cfg.m / 64) * 8 * 2
     return 0.0
 
@@ -207,10 +208,28 @@ def run_ours(args):
     T = len(ys)
     stream = torch.cuda.Stream(dev)
     with torch.cuda.stream(stream):
-        f = pf.ParticleFilter(params, cfg.N, cfg.M, args.seed + rank, stream=stream)
         y_dev = torch.tensor(np.asarray(ys, np.float32), device=dev)
+        if world == 1:
+            f = pf.ParticleFilter(params, cfg.N, cfg.M, args.seed, stream=stream)
+
+            def step(k, yd=None):
+                f.step_dev(y_dev[k % T] if yd is None else yd)
+
+            def estimate():
+                return f.estimate(pf.PF_PHI_X, pf.PF_EST_FILTER)
+        else:
+            from paper_1812_01502_b200 import dist as pfd
+            # strong scaling: the global N of the configuration is split over the ranks
+            f = pfd.LibBackend(params, cfg.N, cfg.M, args.seed, rank, world, stream=stream)
+            tr = pfd.TorchTransport()
+
+            def step(k, yd=None):
+                pfd.sharded_step(f, tr, None, y_dev[k % T] if yd is None else yd)
+
+            def estimate():
+                return f.estimate(pf.PF_PHI_X, pf.PF_EST_FILTER)
         for w in range(args.warmup):
-            f.step_dev(y_dev[w % T])
+            step(w)
         stream.synchronize()
         f.timing_enable(True)
         if world > 1:
@@ -222,7 +241,7 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for k in range(args.steps):
-            f.step_dev(y_dev[(args.warmup + k) % T])
+            step(args.warmup + k)
         e1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -235,14 +254,17 @@ def run_ours(args):
             t = torch.tensor([ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
+        kt = {k: v for k, v in kt.items() if v[1] > 0}
         launches = sum(n for _, n in kt.values())
-        value = cfg.N * world * args.steps / (ms / 1e3)
+        value = cfg.N * args.steps / (ms / 1e3)  # global particles (strong scaling)
 
         # roofline of the dominant kernel
         dom = max(kt, key=lambda k: kt[k][0])
         dom_ms, dom_n = kt[dom]
-        passes = kt["k_compose"][1] // max(args.steps, 1)
-        alg = algorithmic_bytes(cfg, dom, passes)
+        cfg_loc = cfg.with_sizes(cfg.M, cfg.m // world)
+        passes = kt.get("k_compose", (0, 0))[1] // max(args.steps, 1)
+        alg = algorithmic_bytes(cfg_loc, dom, passes, index_mode=(world == 1 and cfg.d >= 4 and
+                                                                  os.environ.get("PF_INDEX_MODE", "1") != "0"))
         achieved = alg / (dom_ms / dom_n / 1e3) / 1e9
         peak, peak_src = measured_peak()
         roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -263,15 +285,15 @@ def run_ours(args):
             t0 = time.perf_counter()
             for k in range(args.steps):
                 y_slot.copy_(y_pin[(args.warmup + k) % T], non_blocking=True)
-                f.step_dev(y_slot)
-                est = f.estimate(pf.PF_PHI_X, pf.PF_EST_FILTER)
+                step(args.warmup + k, y_slot)
+                est = estimate()
             torch.cuda.synchronize()
             te = time.perf_counter() - t0
             if world > 1:
                 t = torch.tensor([te], dtype=torch.float64, device=dev)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 te = float(t.item())
-            e2e = {"value": cfg.N * world * args.steps / te, "unit": UNIT, "h2d_bytes_per_step": 4 * cfg.dy,
+            e2e = {"value": cfg.N * args.steps / te, "unit": UNIT, "h2d_bytes_per_step": 4 * cfg.dy,
                    "d2h_bytes_per_step": 8 * cfg.d, "last_filter_mean": [float(v) for v in est]}
         f.close()
 
@@ -281,8 +303,8 @@ def run_ours(args):
             cpu = oracle_sample(cfg, min(cfg.N, 1 << 21), 2)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": config_dict(cfg, world, "single" if world == 1 else "replicas"),
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": config_dict(cfg, world, "single" if world == 1 else f"groups sharded over {world} GPUs"),
                 "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line))

@@ -110,6 +110,47 @@ void pf_destroy(pf_handle* h);
  * when h is NULL).  Valid until the next call on h. */
 const char* pf_last_error(const pf_handle* h);
 
+/* --- sharded step over G GPUs -------------------
+ * Shard r of G (G a power of two) owns particles [r N/G, (r+1) N/G), i.e. groups
+ * [r m/G, (r+1) m/G); every RNG counter uses the GLOBAL particle index, so a sharded run
+ * draws exactly the numbers of a single-GPU run.  One time step is the collective sequence
+ *   pf_step_local        mutate, weight, stages 1..S - log2 G (all local), shard record
+ *   <allgather the G shard records, rank order>          (caller's transport, e.g. NCCL)
+ *   pf_step_top          top V levels, cross thresholds, global estimate (same on all)
+ *   for t = 1..log2 G:   <exchange pf_cross_buffer with partner rank ^ 2^(t-1)>
+ *                        pf_cross_stage(t, partner's buffer)   (stage S - log2 G + t)
+ * Every call is stream-ordered on the handle's stream; the caller's transport must order
+ * its copies on (or after) that stream. */
+#define PF_SHARD_REC_DOUBLES(d) (3 + 4 * (d)) /* {log V_{S_loc}, partial[2 + 4d]} */
+
+/* Workspace bytes for one shard (0 if invalid). */
+size_t pf_workspace_bytes_sharded(const pf_model* model, uint64_t N, uint32_t M, uint32_t flags, int world);
+
+/* Like pf_init for shard `rank` of `world`; N is the GLOBAL particle count.  Needs m/world
+ * >= 2.  Errors as pf_init.  Sharded handles use the state-moving passes (no gather). */
+int pf_init_sharded(const pf_model* model, uint64_t N, uint32_t M, uint64_t seed, uint32_t flags, int rank,
+                    int world, void* dev_ws, size_t ws_bytes, void* cuda_stream, pf_handle** out);
+
+/* Local phase of one step; y as in pf_step (y_host) or pf_step_dev (y_dev): give one. */
+int pf_step_local(pf_handle* h, const float* y_host, const float* y_dev);
+
+/* DEVICE pointer of this shard's record (PF_SHARD_REC_DOUBLES(d) doubles), valid after
+ * pf_step_local has run on the stream. */
+int pf_shard_record(pf_handle* h, const double** dev_rec);
+
+/* Top levels from all G records (DEVICE, G * PF_SHARD_REC_DOUBLES(d), rank order).
+ * Afterwards pf_estimate returns the global estimate. */
+int pf_step_top(pf_handle* h, const double* dev_all_recs);
+
+/* DEVICE pointer and size of this shard's current state buffer (send it to the partner
+ * of the next cross stage).  Valid until the next pf_cross_stage on this handle. */
+int pf_cross_buffer(pf_handle* h, const void** dev_states, size_t* bytes);
+
+/* Cross stage t (1..log2 G): assemble this shard's stage-(S_loc + t) states from its own
+ * and the partner's (DEVICE, pf_cross_buffer of rank ^ 2^(t-1)) stage-(S_loc + t - 1)
+ * states.  Asynchronous. */
+int pf_cross_stage(pf_handle* h, int t, const void* dev_partner_states);
+
 /* --- debug / test exports (parity harness) ------------------------------------ */
 #define PF_DBG_X 1         /* x_n before resampling, N x d fp32 (needs PF_FLAG_DEBUG) */
 #define PF_DBG_LOGW 2      /* log g_n(x_n^i), N fp32 (needs PF_FLAG_DEBUG) */
@@ -141,8 +182,10 @@ int pf_last_step_launches(const pf_handle* h);
 /* --- kernel timing (bench accounting) ------------------------------------------ */
 #define PF_KERNEL_PASS1 0   /* k_pass1: mutate + weight + stages 1..k1 */
 #define PF_KERNEL_CASCADE 1 /* k_cascade: V levels, thresholds, estimates */
-#define PF_KERNEL_COMPOSE 2 /* k_compose: stages k1+1..S */
-#define PF_KERNEL_KINDS 3
+#define PF_KERNEL_COMPOSE 2 /* k_compose / k_move: stages k1+1..S (S_loc when sharded) */
+#define PF_KERNEL_TOP 3     /* k_top: cross-shard V levels and estimate (sharded) */
+#define PF_KERNEL_CROSS 4   /* k_cross: one cross-shard stage (sharded) */
+#define PF_KERNEL_KINDS 5
 /* When on, every pf_step records a CUDA event pair around each of its kernels on the
  * handle's stream.  pf_timing_read synchronises the stream and returns, per kernel kind,
  * the summed device milliseconds (ms[PF_KERNEL_KINDS], HOST) and launch counts

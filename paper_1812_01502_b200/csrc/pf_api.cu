@@ -65,7 +65,12 @@ uint32_t pick_threads(uint32_t nq, uint32_t maxthr, uint32_t* qpt) {
     return t;
 }
 
-bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err) {
+// N is this shard's particle count; Nglobal the whole problem's.  The pass-1 tile is
+// bounded by Nglobal / kMaxShards so that, for any world size up to kMaxShards, the
+// single-GPU tiles coincide with the sharded ones (bitwise G-invariance).
+constexpr uint64_t kMaxShards = 8;
+bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, bool sharded = false, uint64_t Nglobal = 0) {
+    if (Nglobal == 0) Nglobal = N;
     const uint64_t m = N / M;
     const int S = ilog2_exact(m);
     Plan p;
@@ -74,7 +79,7 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err) {
     // tiles, so no pass makes a random HBM access.  Index mode (PF_INDEX_MODE=1, d >= 4):
     // passes compose int32 ancestor maps and the next step gathers x[A(i)] (one random
     // 4d-byte read per particle, ~3.7e10/s on B200: slower; kept for comparison).
-    p.index_mode = d >= 4 && env_u32("PF_INDEX_MODE", 1u) != 0u;
+    p.index_mode = !sharded && d >= 4 && env_u32("PF_INDEX_MODE", 1u) != 0u;
     const uint32_t kPass1SmemBudget = env_u32("PF_PASS1_SMEM", kPass1SmemBudgetDefault);
     const uint32_t kComposeSmemBudget = env_u32("PF_COMPOSE_SMEM", kComposeSmemBudgetDefault);
     const uint32_t kPass1Threads = env_u32("PF_PASS1_THREADS", kPass1ThreadsDefault);
@@ -82,7 +87,8 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err) {
     const uint32_t kMoveSmemBudget = env_u32("PF_MOVE_SMEM", 118000u);
     const uint32_t kMoveThreads = env_u32("PF_MOVE_THREADS", 256u);
     // pass-1 tile: the largest 2^k1 groups (k1 <= S) whose shared memory fits the budget
-    uint32_t P1 = (uint32_t)std::min<uint64_t>(N, 16384u);
+    uint32_t P1 = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(N, 16384u),
+                                               std::max<uint64_t>(2ull * M, Nglobal / kMaxShards));
     for (;;) {
         const uint32_t k1 = (uint32_t)ilog2_exact(P1 / M);
         uint32_t q;
@@ -155,11 +161,12 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err) {
 
 struct Layout {
     size_t X0, X1, A0, A1, logV, thr, part, scratch, est, ticket, y;
+    size_t shard_rec, recs, top_logV, top_thr, top_scratch;
     size_t dbg_x, dbg_lw, dbg_anc, dbg_A, dbg_xhat;
     size_t total;
 };
 
-Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags) {
+Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags, uint32_t world, int Sglobal) {
     Layout L;
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -182,10 +189,16 @@ Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags) {
     L.est = take(4 * 8 * 8);
     L.ticket = take(16);
     L.y = take(64);
+    L.shard_rec = take((size_t)(1 + PS) * 8);
+    L.recs = take((size_t)world * (1 + PS) * 8);
+    L.top_logV = take((size_t)world * 8);
+    L.top_thr = take((size_t)world * 4);
+    L.top_scratch = take((size_t)2 * world * PS * 8);
     const bool dbg = flags & PF_FLAG_DEBUG;
     L.dbg_x = take(dbg ? xb : 0);
     L.dbg_lw = take(dbg ? N * 4 : 0);
-    L.dbg_anc = take(dbg ? (size_t)N * S * 4 : 0);
+    L.dbg_anc = take(dbg ? (size_t)N * Sglobal * 4 : 0);
+    (void)S;
     L.dbg_A = take(dbg ? N * 4 : 0);
     L.dbg_xhat = take(xb);
     L.total = off;
@@ -196,8 +209,12 @@ Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags) {
 
 struct pf_handle {
     ModelParams mp;
-    uint64_t N;
-    uint32_t M, b, m, S;
+    uint64_t N;                    // particles of this shard (= Nglobal when world == 1)
+    uint32_t M, b, m, S;           // m, S: groups and local stages of this shard
+    uint64_t Nglobal;
+    uint32_t Sglobal, rank, world, L, pos0;
+    uint32_t step_n;               // time index of the step in progress / last completed
+    bool top_done;
     uint64_t seed;
     uint32_t flags;
     Plan plan;
@@ -391,6 +408,7 @@ static void launch_cascade_k(pf_handle* h) {
     c.part = h->at<double>(h->lay.part);
     c.scratch = h->at<double>(h->lay.scratch);
     c.est = h->at<double>(h->lay.est);
+    c.shard_rec = h->world > 1 ? h->at<double>(h->lay.shard_rec) : nullptr;
     c.ticket = h->at<uint32_t>(h->lay.ticket);
     c.N = h->N;
     c.m = h->m;
@@ -428,6 +446,7 @@ static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
     a.y_dev = y_dev;
     for (int k = 0; k < 8; ++k) a.y[k] = (y_host && k < h->mp.dy) ? y_host[k] : 0.0f;
     a.N = h->N;
+    a.pos0 = h->pos0;
     a.m = h->m;
     a.M = h->M;
     a.b = h->b;
@@ -461,6 +480,7 @@ static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
     c.key = a.key;
     c.n = h->n;
     c.N = h->N;
+    c.pos0 = h->pos0;
     c.m = h->m;
     c.M = h->M;
     c.b = h->b;
@@ -504,8 +524,10 @@ static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
         h->cur = xs;
         h->a_identity = true;
     }
+    h->step_n = h->n;
     h->n += 1;
-    h->have_step = true;
+    h->have_step = h->world == 1;
+    h->top_done = h->world == 1;
     h->last_launches = launches;
     return check_cuda(h, "pf_step");
 }
@@ -515,33 +537,60 @@ static int dispatch_step(pf_handle* h, const float* yh, const float* yd) { retur
 // ---------------------------------------------------------------------------------------
 extern "C" {
 
-size_t pf_workspace_bytes(const pf_model* model, uint64_t N, uint32_t M, uint32_t flags) {
-    std::string err;
-    if (!validate_model(model, &err) || !validate_topology(N, M, &err)) return 0;
-    Plan p;
-    if (!make_plan(model->d, N, M, &p, &err)) return 0;
-    return make_layout(p, N, M, flags).total;
+static bool shard_geometry(uint64_t N, uint32_t M, int rank, int world, uint64_t* Nloc, std::string* err) {
+    if (world < 1 || ilog2_exact((uint64_t)world) < 0 || rank < 0 || rank >= world) {
+        *err = "world must be a power of two >= 1 and 0 <= rank < world";
+        return false;
+    }
+    const uint64_t m = N / M;
+    if (m % (uint64_t)world != 0 || m / (uint64_t)world < 2) {
+        *err = "each shard needs >= 2 groups (m / world >= 2)";
+        return false;
+    }
+    *Nloc = N / (uint64_t)world;
+    return true;
 }
 
-int pf_init(const pf_model* model, uint64_t N, uint32_t M, uint64_t seed, uint32_t flags, void* dev_ws,
-            size_t ws_bytes, void* cuda_stream, pf_handle** out) {
+static size_t workspace_bytes(const pf_model* model, uint64_t N, uint32_t M, uint32_t flags, int world,
+                              std::string* err) {
+    uint64_t Nloc = 0;
+    if (!validate_model(model, err) || !validate_topology(N, M, err) || !shard_geometry(N, M, 0, world, &Nloc, err))
+        return 0;
+    Plan p;
+    if (!make_plan(model->d, Nloc, M, &p, err, world > 1, N)) return 0;
+    return make_layout(p, Nloc, M, flags, (uint32_t)world, ilog2_exact(N / M)).total;
+}
+
+static int init_core(const pf_model* model, uint64_t N, uint32_t M, uint64_t seed, uint32_t flags, int rank,
+                     int world, void* dev_ws, size_t ws_bytes, void* cuda_stream, pf_handle** out) {
     if (!out) return fail(nullptr, PF_EINVAL, "out is NULL");
     *out = nullptr;
     std::string err;
+    uint64_t Nloc = 0;
     if (!validate_model(model, &err)) return fail(nullptr, PF_EINVAL, err);
     if (!validate_topology(N, M, &err)) return fail(nullptr, PF_EINVAL, err);
+    if (!shard_geometry(N, M, rank, world, &Nloc, &err)) return fail(nullptr, PF_EINVAL, err);
     Plan p;
-    if (!make_plan(model->d, N, M, &p, &err)) return fail(nullptr, PF_EINVAL, err);
-    Layout L = make_layout(p, N, M, flags);
+    if (!make_plan(model->d, Nloc, M, &p, &err, world > 1, N)) return fail(nullptr, PF_EINVAL, err);
+    const int Sglobal = ilog2_exact(N / M);
+    Layout L = make_layout(p, Nloc, M, flags, (uint32_t)world, Sglobal);
     if (!dev_ws || ws_bytes < L.total) return fail(nullptr, PF_EWORKSPACE, "workspace too small");
     if (reinterpret_cast<uintptr_t>(dev_ws) & 255u) return fail(nullptr, PF_EWORKSPACE, "workspace not 256-byte aligned");
     pf_handle* h = new pf_handle();
     h->mp = to_params(model);
-    h->N = N;
+    h->N = Nloc;
     h->M = M;
     h->b = (uint32_t)ilog2_exact(M);
-    h->m = (uint32_t)(N / M);
+    h->m = (uint32_t)(Nloc / M);
     h->S = (uint32_t)ilog2_exact(h->m);
+    h->Nglobal = N;
+    h->Sglobal = (uint32_t)Sglobal;
+    h->rank = (uint32_t)rank;
+    h->world = (uint32_t)world;
+    h->L = (uint32_t)ilog2_exact((uint64_t)world);
+    h->pos0 = (uint32_t)(Nloc * (uint64_t)rank);
+    h->step_n = 0;
+    h->top_done = false;
     h->seed = seed;
     h->flags = flags;
     h->plan = p;
@@ -560,9 +609,10 @@ int pf_init(const pf_model* model, uint64_t N, uint32_t M, uint64_t seed, uint32
         InitArgs ia;
         ia.mp = h->mp;
         ia.key = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
-        ia.N = N;
+        ia.N = h->N;
+        ia.pos0 = h->pos0;
         ia.x = h->X(0);
-        const uint32_t grid = (uint32_t)std::min<uint64_t>((N / 4 + 255) / 256, 148ull * 16);
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((h->N / 4 + 255) / 256, 148ull * 16);
         launch_init(p.D, h->mp.kind, LaunchCfg{grid, 256u, 0u, h->stream}, ia);
     }
     const cudaError_t e = cudaGetLastError();
@@ -574,8 +624,105 @@ int pf_init(const pf_model* model, uint64_t N, uint32_t M, uint64_t seed, uint32
     return PF_OK;
 }
 
+size_t pf_workspace_bytes(const pf_model* model, uint64_t N, uint32_t M, uint32_t flags) {
+    std::string err;
+    return workspace_bytes(model, N, M, flags, 1, &err);
+}
+
+size_t pf_workspace_bytes_sharded(const pf_model* model, uint64_t N, uint32_t M, uint32_t flags, int world) {
+    std::string err;
+    return workspace_bytes(model, N, M, flags, world, &err);
+}
+
+int pf_init(const pf_model* model, uint64_t N, uint32_t M, uint64_t seed, uint32_t flags, void* dev_ws,
+            size_t ws_bytes, void* cuda_stream, pf_handle** out) {
+    return init_core(model, N, M, seed, flags, 0, 1, dev_ws, ws_bytes, cuda_stream, out);
+}
+
+int pf_init_sharded(const pf_model* model, uint64_t N, uint32_t M, uint64_t seed, uint32_t flags, int rank, int world,
+                    void* dev_ws, size_t ws_bytes, void* cuda_stream, pf_handle** out) {
+    return init_core(model, N, M, seed, flags, rank, world, dev_ws, ws_bytes, cuda_stream, out);
+}
+
+int pf_step_local(pf_handle* h, const float* y_host, const float* y_dev) {
+    if (!h || (!y_host && !y_dev)) return fail(h, PF_EINVAL, "NULL argument");
+    if (y_host)
+        for (int k = 0; k < h->mp.dy; ++k)
+            if (!std::isfinite(y_host[k])) return fail(h, PF_EOBS, "non-finite observation");
+    return dispatch_step(h, y_host, y_dev);
+}
+
+int pf_shard_record(pf_handle* h, const double** dev_rec) {
+    if (!h || !dev_rec) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
+    *dev_rec = h->at<double>(h->lay.shard_rec);
+    return PF_OK;
+}
+
+int pf_step_top(pf_handle* h, const double* dev_all_recs) {
+    if (!h || !dev_all_recs) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
+    TopArgs t;
+    t.recs = dev_all_recs;
+    t.top_logV = h->at<double>(h->lay.top_logV);
+    t.top_thr = h->at<uint32_t>(h->lay.top_thr);
+    t.est = h->at<double>(h->lay.est);
+    t.scratch = h->at<double>(h->lay.top_scratch);
+    t.Nglobal = h->Nglobal;
+    t.G = h->world;
+    t.L = h->L;
+    t.b = h->b;
+    h->mark(PF_KERNEL_TOP, true);
+    launch_top(h->plan.D, LaunchCfg{1u, 1024u, 0u, h->stream}, t);
+    h->mark(PF_KERNEL_TOP, false);
+    h->top_done = true;
+    h->have_step = true;
+    return check_cuda(h, "pf_step_top");
+}
+
+int pf_cross_buffer(pf_handle* h, const void** dev_states, size_t* bytes) {
+    if (!h || !dev_states || !bytes) return fail(h, PF_EINVAL, "NULL argument");
+    *dev_states = h->X(h->cur);
+    *bytes = (size_t)h->N * (size_t)h->plan.D * 4u;
+    return PF_OK;
+}
+
+int pf_cross_stage(pf_handle* h, int t, const void* dev_partner_states) {
+    // Stream-ordered: k_cross reads the stage threshold that k_top wrote on this stream.
+    if (!h || !dev_partner_states) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world < 2 || t < 1 || (uint32_t)t > h->L) return fail(h, PF_EINVAL, "cross stage out of range");
+    if (!h->top_done) return fail(h, PF_ESTATE, "pf_step_top must run first");
+    const uint32_t* top_thr = h->at<uint32_t>(h->lay.top_thr);
+    const uint32_t G = h->world;
+    CrossArgs c;
+    c.key = {(uint32_t)(h->seed & 0xffffffffu), (uint32_t)(h->seed >> 32)};
+    c.n = h->step_n;
+    c.s = h->S + (uint32_t)t;
+    c.t = (uint32_t)t;
+    c.rank = h->rank;
+    c.b = h->b;
+    c.M = h->M;
+    c.Nloc = h->N;
+    c.pos0 = h->pos0;
+    c.pos0_partner = (uint32_t)(h->N * (uint64_t)(h->rank ^ (1u << (t - 1))));
+    c.thr = top_thr + (G - (G >> (t - 1))) + (h->rank >> t);
+    c.own_in = h->X(h->cur);
+    c.partner_in = dev_partner_states;
+    c.out = h->X(h->cur ^ 1);
+    c.dbg_anc = (h->flags & PF_FLAG_DEBUG) ? h->at<int32_t>(h->lay.dbg_anc) : nullptr;
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((h->N / 4 + 255) / 256, (uint64_t)148 * 8);
+    const int D = h->plan.D;
+    h->mark(PF_KERNEL_CROSS, true);
+    launch_cross(D == 1 ? kPayloadF1 : (D == 2 ? kPayloadF2 : (D == 4 ? kPayloadF4 : kPayloadF8)),
+                 (h->flags & PF_FLAG_DEBUG) != 0, LaunchCfg{grid, 256u, 0u, h->stream}, c);
+    h->mark(PF_KERNEL_CROSS, false);
+    h->cur ^= 1;
+    return check_cuda(h, "pf_cross_stage");
+}
+
 int pf_step(pf_handle* h, const float* y_host) {
     if (!h || !y_host) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world > 1) return fail(h, PF_ESTATE, "sharded handle: use pf_step_local / pf_step_top / pf_cross_stage");
     for (int k = 0; k < h->mp.dy; ++k)
         if (!std::isfinite(y_host[k])) return fail(h, PF_EOBS, "non-finite observation");
     return dispatch_step(h, y_host, nullptr);
@@ -583,6 +730,7 @@ int pf_step(pf_handle* h, const float* y_host) {
 
 int pf_step_dev(pf_handle* h, const float* y_dev) {
     if (!h || !y_dev) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world > 1) return fail(h, PF_ESTATE, "sharded handle: use pf_step_local / pf_step_top / pf_cross_stage");
     return dispatch_step(h, nullptr, y_dev);
 }
 
@@ -653,10 +801,11 @@ int pf_debug_ptr(pf_handle* h, int what, int stage, void** dev_out) {
         case PF_DBG_X: *dev_out = h->at<float>(h->lay.dbg_x); return PF_OK;
         case PF_DBG_LOGW: *dev_out = h->at<float>(h->lay.dbg_lw); return PF_OK;
         case PF_DBG_ANC_STAGE:
-            if (stage < 1 || stage > (int)h->S) return fail(h, PF_EINVAL, "stage out of range");
+            if (stage < 1 || stage > (int)h->Sglobal) return fail(h, PF_EINVAL, "stage out of range");
             *dev_out = h->at<int32_t>(h->lay.dbg_anc) + (size_t)(stage - 1) * h->N;
             return PF_OK;
         case PF_DBG_ANC_FINAL: {
+            if (h->world > 1) return fail(h, PF_ESTATE, "composed ancestors span shards: use the stage tables");
             int32_t* A = h->at<int32_t>(h->lay.dbg_A);
             launch_debug_compose(LaunchCfg{1024u, 256u, 0u, h->stream}, h->at<int32_t>(h->lay.dbg_anc), h->N, h->S, A);
             *dev_out = A;

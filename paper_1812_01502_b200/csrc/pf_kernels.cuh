@@ -83,7 +83,8 @@ __device__ __forceinline__ void store_quad(float* __restrict__ x, uint64_t i0, c
 struct InitArgs {
     ModelParams mp;
     Key key;
-    uint64_t N;
+    uint64_t N;     // particles of this shard
+    uint32_t pos0;  // global index of its first particle (multiple of 4)
     float* x;
 };
 
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(256) k_init(const __grid_constant__ InitArgs a
         float z[4 * D], v[4 * D];
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            const uint4 blk = rng_block(a.key, (uint32_t)(q * D + j), 0u, kDomainInit, 0u);
+            const uint4 blk = rng_block(a.key, (uint32_t)(((a.pos0 >> 2) + q) * D + j), 0u, kDomainInit, 0u);
             normals4(blk, z + 4 * j);
         }
 #pragma unroll
@@ -118,7 +119,7 @@ struct TileGeom {
 template <bool DBG, int QPT>
 __device__ __forceinline__ void tile_stage(const Key key, uint32_t n, uint32_t s, uint32_t st, const TileGeom& G,
                                            const uint32_t* __restrict__ thr_s, const uint16_t* Lo, uint16_t* Ln,
-                                           uint32_t nq, int32_t* __restrict__ dbg_s) {
+                                           uint32_t nq, int32_t* __restrict__ dbg_s, uint32_t pos0) {
     const uint32_t b = G.b, mask = G.M - 1u, bit = 1u << st;
 #pragma unroll
     for (int it = 0; it < QPT; ++it) {
@@ -129,7 +130,7 @@ __device__ __forceinline__ void tile_stage(const Key key, uint32_t n, uint32_t s
         if (G.M >= 4u) {
             const uint32_t j = l0 >> b;
             const uint32_t g = G.gof(j);
-            const uint32_t c0 = ((g << b) | (l0 & mask)) >> 2;
+            const uint32_t c0 = (pos0 + ((g << b) | (l0 & mask))) >> 2;
             const uint4 blk = rng_block(key, c0, n, kDomainResample, s);
             const uint32_t P = thr_s[j >> (st + 1)];
             const uint32_t bl = (j & ~bit) << b, br = (j | bit) << b;
@@ -141,7 +142,7 @@ __device__ __forceinline__ void tile_stage(const Key key, uint32_t n, uint32_t s
             for (int e = 0; e < 4; ++e) {
                 const uint32_t l = l0 + e;
                 const uint32_t j = l >> 1;
-                const uint32_t gi = (G.gof(j) << 1) | (l & 1u);
+                const uint32_t gi = pos0 + ((G.gof(j) << 1) | (l & 1u));
                 const uint4 blk = rng_block(key, gi >> 2, n, kDomainResample, s);
                 const uint32_t r = word_of(blk, (int)(gi & 3u));
                 const uint32_t P = thr_s[j >> (st + 1)];
@@ -153,7 +154,7 @@ __device__ __forceinline__ void tile_stage(const Key key, uint32_t n, uint32_t s
         *reinterpret_cast<uint2*>(Ln + l0) = make_uint2((uint32_t)v0 | ((uint32_t)v1 << 16), (uint32_t)v2 | ((uint32_t)v3 << 16));
         if constexpr (DBG) {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) dbg_s[G.gpos(l0 + e)] = (int32_t)G.gpos(res[e]);
+            for (int e = 0; e < 4; ++e) dbg_s[G.gpos(l0 + e)] = (int32_t)(pos0 + G.gpos(res[e]));
         }
     }
 }
@@ -194,7 +195,8 @@ struct Pass1Args {
     int do_mutate;
     const float* y_dev;  // if non-null, y is read from device memory
     float y[8];
-    uint64_t N;
+    uint64_t N;           // particles of this shard
+    uint32_t pos0;        // global index of the shard's first particle (RNG counters)
     uint32_t m, M, b, S, k1, P1, T1;
     Pass1Smem sl;         // shared-memory layout (pass1_smem)
     const float* x_in;    // xhat_{n-1} source (or x_0)
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(1024) k_pass1(const __grid_constant__ Pass1Arg
             float z[4 * D];
 #pragma unroll
             for (int j = 0; j < D; ++j) {
-                const uint4 blk = rng_block(a.key, (i0 >> 2) * D + j, a.n, kDomainMutate, 0u);
+                const uint4 blk = rng_block(a.key, ((a.pos0 + i0) >> 2) * D + j, a.n, kDomainMutate, 0u);
                 normals4(blk, z + 4 * j);
             }
 #pragma unroll
@@ -422,7 +424,7 @@ __global__ void __launch_bounds__(1024) k_pass1(const __grid_constant__ Pass1Arg
         for (int it = 0; it < QPT; ++it) {
             const uint32_t q = tid + it * threads;
             const bool valid = q < nq;
-            const uint4 blk = rng_block(a.key, (base >> 2) + q, a.n, kDomainResample, 1u);
+            const uint4 blk = rng_block(a.key, ((a.pos0 + base) >> 2) + q, a.n, kDomainResample, 1u);
             const uint32_t pb = valid ? (((4u * q) >> (b + 1)) << (b + 1)) : 0u;
             const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
 #pragma unroll
@@ -444,8 +446,8 @@ __global__ void __launch_bounds__(1024) k_pass1(const __grid_constant__ Pass1Arg
             if (q >= nq) continue;
             if constexpr (DBG)
                 reinterpret_cast<int4*>(a.dbg_anc + base + 4u * q)[0] =
-                    make_int4((int)(base + lo[it][0]), (int)(base + lo[it][1]), (int)(base + lo[it][2]),
-                              (int)(base + lo[it][3]));
+                    make_int4((int)(a.pos0 + base + lo[it][0]), (int)(a.pos0 + base + lo[it][1]),
+                              (int)(a.pos0 + base + lo[it][2]), (int)(a.pos0 + base + lo[it][3]));
             *reinterpret_cast<uint2*>(L1 + 4u * q) =
                 make_uint2(lo[it][0] | (lo[it][1] << 16), lo[it][2] | (lo[it][3] << 16));
         }
@@ -461,12 +463,12 @@ __global__ void __launch_bounds__(1024) k_pass1(const __grid_constant__ Pass1Arg
 #pragma unroll
         for (int k = 1; k < PS; ++k) W[k * 33 + lane] = (k < 2 + 2 * D) ? acc[k] * f : acc[k];
         __syncwarp();
-        if (lane < (uint32_t)(PS - 1)) {
-            const float* row = W + (lane + 1) * 33;
+        for (uint32_t k = lane + 1; k < (uint32_t)PS; k += 32u) {  // PS - 1 can exceed 32 (d = 8)
+            const float* row = W + k * 33;
             float sacc = 0.0f;
 #pragma unroll 8
             for (int j = 0; j < 32; ++j) sacc += row[j];
-            red[warp * PS + lane + 1] = sacc;
+            red[warp * PS + k] = sacc;
         }
         if (lane == 0) red[warp * PS] = wmax;
     }
@@ -474,21 +476,23 @@ __global__ void __launch_bounds__(1024) k_pass1(const __grid_constant__ Pass1Arg
 
     // warp 0: tile estimate partial, V levels 1..k1, thresholds (stage s uses level s-1)
     if (warp == 0) {
-        if (lane < (uint32_t)PS) {
+        {
             float tmax = -CUDART_INF_F;
             for (uint32_t wv = 0; wv < nwarps; ++wv) tmax = fmaxf(tmax, red[wv * PS]);
-            double v;
-            if (lane == 0) {
-                v = (double)tmax;
-            } else {
-                v = 0.0;
-                for (uint32_t wv = 0; wv < nwarps; ++wv) {
-                    const float wm = red[wv * PS];
-                    const float f = (lane < (uint32_t)(2 + 2 * D)) ? (wm == -CUDART_INF_F ? 0.0f : expf(wm - tmax)) : 1.0f;
-                    v += (double)(red[wv * PS + lane] * f);
+            for (uint32_t k = lane; k < (uint32_t)PS; k += 32u) {  // PS can exceed 32 (d = 8)
+                double v;
+                if (k == 0) {
+                    v = (double)tmax;
+                } else {
+                    v = 0.0;
+                    for (uint32_t wv = 0; wv < nwarps; ++wv) {
+                        const float wm = red[wv * PS];
+                        const float f = (k < (uint32_t)(2 + 2 * D)) ? (wm == -CUDART_INF_F ? 0.0f : expf(wm - tmax)) : 1.0f;
+                        v += (double)(red[wv * PS + k] * f);
+                    }
                 }
+                a.part[(uint64_t)tile * PS + k] = v;
             }
-            a.part[(uint64_t)tile * PS + lane] = v;
         }
         const float log2M = logf((float)(2u * M));
         for (uint32_t p = lane; p < T1 / 2; p += 32u) {
@@ -527,7 +531,7 @@ __global__ void __launch_bounds__(1024) k_pass1(const __grid_constant__ Pass1Arg
                 const uint32_t q = tid + it * threads;
                 if (q >= nq) continue;
                 const uint32_t l0 = 4u * q;
-                const uint4 blk = rng_block(a.key, (base >> 2) + q, a.n, kDomainResample, s);
+                const uint4 blk = rng_block(a.key, ((a.pos0 + base) >> 2) + q, a.n, kDomainResample, s);
                 const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
                 uint32_t res[4];
                 if (M >= 4u) {
@@ -547,8 +551,8 @@ __global__ void __launch_bounds__(1024) k_pass1(const __grid_constant__ Pass1Arg
                 *reinterpret_cast<uint2*>(Ts + l0) = make_uint2(res[0] | (res[1] << 16), res[2] | (res[3] << 16));
                 if constexpr (DBG)
                     reinterpret_cast<int4*>(a.dbg_anc + (uint64_t)(s - 1) * a.N + base + l0)[0] =
-                        make_int4((int)(base + res[0]), (int)(base + res[1]), (int)(base + res[2]),
-                                  (int)(base + res[3]));
+                        make_int4((int)(a.pos0 + base + res[0]), (int)(a.pos0 + base + res[1]),
+                                  (int)(a.pos0 + base + res[2]), (int)(a.pos0 + base + res[3]));
             }
         }
     }
@@ -598,7 +602,8 @@ struct CascadeArgs {
     uint32_t* thr;
     const double* part;  // NT tile partials
     double* scratch;     // >= NT + 2 partials (tree levels)
-    double* est;         // outputs: filter[2D], predict[2D]
+    double* est;         // outputs: filter[2D], predict[2D] (single shard)
+    double* shard_rec;   // sharded runs: {log V at level S (= S_loc), root partial[2+4D]}
     uint32_t* ticket;
     uint64_t N;
     uint32_t m, S, k1, b, NT, LPC;
@@ -709,6 +714,13 @@ __global__ void __launch_bounds__(kCascadeThreads) k_cascade(const __grid_consta
     double* roots = a.scratch + (uint64_t)(a.NT / 2) * PS;
     double* fin = a.scratch;  // reuse (all CTAs are done with their subtrees)
     tree_combine<D>(roots, R, fin);
+    if (a.shard_rec) {  // this shard's root record for the cross-shard top levels
+        if (tid == 0) a.shard_rec[0] = a.logV[level_offset(a.m, (int)a.S)];
+        if (tid < PS) a.shard_rec[1 + tid] = fin[tid];
+        __syncthreads();
+        if (tid == 0) *a.ticket = 0u;
+        return;
+    }
     if (tid == 0) {
         const double sw = fin[1];
         for (int k = 0; k < D; ++k) {
@@ -725,7 +737,8 @@ __global__ void __launch_bounds__(kCascadeThreads) k_cascade(const __grid_consta
 struct ComposeArgs {
     Key key;
     uint32_t n;
-    uint64_t N;
+    uint64_t N;     // particles of this shard
+    uint32_t pos0;  // global index of the shard's first particle
     uint32_t m, M, b, s0, k, P, lowbits;
     const void* pin;
     void* pout;
@@ -797,7 +810,7 @@ __global__ void __launch_bounds__(1024) k_compose(const __grid_constant__ Compos
         __syncthreads();
         const uint32_t s = a.s0 + st;
         tile_stage<DBG, QPT>(a.key, a.n, s, st, G, ths + ((1u << k) - (1u << (k - st))), Lo, Ln, nq,
-                             DBG ? a.dbg_anc + (uint64_t)(s - 1) * a.N : nullptr);
+                             DBG ? a.dbg_anc + (uint64_t)(s - 1) * a.N : nullptr, a.pos0);
         uint16_t* tmp = Lo;
         Lo = Ln;
         Ln = tmp;
@@ -896,7 +909,7 @@ __global__ void __launch_bounds__(1024) k_move(const __grid_constant__ ComposeAr
             uint32_t res[4];
             if (M >= 4u) {
                 const uint32_t j = l0 >> b;
-                const uint32_t c0 = ((G.gof(j) << b) | (l0 & mask)) >> 2;
+                const uint32_t c0 = (a.pos0 + ((G.gof(j) << b) | (l0 & mask))) >> 2;
                 const uint4 blk = rng_block(a.key, c0, a.n, kDomainResample, s);
                 const uint32_t Pt = thr_s[j >> (st + 1)];
                 const uint32_t bl = (j & ~bit) << b, br = (j | bit) << b;
@@ -908,7 +921,7 @@ __global__ void __launch_bounds__(1024) k_move(const __grid_constant__ ComposeAr
                 for (int e = 0; e < 4; ++e) {
                     const uint32_t l = l0 + e;
                     const uint32_t j = l >> 1;
-                    const uint32_t gi = (G.gof(j) << 1) | (l & 1u);
+                    const uint32_t gi = a.pos0 + ((G.gof(j) << 1) | (l & 1u));
                     const uint4 blk = rng_block(a.key, gi >> 2, a.n, kDomainResample, s);
                     const uint32_t r = word_of(blk, (int)(gi & 3u));
                     const uint32_t jj = ((r >> 1) < thr_s[j >> (st + 1)]) ? (j & ~bit) : (j | bit);
@@ -919,7 +932,7 @@ __global__ void __launch_bounds__(1024) k_move(const __grid_constant__ ComposeAr
             if constexpr (DBG) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
-                    a.dbg_anc[(uint64_t)(s - 1) * a.N + G.gpos(l0 + e)] = (int32_t)G.gpos(res[e]);
+                    a.dbg_anc[(uint64_t)(s - 1) * a.N + G.gpos(l0 + e)] = (int32_t)(a.pos0 + G.gpos(res[e]));
             }
         }
     }
@@ -946,6 +959,113 @@ __global__ void __launch_bounds__(1024) k_move(const __grid_constant__ ComposeAr
         } else {
 #pragma unroll
             for (int e = 0; e < 4; ++e) pout[G.gpos(l0 + e)] = o.v[e];
+        }
+    }
+}
+
+// -------------------------------------------------------------------------------------
+// Sharded runs (G = 2^L GPUs, shard r owns groups [r m/G, (r+1) m/G)).
+//
+// k_top: from the G shard records (rank order) every rank computes, identically, the V
+// levels S_loc+1..S (same log-domain pair means and operand order as k_cascade, so the
+// values are bitwise those of a single-GPU run), the cross-stage side thresholds, and the
+// estimate (perfect binary tree over the shard partials = the upper levels of the
+// single-GPU tree over tiles).  Top level t (= stage S_loc + t) has G >> t entries at
+// offset G - (G >> (t-1)).
+struct TopArgs {
+    const double* recs;  // G x (1 + PS)
+    double* top_logV;    // G - 1
+    uint32_t* top_thr;   // G - 1
+    double* est;
+    double* scratch;     // >= 2 G partials
+    uint64_t Nglobal;
+    uint32_t G, L, b;
+};
+
+template <int D>
+__global__ void __launch_bounds__(1024) k_top(const __grid_constant__ TopArgs a) {
+    constexpr int PS = 2 + 4 * D;
+    __shared__ double vb[1024];
+    const uint32_t tid = threadIdx.x, G = a.G;
+    for (uint32_t i = tid; i < G; i += blockDim.x) vb[i] = a.recs[(uint64_t)i * (1 + PS)];
+    __syncthreads();
+    for (uint32_t t = 1, cnt = G / 2; t <= a.L; ++t, cnt >>= 1) {
+        double nv = 0.0;
+        const bool act = tid < cnt;
+        if (act) {
+            const double vl = vb[2 * tid], vr = vb[2 * tid + 1];
+            nv = log_pair_mean(vl, vr);
+            a.top_logV[(G - (G >> (t - 1))) + tid] = nv;
+            a.top_thr[(G - (G >> (t - 1))) + tid] = side_threshold(vl, vr, (int)a.b);
+        }
+        __syncthreads();
+        if (act) vb[tid] = nv;
+        __syncthreads();
+    }
+    // estimate: perfect binary tree over the G root partials (copied contiguous)
+    for (uint32_t i = tid; i < G * PS; i += blockDim.x) {
+        const uint32_t r = i / PS, c = i % PS;
+        a.scratch[G * PS + i] = a.recs[(uint64_t)r * (1 + PS) + 1 + c];
+    }
+    __syncthreads();
+    tree_combine<D>(a.scratch + G * PS, G, a.scratch);
+    if (tid == 0) {
+        const double* fin = a.scratch;
+        const double sw = fin[1];
+        for (int k = 0; k < D; ++k) {
+            a.est[k] = fin[2 + k] / sw;
+            a.est[D + k] = fin[2 + D + k] / sw;
+            a.est[2 * D + k] = fin[2 + 2 * D + k] / (double)a.Nglobal;
+            a.est[3 * D + k] = fin[2 + 3 * D + k] / (double)a.Nglobal;
+        }
+    }
+}
+
+// k_cross: cross-shard stage s = S_loc + t.  Shard r pairs with r ^ 2^{t-1}; a particle of
+// local group gl pairs with the SAME local group of the partner.  Every output's draw
+// (side, index) is counter-based, so each output reads its source state from this
+// shard's or the partner's stage-(s-1) buffer (the partner's arrives whole over NVLink).
+struct CrossArgs {
+    Key key;
+    uint32_t n, s, t, rank, b, M;
+    uint64_t Nloc;
+    uint32_t pos0, pos0_partner;
+    const uint32_t* thr;    // the stage threshold (device): top_thr entry of block rank >> t
+    const void* own_in;
+    const void* partner_in;
+    void* out;
+    int32_t* dbg_anc;       // this shard's stage tables (global source positions)
+};
+
+template <typename T, bool DBG>
+__global__ void __launch_bounds__(256) k_cross(const __grid_constant__ CrossArgs a) {
+    const T* own = reinterpret_cast<const T*>(a.own_in);
+    const T* par = reinterpret_cast<const T*>(a.partner_in);
+    T* out = reinterpret_cast<T*>(a.out);
+    const uint32_t mask = a.M - 1u;
+    const bool own_is_low = ((a.rank >> (a.t - 1)) & 1u) == 0u;
+    const uint32_t P = __ldg(a.thr);
+    const uint64_t nq = a.Nloc >> 2;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t l0 = (uint32_t)(4u * q);
+        const uint4 blk = rng_block(a.key, (a.pos0 + l0) >> 2, a.n, kDomainResample, a.s);
+        const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
+        Vec4<T> o;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t l = l0 + e;
+            const bool low = (r[e] >> a.b) < P;
+            const bool from_own = (low == own_is_low);
+            const uint32_t src = ((l >> a.b) << a.b) | (r[e] & mask);
+            o.v[e] = from_own ? own[src] : par[src];
+            if constexpr (DBG)
+                a.dbg_anc[(uint64_t)(a.s - 1) * a.Nloc + l] = (int32_t)((from_own ? a.pos0 : a.pos0_partner) + src);
+        }
+        if (a.M >= 4u) {
+            *reinterpret_cast<Vec4<T>*>(out + l0) = o;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) out[l0 + e] = o.v[e];
         }
     }
 }

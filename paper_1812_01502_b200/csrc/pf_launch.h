@@ -29,6 +29,8 @@ void launch_compose_dbg(int payload, int qpt, const LaunchCfg& c, const ComposeA
 void launch_move(int payload, bool dbg, int qpt, const LaunchCfg& c, const ComposeArgs& a);
 void launch_cascade(int D, const LaunchCfg& c, const CascadeArgs& a);
 void launch_init(int D, int kind, const LaunchCfg& c, const InitArgs& a);
+void launch_top(int D, const LaunchCfg& c, const TopArgs& a);
+void launch_cross(int payload, bool dbg, const LaunchCfg& c, const CrossArgs& a);
 void launch_debug_compose(const LaunchCfg& c, const int32_t* anc, uint64_t N, uint32_t S, int32_t* A);
 void launch_gather(int D, const LaunchCfg& c, const float* x, const int32_t* A, uint64_t N, float* out);
 

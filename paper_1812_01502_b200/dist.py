@@ -1,0 +1,215 @@
+"""Multi-GPU orchestration of the sharded BPF step.
+
+G = 2^L ranks, one GPU each; rank r owns particles [r N/G, (r+1) N/G).  One time step:
+
+    local      pf_step_local: mutate, weight, stages 1..S_loc (S_loc = S - L), all on-GPU
+    allgather  the G shard records {log V_{S_loc}, estimate partial}      (8 (3+4d) B each)
+    top        pf_step_top: V levels S_loc+1..S, cross thresholds, global estimate,
+               identical on every rank (same fp64 operations as one GPU)
+    cross      for t = 1..L: exchange the stage-(S_loc+t-1) state buffer with
+               partner = rank ^ 2^(t-1) (the butterfly partner of PAPER.md:562-568,
+               hypercube remark PAPER.md:1311), then pf_cross_stage(t)
+
+The orchestration is written against a small Backend interface (the C-ABI library on a
+GPU; tests substitute a CPU stand-in) and a Transport (torch.distributed over NCCL on
+GPUs, gloo on CPU, or an in-process loopback that runs G shards on one GPU).
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+
+def partner(rank: int, t: int) -> int:
+    """Partner rank at cross stage t (1-based): the ranks differ in bit t-1."""
+    return rank ^ (1 << (t - 1))
+
+
+def cross_stage_of(S: int, L: int, t: int) -> int:
+    """Global stage number of cross stage t (1..L)."""
+    return S - L + t
+
+
+def exchange_schedule(world: int) -> List[List[tuple]]:
+    """Per cross stage, the list of (rank, partner) pairs: a perfect matching of ranks."""
+    L = world.bit_length() - 1
+    if world < 1 or (1 << L) != world:
+        raise ValueError("world must be a power of two")
+    out = []
+    for t in range(1, L + 1):
+        pairs = sorted({(min(r, partner(r, t)), max(r, partner(r, t))) for r in range(world)})
+        out.append(pairs)
+    return out
+
+
+# ----------------------------------------------------------------------------- transports
+class TorchTransport:
+    """torch.distributed transport: all_gather for the records, isend/irecv pairs for the
+    state exchange (NCCL over NVLink on GPUs; gloo on CPU tensors)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+        self.nccl = dist.get_backend(group) == "nccl"
+        self._recv = {}
+
+    def allgather(self, rec):
+        import torch
+        if self.nccl:
+            out = torch.empty((self.world,) + tuple(rec.shape), dtype=rec.dtype, device=rec.device)
+            self.dist.all_gather_into_tensor(out, rec.contiguous(), group=self.group)
+            return out
+        outs = [torch.empty_like(rec) for _ in range(self.world)]
+        self.dist.all_gather(outs, rec, group=self.group)
+        return torch.stack(outs)
+
+    def exchange(self, send, peer: int):
+        import torch
+        key = (send.numel(), send.dtype, str(send.device), peer)
+        recv = self._recv.get(key)  # reused receive buffer: no per-step allocation
+        if recv is None:
+            recv = self._recv[key] = torch.empty_like(send)
+        if self.nccl:
+            ops = [self.dist.P2POp(self.dist.isend, send, peer, group=self.group),
+                   self.dist.P2POp(self.dist.irecv, recv, peer, group=self.group)]
+            for r in self.dist.batch_isend_irecv(ops):
+                r.wait()
+        else:
+            reqs = [self.dist.isend(send, peer, group=self.group), self.dist.irecv(recv, peer, group=self.group)]
+            for r in reqs:
+                r.wait()
+        return recv
+
+
+# ----------------------------------------------------------------------------- backend
+class LibBackend:
+    """One shard on the current GPU through the C-ABI (libpf.so)."""
+
+    def __init__(self, params: dict, N: int, M: int, seed: int, rank: int, world: int, debug: bool = False,
+                 stream=None):
+        import torch
+
+        from . import pf
+
+        self.torch = torch
+        self.pf = pf
+        self.params = params
+        self.N, self.M, self.rank, self.world = int(N), int(M), int(rank), int(world)
+        self.d = int(params["d"])
+        self.flags = pf.PF_FLAG_DEBUG if debug else 0
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        L = pf.lib()
+        m, keep = pf.make_model(params)
+        nbytes = int(L.pf_workspace_bytes_sharded(ctypes.byref(m), self.N, self.M, self.flags, self.world))
+        if nbytes == 0:
+            raise pf.PFError(pf.PF_EINVAL, "invalid sharded topology")
+        self.ws = torch.empty(nbytes + 256, dtype=torch.uint8, device="cuda")
+        base = self.ws.data_ptr()
+        self.ws_ptr = base + ((-base) % 256)
+        h = ctypes.c_void_p()
+        pf._check(L.pf_init_sharded(ctypes.byref(m), self.N, self.M, seed, self.flags, self.rank, self.world,
+                                    self.ws_ptr, nbytes, self.stream.cuda_stream, ctypes.byref(h)))
+        self.h = h
+        self.rec_len = 3 + 4 * self.d
+
+    def _view(self, ptr: int, nbytes: int, dtype):
+        off = ptr - self.ws.data_ptr()
+        return self.ws[off: off + nbytes].view(dtype)
+
+    def step_local(self, y):
+        yy = np.ascontiguousarray(y, dtype=np.float32)
+        self.pf._check(self.pf.lib().pf_step_local(self.h, yy.ctypes.data, None), self.h)
+        p = ctypes.c_void_p()
+        self.pf._check(self.pf.lib().pf_shard_record(self.h, ctypes.byref(p)), self.h)
+        return self._view(int(p.value), 8 * self.rec_len, self.torch.float64)
+
+    def step_top(self, all_recs):
+        all_recs = all_recs.contiguous()
+        self._keep = all_recs
+        self.pf._check(self.pf.lib().pf_step_top(self.h, all_recs.data_ptr()), self.h)
+
+    def cross_buffer(self):
+        p, n = ctypes.c_void_p(), ctypes.c_size_t()
+        self.pf._check(self.pf.lib().pf_cross_buffer(self.h, ctypes.byref(p), ctypes.byref(n)), self.h)
+        return self._view(int(p.value), int(n.value), self.torch.uint8)
+
+    def cross_stage(self, t: int, partner_buf):
+        self._keep_p = partner_buf
+        self.pf._check(self.pf.lib().pf_cross_stage(self.h, t, partner_buf.data_ptr()), self.h)
+
+    def step_local_dev(self, y_dev):
+        self.pf._check(self.pf.lib().pf_step_local(self.h, None, y_dev.data_ptr()), self.h)
+        p = ctypes.c_void_p()
+        self.pf._check(self.pf.lib().pf_shard_record(self.h, ctypes.byref(p)), self.h)
+        return self._view(int(p.value), 8 * self.rec_len, self.torch.float64)
+
+    def timing_enable(self, on: bool = True):
+        self.pf._check(self.pf.lib().pf_timing_enable(self.h, 1 if on else 0), self.h)
+
+    def timing_read(self):
+        pf = self.pf
+        ms = np.zeros(pf.PF_KERNEL_KINDS, np.float64)
+        n = np.zeros(pf.PF_KERNEL_KINDS, np.int32)
+        pf._check(pf.lib().pf_timing_read(self.h, ms.ctypes.data, n.ctypes.data), self.h)
+        return {pf.KERNEL_NAMES[k]: (float(ms[k]), int(n[k])) for k in range(pf.PF_KERNEL_KINDS)}
+
+    def estimate(self, phi=None, kind=None):
+        pf = self.pf
+        return pf.pf_estimate(self.h, self.d, phi or pf.PF_PHI_X, kind or pf.PF_EST_FILTER)
+
+    def debug_get(self, what: int, stage: int = 0) -> np.ndarray:
+        pf = self.pf
+        ptr = pf.pf_debug_ptr(self.h, what, stage)
+        nloc = self.N // self.world
+        if what in (pf.PF_DBG_X, pf.PF_DBG_XHAT):
+            t = self._view(ptr, nloc * self.d * 4, self.torch.float32).view(nloc, self.d)
+        elif what == pf.PF_DBG_LOGW:
+            t = self._view(ptr, nloc * 4, self.torch.float32)
+        elif what == pf.PF_DBG_ANC_STAGE:
+            t = self._view(ptr, nloc * 4, self.torch.int32)
+        else:
+            raise ValueError(what)
+        self.stream.synchronize()
+        return t.cpu().numpy()
+
+    def close(self):
+        if getattr(self, "h", None) is not None:
+            self.pf.lib().pf_destroy(self.h)
+            self.h = None
+
+
+# ----------------------------------------------------------------------------- steps
+def sharded_step(backend, transport, y, y_dev=None) -> None:
+    """One collective time step on this rank (every rank calls it with the same y; with
+    y_dev the observation is read from device memory)."""
+    rec = backend.step_local(y) if y_dev is None else backend.step_local_dev(y_dev)
+    backend.step_top(transport.allgather(rec))
+    world = transport.world
+    L = world.bit_length() - 1
+    for t in range(1, L + 1):
+        buf = backend.cross_buffer()
+        recv = transport.exchange(buf, partner(transport.rank, t))
+        backend.cross_stage(t, recv)
+
+
+def loopback_step(backends: Sequence, y) -> None:
+    """The same collective sequence for G shards held by one process on one GPU (the
+    exchange is a pointer hand-over; every kernel is stream-ordered, none waits on
+    another shard's kernel)."""
+    import torch
+    recs = [b.step_local(y) for b in backends]
+    allr = torch.stack([r for r in recs])
+    for b in backends:
+        b.step_top(allr)
+    world = len(backends)
+    L = world.bit_length() - 1
+    for t in range(1, L + 1):
+        bufs = [b.cross_buffer() for b in backends]  # all inputs taken before any stage runs
+        for r, b in enumerate(backends):
+            b.cross_stage(t, bufs[partner(r, t)])

@@ -68,15 +68,25 @@ def lib() -> ctypes.CDLL:
         L.pf_last_step_launches.argtypes = [vp]
         L.pf_timing_enable.argtypes = [vp, ctypes.c_int]
         L.pf_timing_read.argtypes = [vp, vp, vp]
+        L.pf_workspace_bytes_sharded.argtypes = [vp, u64, u32, u32, ctypes.c_int]
+        L.pf_workspace_bytes_sharded.restype = sz
+        L.pf_init_sharded.argtypes = [vp, u64, u32, u64, u32, ctypes.c_int, ctypes.c_int, vp, sz, vp,
+                                      ctypes.POINTER(vp)]
+        L.pf_step_local.argtypes = [vp, vp, vp]
+        L.pf_shard_record.argtypes = [vp, ctypes.POINTER(vp)]
+        L.pf_step_top.argtypes = [vp, vp]
+        L.pf_cross_buffer.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(sz)]
+        L.pf_cross_stage.argtypes = [vp, ctypes.c_int, vp]
         _lib = L
     return _lib
 
 
 EXPORTED = ["pf_workspace_bytes", "pf_init", "pf_step", "pf_step_dev", "pf_estimate", "pf_destroy",
             "pf_last_error", "pf_debug_get", "pf_debug_ptr", "pf_debug_set_state", "pf_last_step_launches",
-            "pf_timing_enable", "pf_timing_read"]
-PF_KERNEL_KINDS = 3
-KERNEL_NAMES = ("k_pass1", "k_cascade", "k_compose")
+            "pf_timing_enable", "pf_timing_read", "pf_workspace_bytes_sharded", "pf_init_sharded",
+            "pf_step_local", "pf_shard_record", "pf_step_top", "pf_cross_buffer", "pf_cross_stage"]
+PF_KERNEL_KINDS = 5
+KERNEL_NAMES = ("k_pass1", "k_cascade", "k_compose", "k_top", "k_cross")
 
 
 def _check(rc: int, h=None):

@@ -1,0 +1,137 @@
+"""Multi-rank orchestration of the sharded step (paper_1812_01502_b200/dist.py) with
+world_size = 2 over gloo on CPU.  The per-shard compute is a CPU stand-in built from the
+oracle (test infrastructure), so this checks the collective sequence itself: records
+gathered in rank order, butterfly partners, every cross-stage source lies in the own or
+the partner shard, the exchanged buffers, and the final shards = the oracle's x_hat."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1812_01502_b200 import dist as pfd
+from paper_1812_01502_b200 import inputs
+
+
+def test_partners_and_schedule():
+    for world in (2, 4, 8, 16):
+        L = world.bit_length() - 1
+        sched = pfd.exchange_schedule(world)
+        assert len(sched) == L
+        for t, pairs in enumerate(sched, start=1):
+            seen = sorted(r for pr in pairs for r in pr)
+            assert seen == list(range(world))  # a perfect matching
+            for a, b in pairs:
+                assert pfd.partner(a, t) == b and pfd.partner(b, t) == a
+                assert a ^ b == 1 << (t - 1)
+    assert pfd.cross_stage_of(22, 3, 1) == 20 and pfd.cross_stage_of(22, 3, 3) == 22
+    with pytest.raises(ValueError):
+        pfd.exchange_schedule(6)
+
+
+class OracleShard:
+    """CPU stand-in for LibBackend: one shard's view of the oracle's full step."""
+
+    def __init__(self, params, N, M, seed, rank, world):
+        from oracle import oracle as orc
+        self.orc = orc
+        self.params, self.N, self.M, self.seed = params, N, M, seed
+        self.rank, self.world = rank, world
+        self.d = int(params["d"])
+        self.m = N // M
+        self.S = int(np.log2(self.m))
+        self.L = world.bit_length() - 1
+        self.Sloc = self.S - self.L
+        self.nloc = N // world
+        self.pos0 = rank * self.nloc
+        self.xhat = orc.init(params, N, seed).astype(np.float32)
+        self.n = 0
+
+    def _states_at(self, s):
+        """Full-problem states at stage s positions: x[a_1(...a_s(i))]."""
+        pos = np.arange(self.N)
+        for st in range(s, 0, -1):
+            pos = self.r["a"][st - 1][pos]
+        return self.r["x"][pos].astype(np.float32)
+
+    def step_local(self, y):
+        self.r = self.orc.step(self.params, self.N, self.M, self.seed, self.n, y, self.xhat)
+        self.stage = self.Sloc
+        self.buf = self._states_at(self.Sloc)[self.pos0: self.pos0 + self.nloc].copy()
+        lv = self.r["logV"][self.orc.level_offset(self.m, self.Sloc) + self.rank]
+        return torch.tensor([lv] + [0.0] * (2 + 4 * self.d), dtype=torch.float64)
+
+    def step_top(self, all_recs):
+        for q in range(self.world):
+            want = self.r["logV"][self.orc.level_offset(self.m, self.Sloc) + q]
+            assert float(all_recs[q][0]) == want, "records not gathered in rank order"
+
+    def cross_buffer(self):
+        return torch.from_numpy(self.buf.view(np.uint8).reshape(-1).copy())
+
+    def cross_stage(self, t, recv):
+        s = self.Sloc + t
+        peer = pfd.partner(self.rank, t)
+        pbuf = recv.numpy().view(np.float32).reshape(self.nloc, self.d)
+        want = self._states_at(s - 1)[peer * self.nloc:(peer + 1) * self.nloc]
+        assert np.array_equal(pbuf, want), "wrong partner buffer"
+        a = self.r["a"][s - 1]
+        out = np.empty_like(self.buf)
+        for l in range(self.nloc):
+            src = int(a[self.pos0 + l])
+            owner = src // self.nloc
+            assert owner in (self.rank, peer), "cross-stage source outside own/partner shard"
+            out[l] = self.buf[src - self.pos0] if owner == self.rank else pbuf[src - peer * self.nloc]
+        self.buf = out
+
+    def finish(self):
+        full = self.r["xhat"].astype(np.float32)
+        assert np.array_equal(self.buf, full[self.pos0: self.pos0 + self.nloc])
+        self.xhat = full
+        self.n += 1
+
+
+def _worker(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        cfg = inputs.CONFIGS["C1"]
+        params = inputs.model_params(cfg)
+        N, M = 256, 16
+        be = OracleShard(params, N, M, 5, rank, world)
+        tr = pfd.TorchTransport()
+        _, ys = inputs.simulate(cfg, T=3)
+        for y in ys:
+            pfd.sharded_step(be, tr, y)
+            be.finish()
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_sharded_sequence(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(v == "ok" for v in res.values()), res

@@ -67,6 +67,7 @@ def _compare(orc, cfg_name, N, M, n, seed=1234, cloud_seed=99, outlier=0.0, xhat
     pu.check_estimate(g["filt"], o["filter"][:d], o["filter"][d:])
     pu.check_estimate(g["pred"], o["predict"][:d], o["predict"][d:])
     assert np.all(np.abs(g["filt2"] - o["filter"][d:]) <= 1e-4 * np.abs(o["filter"][d:]) + 1e-12)
+    assert np.all(np.abs(g["pred2"] - o["predict"][d:]) <= 1e-4 * np.abs(o["predict"][d:]) + 1e-12)
     return dict(stats=stats, flagged_paths=int(flagged.sum()), launches=g["launches"])
 
 

@@ -1,0 +1,45 @@
+"""Sharded step on one GPU through the loopback transport: G = 2, 4 shards must reproduce
+the single-GPU run BITWISE (counter-based draws on global indices, shard-aligned V and
+estimate trees) -- resampled particles, every stage's ancestor table and the estimates."""
+import numpy as np
+import pytest
+
+from paper_1812_01502_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+from paper_1812_01502_b200 import dist as pfd  # noqa: E402
+from paper_1812_01502_b200 import pf as pfb  # noqa: E402
+
+
+@pytest.mark.parametrize("name,N,M,G", [("C4", 1 << 16, 64, 2), ("C4", 1 << 16, 64, 4), ("C3", 1 << 15, 32, 4),
+                                        ("C2", 1 << 15, 256, 2), ("C3", 1 << 12, 2, 8), ("C1", 1024, 64, 8)])
+def test_loopback_matches_single_gpu(name, N, M, G):
+    cfg = inputs.CONFIGS[name]
+    p = inputs.model_params(cfg)
+    _, ys = inputs.simulate(cfg, T=3)
+    S = int(np.log2(N // M))
+    single = pfb.ParticleFilter(p, N, M, 21, debug=True)
+    shards = [pfd.LibBackend(p, N, M, 21, r, G, debug=True) for r in range(G)]
+    for n, y in enumerate(ys):
+        single.step(y)
+        pfd.loopback_step(shards, y)
+        for phi in (pfb.PF_PHI_X, pfb.PF_PHI_X2):
+            for kind in (pfb.PF_EST_FILTER, pfb.PF_EST_PREDICT):
+                e1 = single.estimate(phi, kind)
+                for b in shards:
+                    assert np.array_equal(b.estimate(phi, kind), e1), (n, phi, kind)
+        xs = single.debug_get(pfb.PF_DBG_XHAT)
+        xg = np.concatenate([b.debug_get(pfb.PF_DBG_XHAT) for b in shards])
+        assert np.array_equal(xs.reshape(xg.shape), xg), n
+        for s in range(1, S + 1):
+            a1 = single.debug_get(pfb.PF_DBG_ANC_STAGE, s)
+            ag = np.concatenate([b.debug_get(pfb.PF_DBG_ANC_STAGE, s) for b in shards])
+            assert np.array_equal(a1, ag), (n, s)
+    single.close()
+    for b in shards:
+        b.close()
