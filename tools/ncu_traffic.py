@@ -1,0 +1,33 @@
+"""Record per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) of the
+kernels in an `ncu --set full` report into profiles/ncu_traffic.json, keyed by workload,
+so bench.py can put it beside the algorithmic bytes in its roofline object.
+
+  python tools/ncu_traffic.py REPORT.ncu-rep WORKLOAD_KEY   (e.g. C4:N=268435456:M=64)
+Several launches of one kernel are averaged.
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+rep, key = sys.argv[1], sys.argv[2]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+r = csv.reader(io.StringIO(raw))
+hdr = next(r)
+units = dict(zip(hdr, next(r)))
+scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+acc = {}
+for row in r:
+    d = dict(zip(hdr, row))
+    name = d["Kernel Name"].replace("void ", "").split("<")[0].split("(")[0]
+    tot = sum(float(d[m].replace(",", "")) * scale[units[m]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    acc.setdefault(name, []).append(tot)
+path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
+db = json.load(open(path)) if os.path.exists(path) else {}
+ent = db.setdefault(key, {})
+for k, v in acc.items():
+    ent[k] = sum(v) / len(v)
+    print(f"{key} {k}: {ent[k] / 1e9:.3f} GB per launch ({len(v)} launches)")
+json.dump(db, open(path, "w"), indent=1, sort_keys=True)
