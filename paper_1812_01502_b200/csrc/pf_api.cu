@@ -1,10 +1,9 @@
 // pf_api.cu -- C-ABI (include/pf.h) and host orchestration of one BPF step.
 //
 // Launch sequence of pf_step:
-//   k_pass1 (NT tiles) -> k_cascade (ceil(NT/2048) CTAs) -> k_compose x (#passes)
-// Index mode (d >= 4): the passes compose int32 ancestor maps; the next step's k_pass1
-// gathers x[A(i)] (one random 4d-byte read per particle).  State mode (d <= 2): the
-// passes move the fp32 states themselves (a state is no bigger than an index).
+//   k_pass1 (NT tiles) -> k_cascade (ceil(NT/2048) CTAs) -> k_stages x (#passes)
+// Every pass moves the particle states through shared-memory tiles (coalesced reads and
+// writes; no random HBM access anywhere on the step).
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -22,9 +21,10 @@ using namespace pfk;
 namespace {
 
 constexpr uint32_t kPass1SmemBudgetDefault = 64u * 1024u;
-constexpr uint32_t kComposeSmemBudgetDefault = 200u * 1024u;
 constexpr uint32_t kPass1ThreadsDefault = 256u;
-constexpr uint32_t kComposeThreadsDefault = 1024u;
+constexpr uint32_t kStageSmemDefault = 232448u;  // one persistent CTA per SM
+constexpr uint32_t kStageThreadsDefault = 1024u;
+constexpr uint32_t kSmemPerSM = 233472u;          // 228 KiB (1 KiB of it reserved per CTA)
 
 // Tuning knobs (environment, read at pf_init; for experiments only).
 uint32_t env_u32(const char* name, uint32_t dflt) {
@@ -33,17 +33,16 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 }
 constexpr uint32_t kLPC = 2048u;
 
-struct ComposePass {
-    uint32_t s0, k, P, threads, qpt;
-    bool ident;
+struct StagePass {
+    uint32_t s0, k, P, threads, qpt, smem, tb, grid, pipe;
 };
 
 struct Plan {
     int D;
-    bool index_mode;
+    uint32_t tb;  // k_pass1 table entry bytes (1: side|index, M <= 128; 2: tile position)
     uint32_t P1, k1, NT, LPC, cascade_grid, pass1_threads, pass1_qpt;
     uint32_t pass1_smem;
-    std::vector<ComposePass> passes;
+    std::vector<StagePass> passes;
 };
 
 int ilog2_exact(uint64_t v) {
@@ -69,31 +68,44 @@ uint32_t pick_threads(uint32_t nq, uint32_t maxthr, uint32_t* qpt) {
 // bounded by Nglobal / kMaxShards so that, for any world size up to kMaxShards, the
 // single-GPU tiles coincide with the sharded ones (bitwise G-invariance).
 constexpr uint64_t kMaxShards = 8;
-bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, bool sharded = false, uint64_t Nglobal = 0) {
+bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, uint64_t Nglobal = 0, uint32_t nsm = 148) {
     if (Nglobal == 0) Nglobal = N;
     const uint64_t m = N / M;
     const int S = ilog2_exact(m);
     Plan p;
     p.D = d;
-    // State mode (default): every pass moves the particle states through shared-memory
-    // tiles, so no pass makes a random HBM access.  Index mode (PF_INDEX_MODE=1, d >= 4):
-    // passes compose int32 ancestor maps and the next step gathers x[A(i)] (one random
-    // 4d-byte read per particle, ~3.7e10/s on B200: slower; kept for comparison).
-    p.index_mode = !sharded && d >= 4 && env_u32("PF_INDEX_MODE", 1u) != 0u;
-    const uint32_t kPass1SmemBudget = env_u32("PF_PASS1_SMEM", kPass1SmemBudgetDefault);
-    const uint32_t kComposeSmemBudget = env_u32("PF_COMPOSE_SMEM", kComposeSmemBudgetDefault);
-    const uint32_t kPass1Threads = env_u32("PF_PASS1_THREADS", kPass1ThreadsDefault);
-    const uint32_t kComposeThreads = env_u32("PF_COMPOSE_THREADS", kComposeThreadsDefault);
-    const uint32_t kMoveSmemBudget = env_u32("PF_MOVE_SMEM", 118000u);
-    const uint32_t kMoveThreads = env_u32("PF_MOVE_THREADS", 256u);
-    // pass-1 tile: the largest 2^k1 groups (k1 <= S) whose shared memory fits the budget
-    uint32_t P1 = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(N, 16384u),
+    const uint32_t budget1 = env_u32("PF_PASS1_SMEM", kPass1SmemBudgetDefault);
+    const uint32_t threads1 = env_u32("PF_PASS1_THREADS", kPass1ThreadsDefault);
+    const uint32_t maxqpt1 = env_u32("PF_PASS1_MAXQPT", 8u);
+    // pass-1 tile: the largest 2^k1 <= 64 groups (k1 <= S) whose shared memory fits the budget
+    uint32_t P1 = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(N, (uint64_t)kPass1MaxGroups * M),
                                                std::max<uint64_t>(2ull * M, Nglobal / kMaxShards));
-    for (;;) {
-        const uint32_t k1 = (uint32_t)ilog2_exact(P1 / M);
+    auto threads_for = [&](uint32_t P, uint32_t* q) {
+        uint32_t t = pick_threads(P / 4, threads1, q);
+        while (*q > maxqpt1 && t < 512u) {  // k_pass1 is instantiated for up to 8 quads per thread
+            t *= 2;
+            *q /= 2;
+        }
+        return t;
+    };
+    // table entries: 16-bit tile positions when they fit (cheapest walk), else 1 byte
+    auto fits1 = [&](uint32_t P, uint32_t tb) {
         uint32_t q;
-        const uint32_t thr = pick_threads(P1 / 4, kPass1Threads, &q);
-        if (pass1_smem(d, P1, M, k1, thr).total <= kPass1SmemBudget || P1 <= 2 * M) break;
+        const uint32_t thr = threads_for(P, &q);
+        if (tb == 1u && M > 128u) return false;
+        return thr <= 512u && pass1_smem(d, P, M, (uint32_t)ilog2_exact(P / M), thr, tb).total <= budget1;
+    };
+    p.tb = M <= 128u ? 1u : 2u;
+    for (;;) {
+        if (fits1(P1, 2u)) {
+            p.tb = 2u;
+            break;
+        }
+        if (fits1(P1, 1u)) {
+            p.tb = 1u;
+            break;
+        }
+        if (P1 <= 2 * M) break;
         P1 >>= 1;
     }
     if (P1 < 2 * M) P1 = 2 * M;
@@ -103,12 +115,12 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, bool s
         *err = "internal: k1 > S";
         return false;
     }
-    p.pass1_threads = pick_threads(P1 / 4, kPass1Threads, &p.pass1_qpt);
-    if (p.pass1_qpt > 8u) {
-        *err = "internal: too many quads per thread";
+    p.pass1_threads = threads_for(P1, &p.pass1_qpt);
+    if (p.pass1_threads > 512u) {
+        *err = "pass-1 tile needs more than 512 threads";
         return false;
     }
-    p.pass1_smem = pass1_smem(d, P1, M, p.k1, p.pass1_threads).total;
+    p.pass1_smem = pass1_smem(d, P1, M, p.k1, p.pass1_threads, p.tb).total;
     if (p.pass1_smem > 227u * 1024u) {
         *err = "pass-1 tile does not fit in shared memory (M too large for d)";
         return false;
@@ -120,49 +132,59 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, bool s
         *err = "too many pass-1 tiles for the cascade tree";
         return false;
     }
-    // compose passes for stages k1+1..S
+    // stages k1+1..S in persistent k_stages passes: the largest tile in the shared-memory
+    // budget (default: one double-buffered CTA per SM), fewest passes, stages spread evenly
     uint32_t s = p.k1 + 1;
-    bool first = true;
-    while ((int)s <= S) {
-        const bool ident = p.index_mode && first;
-        const uint32_t payload = ident ? 0u : (p.index_mode ? 4u : (uint32_t)(4 * d));
-        const bool move = !p.index_mode;
-        auto smem_of = [&](uint32_t PP, uint32_t kk) {
-            return move ? move_smem(PP, payload, kk) : compose_smem(PP, payload, kk);
-        };
-        const uint32_t budget = move ? kMoveSmemBudget : kComposeSmemBudget;
-        uint32_t P = 32768u;
-        while (P > 2 * M && (smem_of(P, (uint32_t)ilog2_exact(P / M)) > budget || P > N)) P >>= 1;
-        if (P < 2 * M) P = 2 * M;
-        uint32_t k = (uint32_t)ilog2_exact(P / M);
-        if (k > (uint32_t)S - s + 1) k = (uint32_t)S - s + 1;
-        P = M << k;
-        if (smem_of(P, k) > 227u * 1024u) {
-            *err = "compose tile does not fit in shared memory";
-            return false;
+    const uint32_t sb = (uint32_t)(4 * d);
+    const uint32_t budget = std::min(env_u32("PF_STAGE_SMEM", kStageSmemDefault), 232448u);
+    const uint32_t rem = (uint32_t)S - p.k1;
+    const uint32_t tbmin = M <= 128u ? 1u : 2u;
+    auto kmax = [&](uint32_t pipe) {
+        uint32_t K = 0;
+        for (uint32_t k = 1; k <= rem; ++k) {
+            const uint64_t P = (uint64_t)M << k;
+            if (P > N || P > 65536u || P / 4u > 8u * 1024u) break;
+            if (stages_smem((uint32_t)P, sb, k, tbmin, pipe) > budget) break;
+            K = k;
         }
-        ComposePass cp;
-        cp.s0 = s;
-        cp.k = k;
-        cp.P = P;
-        cp.ident = ident;
-        cp.threads = pick_threads(P / 4, move ? kMoveThreads : kComposeThreads, &cp.qpt);
-        if (cp.qpt > 8u) {
-            *err = "internal: compose quads per thread";
-            return false;
-        }
-        p.passes.push_back(cp);
+        return K;
+    };
+    // software-pipelined unless only the single-buffered tile fits (or it is forced)
+    uint32_t pipe = env_u32("PF_STAGE_PIPE", 1u) ? 1u : 0u;
+    uint32_t K = kmax(pipe);
+    if (K == 0 && pipe) {
+        pipe = 0u;
+        K = kmax(0u);
+    }
+    if (rem > 0 && K == 0) {
+        *err = "stage tile does not fit in shared memory";
+        return false;
+    }
+    const uint32_t npass = rem ? (rem + K - 1) / K : 0;
+    for (uint32_t i = 0; i < npass; ++i) {
+        const uint32_t left = rem - (s - p.k1 - 1);
+        const uint32_t k = (left + (npass - i) - 1) / (npass - i);
+        StagePass sp;
+        sp.s0 = s;
+        sp.k = k;
+        sp.P = M << k;
+        sp.pipe = pipe;
+        sp.tb = (env_u32("PF_STAGE_TB", 2u) == 2u && stages_smem(sp.P, sb, k, 2u, pipe) <= budget) ? 2u : tbmin;
+        sp.threads = pick_threads(sp.P / 4, env_u32("PF_STAGE_THREADS", kStageThreadsDefault), &sp.qpt);
+        sp.smem = stages_smem(sp.P, sb, k, sp.tb, pipe);
+        const uint32_t per_sm = std::max(1u, std::min(kSmemPerSM / (sp.smem + 1024u), 2048u / sp.threads));
+        sp.grid = (uint32_t)std::min<uint64_t>(N / sp.P, (uint64_t)nsm * per_sm);
+        p.passes.push_back(sp);
         s += k;
-        first = false;
     }
     *pl = p;
     return true;
 }
 
 struct Layout {
-    size_t X0, X1, A0, A1, logV, thr, part, scratch, est, ticket, y;
+    size_t X0, X1, logV, thr, part, scratch, est, ticket, y;
     size_t shard_rec, recs, top_logV, top_thr, top_scratch;
-    size_t dbg_x, dbg_lw, dbg_anc, dbg_A, dbg_xhat;
+    size_t dbg_x, dbg_lw, dbg_anc, dbg_A;
     size_t total;
 };
 
@@ -180,8 +202,6 @@ Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags, uint32
     const size_t xb = (size_t)N * p.D * 4;
     L.X0 = take(xb);
     L.X1 = take(xb);
-    L.A0 = take(p.index_mode ? N * 4 : 0);
-    L.A1 = take(p.index_mode ? N * 4 : 0);
     L.logV = take(m * 8);
     L.thr = take(m * 4);
     L.part = take((size_t)p.NT * PS * 8);
@@ -200,7 +220,6 @@ Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags, uint32
     L.dbg_anc = take(dbg ? (size_t)N * Sglobal * 4 : 0);
     (void)S;
     L.dbg_A = take(dbg ? N * 4 : 0);
-    L.dbg_xhat = take(xb);
     L.total = off;
     return L;
 }
@@ -224,8 +243,6 @@ struct pf_handle {
     // state
     uint32_t n;          // index of the next step
     int cur;             // X buffer that holds the gather source / xhat for the next step
-    int amap;            // A buffer holding the next step's gather map (index mode)
-    bool a_identity;     // next step reads X[cur] without a map
     bool have_step;
     int last_launches;
     // kernel timing
@@ -264,7 +281,6 @@ struct pf_handle {
         for (cudaEvent_t e : pool) cudaEventDestroy(e);
     }
     float* X(int i) { return reinterpret_cast<float*>(ws + (i ? lay.X1 : lay.X0)); }
-    int32_t* A(int i) { return reinterpret_cast<int32_t*>(ws + (i ? lay.A1 : lay.A0)); }
     template <typename T>
     T* at(size_t off) { return reinterpret_cast<T*>(ws + off); }
 };
@@ -387,16 +403,16 @@ static bool validate_topology(uint64_t N, uint32_t M, std::string* err) {
 
 // ---------------------------------------------------------------------------------------
 // kernel dispatch (instantiations live in pf_inst_*.cu)
-static void launch_pass1(pf_handle* h, const Pass1Args& a, bool gather) {
+static void launch_pass1(pf_handle* h, const Pass1Args& a) {
     const Plan& p = h->plan;
     const LaunchCfg c{p.NT, p.pass1_threads, p.pass1_smem, h->stream};
     const bool dbg = h->flags & PF_FLAG_DEBUG;
     const int q = (int)p.pass1_qpt;
     switch (p.D) {
-        case 1: launch_pass1_d1(h->mp.kind, gather, dbg, q, c, a); break;
-        case 2: launch_pass1_d2(h->mp.kind, gather, dbg, q, c, a); break;
-        case 4: launch_pass1_d4(h->mp.kind, gather, dbg, q, c, a); break;
-        default: launch_pass1_d8(h->mp.kind, gather, dbg, q, c, a); break;
+        case 1: launch_pass1_d1(h->mp.kind, (int)p.tb, dbg, q, c, a); break;
+        case 2: launch_pass1_d2(h->mp.kind, (int)p.tb, dbg, q, c, a); break;
+        case 4: launch_pass1_d4(h->mp.kind, (int)p.tb, dbg, q, c, a); break;
+        default: launch_pass1_d8(h->mp.kind, (int)p.tb, dbg, q, c, a); break;
     }
 }
 
@@ -420,18 +436,26 @@ static void launch_cascade_k(pf_handle* h) {
     launch_cascade(p.D, LaunchCfg{p.cascade_grid, (uint32_t)kCascadeThreads, 0u, h->stream}, c);
 }
 
-static void launch_compose_k(pf_handle* h, int payload, const ComposeArgs& a, const ComposePass& cp) {
-    static const uint32_t bytes[6] = {0u, 4u, 4u, 8u, 16u, 32u};
-    const uint32_t pb = bytes[payload];
-    const bool dbg = h->flags & PF_FLAG_DEBUG;
-    if (payload >= kPayloadF1) {
-        const LaunchCfg c{(uint32_t)(h->N / cp.P), cp.threads, move_smem(cp.P, pb, cp.k), h->stream};
-        launch_move(payload, dbg, (int)cp.qpt, c, a);
-        return;
-    }
-    const LaunchCfg c{(uint32_t)(h->N / cp.P), cp.threads, compose_smem(cp.P, pb, cp.k), h->stream};
-    if (dbg) launch_compose_dbg(payload, (int)cp.qpt, c, a);
-    else launch_compose_nodbg(payload, (int)cp.qpt, c, a);
+static void launch_stages_k(pf_handle* h, const StagePass& cp, const void* pin, void* pout) {
+    StageArgs a;
+    a.key = make_key(h->seed);
+    a.n = h->n;
+    a.N = h->N;
+    a.pos0 = h->pos0;
+    a.m = h->m;
+    a.M = h->M;
+    a.b = h->b;
+    a.s0 = cp.s0;
+    a.k = cp.k;
+    a.P = cp.P;
+    a.lowbits = cp.s0 - 1;
+    a.pipe = cp.pipe;
+    a.pin = pin;
+    a.pout = pout;
+    a.thr = h->at<uint32_t>(h->lay.thr);
+    a.dbg_anc = (h->flags & PF_FLAG_DEBUG) ? h->at<int32_t>(h->lay.dbg_anc) : nullptr;
+    const LaunchCfg c{cp.grid, cp.threads, cp.smem, h->stream};
+    launch_stages(h->plan.D, (int)cp.tb, (h->flags & PF_FLAG_DEBUG) != 0, (int)cp.qpt, c, a);
 }
 
 static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
@@ -440,7 +464,7 @@ static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
     const bool dbg = h->flags & PF_FLAG_DEBUG;
     Pass1Args a;
     a.mp = h->mp;
-    a.key = {(uint32_t)(h->seed & 0xffffffffu), (uint32_t)(h->seed >> 32)};
+    a.key = make_key(h->seed);
     a.n = h->n;
     a.do_mutate = h->n > 0 ? 1 : 0;
     a.y_dev = y_dev;
@@ -454,11 +478,9 @@ static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
     a.k1 = p.k1;
     a.P1 = p.P1;
     a.T1 = p.P1 / h->M;
-    a.sl = pass1_smem(p.D, p.P1, h->M, p.k1, p.pass1_threads);
+    a.sl = pass1_smem(p.D, p.P1, h->M, p.k1, p.pass1_threads, p.tb);
     const int src = h->cur, dst = h->cur ^ 1;
     a.x_in = h->X(src);
-    const bool gather = p.index_mode && !h->a_identity;
-    a.A_in = gather ? h->A(h->amap) : nullptr;
     a.x_out = h->X(dst);
     a.logV = h->at<double>(h->lay.logV);
     a.thr = h->at<uint32_t>(h->lay.thr);
@@ -467,7 +489,7 @@ static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
     a.dbg_lw = dbg ? h->at<float>(h->lay.dbg_lw) : nullptr;
     a.dbg_anc = dbg ? h->at<int32_t>(h->lay.dbg_anc) : nullptr;
     h->mark(PF_KERNEL_PASS1, true);
-    launch_pass1(h, a, gather);
+    launch_pass1(h, a);
     h->mark(PF_KERNEL_PASS1, false);
     int launches = 1;
     h->mark(PF_KERNEL_CASCADE, true);
@@ -475,55 +497,16 @@ static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
     h->mark(PF_KERNEL_CASCADE, false);
     ++launches;
 
-    // compose passes
-    ComposeArgs c;
-    c.key = a.key;
-    c.n = h->n;
-    c.N = h->N;
-    c.pos0 = h->pos0;
-    c.m = h->m;
-    c.M = h->M;
-    c.b = h->b;
-    c.thr = a.thr;
-    c.dbg_anc = a.dbg_anc;
-    int amap_out = h->amap;
-    int xs = dst;  // state mode: current payload buffer
-    for (size_t i = 0; i < p.passes.size(); ++i) {
-        const ComposePass& cp = p.passes[i];
-        c.s0 = cp.s0;
-        c.k = cp.k;
-        c.P = cp.P;
-        c.lowbits = cp.s0 - 1;
+    // stages k1+1..S: state-moving tile passes
+    int xs = dst;
+    for (const StagePass& sp : p.passes) {
         h->mark(PF_KERNEL_COMPOSE, true);
-        if (p.index_mode) {
-            if (cp.ident) {
-                amap_out = 0;
-                c.pin = nullptr;
-                c.pout = h->A(0);
-                launch_compose_k(h, kPayloadIdent, c, cp);
-            } else {
-                c.pin = h->A(amap_out);
-                c.pout = h->A(amap_out ^ 1);
-                amap_out ^= 1;
-                launch_compose_k(h, kPayloadIndex, c, cp);
-            }
-        } else {
-            c.pin = h->X(xs);
-            c.pout = h->X(xs ^ 1);
-            xs ^= 1;
-            launch_compose_k(h, D == 1 ? kPayloadF1 : (D == 2 ? kPayloadF2 : (D == 4 ? kPayloadF4 : kPayloadF8)), c, cp);
-        }
+        launch_stages_k(h, sp, h->X(xs), h->X(xs ^ 1));
         h->mark(PF_KERNEL_COMPOSE, false);
+        xs ^= 1;
         ++launches;
     }
-    if (p.index_mode) {
-        h->cur = dst;
-        h->amap = amap_out;
-        h->a_identity = p.passes.empty();
-    } else {
-        h->cur = xs;
-        h->a_identity = true;
-    }
+    h->cur = xs;
     h->step_n = h->n;
     h->n += 1;
     h->have_step = h->world == 1;
@@ -557,7 +540,7 @@ static size_t workspace_bytes(const pf_model* model, uint64_t N, uint32_t M, uin
     if (!validate_model(model, err) || !validate_topology(N, M, err) || !shard_geometry(N, M, 0, world, &Nloc, err))
         return 0;
     Plan p;
-    if (!make_plan(model->d, Nloc, M, &p, err, world > 1, N)) return 0;
+    if (!make_plan(model->d, Nloc, M, &p, err, N)) return 0;
     return make_layout(p, Nloc, M, flags, (uint32_t)world, ilog2_exact(N / M)).total;
 }
 
@@ -571,11 +554,24 @@ static int init_core(const pf_model* model, uint64_t N, uint32_t M, uint64_t see
     if (!validate_topology(N, M, &err)) return fail(nullptr, PF_EINVAL, err);
     if (!shard_geometry(N, M, rank, world, &Nloc, &err)) return fail(nullptr, PF_EINVAL, err);
     Plan p;
-    if (!make_plan(model->d, Nloc, M, &p, &err, world > 1, N)) return fail(nullptr, PF_EINVAL, err);
+    int nsm = 148, dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        nsm <= 0) {
+        cudaGetLastError();
+        nsm = 148;
+    }
+    if (!make_plan(model->d, Nloc, M, &p, &err, N, (uint32_t)nsm)) return fail(nullptr, PF_EINVAL, err);
     const int Sglobal = ilog2_exact(N / M);
     Layout L = make_layout(p, Nloc, M, flags, (uint32_t)world, Sglobal);
     if (!dev_ws || ws_bytes < L.total) return fail(nullptr, PF_EWORKSPACE, "workspace too small");
     if (reinterpret_cast<uintptr_t>(dev_ws) & 255u) return fail(nullptr, PF_EWORKSPACE, "workspace not 256-byte aligned");
+    if (env_u32("PF_PLAN_VERBOSE", 0u)) {
+        fprintf(stderr, "[pf plan] N=%llu M=%u d=%d tb=%u pass1: P1=%u k1=%u threads=%u qpt=%u smem=%u tiles=%u\n",
+                (unsigned long long)Nloc, M, p.D, p.tb, p.P1, p.k1, p.pass1_threads, p.pass1_qpt, p.pass1_smem, p.NT);
+        for (const StagePass& sp : p.passes)
+            fprintf(stderr, "[pf plan]   pass s0=%u k=%u P=%u tb=%u pipe=%u threads=%u qpt=%u smem=%u grid=%u\n", sp.s0,
+                    sp.k, sp.P, sp.tb, sp.pipe, sp.threads, sp.qpt, sp.smem, sp.grid);
+    }
     pf_handle* h = new pf_handle();
     h->mp = to_params(model);
     h->N = Nloc;
@@ -599,8 +595,6 @@ static int init_core(const pf_model* model, uint64_t N, uint32_t M, uint64_t see
     h->stream = static_cast<cudaStream_t>(cuda_stream);
     h->n = 0;
     h->cur = 0;
-    h->amap = 0;
-    h->a_identity = true;
     h->have_step = false;
     h->last_launches = 0;
     h->timing = false;
@@ -608,7 +602,7 @@ static int init_core(const pf_model* model, uint64_t N, uint32_t M, uint64_t see
     {
         InitArgs ia;
         ia.mp = h->mp;
-        ia.key = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+        ia.key = make_key(seed);
         ia.N = h->N;
         ia.pos0 = h->pos0;
         ia.x = h->X(0);
@@ -695,7 +689,7 @@ int pf_cross_stage(pf_handle* h, int t, const void* dev_partner_states) {
     const uint32_t* top_thr = h->at<uint32_t>(h->lay.top_thr);
     const uint32_t G = h->world;
     CrossArgs c;
-    c.key = {(uint32_t)(h->seed & 0xffffffffu), (uint32_t)(h->seed >> 32)};
+    c.key = make_key(h->seed);
     c.n = h->step_n;
     c.s = h->S + (uint32_t)t;
     c.t = (uint32_t)t;
@@ -811,14 +805,7 @@ int pf_debug_ptr(pf_handle* h, int what, int stage, void** dev_out) {
             *dev_out = A;
             return check_cuda(h, "pf_debug_ptr");
         }
-        case PF_DBG_XHAT: {
-            float* out = h->at<float>(h->lay.dbg_xhat);
-            const float* x = h->X(h->cur);
-            const int32_t* A = (h->plan.index_mode && !h->a_identity) ? h->A(h->amap) : nullptr;
-            launch_gather(D, LaunchCfg{1024u, 256u, 0u, h->stream}, x, A, h->N, out);
-            *dev_out = out;
-            return check_cuda(h, "pf_debug_ptr");
-        }
+        case PF_DBG_XHAT: *dev_out = h->X(h->cur); return PF_OK;
         case PF_DBG_LOGV: *dev_out = h->at<double>(h->lay.logV); return PF_OK;
         case PF_DBG_THRESH: *dev_out = h->at<uint32_t>(h->lay.thr); return PF_OK;
     }
@@ -853,7 +840,6 @@ int pf_debug_set_state(pf_handle* h, const float* host_xhat, uint32_t n) {
                                     h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_debug_set_state: ") + cudaGetErrorString(e));
-    h->a_identity = true;
     h->n = n;
     return PF_OK;
 }

@@ -17,29 +17,42 @@ constexpr uint32_t kDomainInit = 1u;
 constexpr uint32_t kDomainMutate = 2u;
 constexpr uint32_t kDomainResample = 3u;
 
+// Offset of V level s (s >= 1) in the (m - 1)-entry level tables: level s has m / 2^s
+// entries (blocks of 2^s groups).
+__host__ __device__ inline uint64_t level_offset(uint64_t m, int s) { return m - (m >> (s - 1)); }
+
+// Philox key schedule: round r uses (k[2r], k[2r+1]) = (k0 + r W0, k1 + r W1).  Computed
+// once on the host and passed inside the kernel parameters, so every round's key XOR reads
+// a constant-bank operand (no per-thread key registers or adds).
 struct Key {
-    uint32_t k0, k1;
+    uint32_t k[20];
 };
+
+__host__ __device__ inline Key make_key(uint64_t seed) {
+    Key key;
+    const uint32_t k0 = (uint32_t)(seed & 0xffffffffu), k1 = (uint32_t)(seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        key.k[2 * r] = k0 + (uint32_t)r * 0x9E3779B9u;
+        key.k[2 * r + 1] = k1 + (uint32_t)r * 0xBB67AE85u;
+    }
+    return key;
+}
 
 // Philox4x32-10: per round (hi0,lo0) = M0*c0, (hi1,lo1) = M1*c2,
 // c <- (hi1^c1^k0, lo1, hi0^c3^k1, lo0); key += (W0, W1) between rounds.
-__device__ __forceinline__ uint4 philox10(uint4 c, Key key) {
-    uint32_t k0 = key.k0, k1 = key.k1;
+__device__ __forceinline__ uint4 philox10(uint4 c, const Key& key) {
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
-        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
-        const uint32_t lo0 = 0xD2511F53u * c.x;
-        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z);
-        const uint32_t lo1 = 0xCD9E8D57u * c.z;
-        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
-        k0 += 0x9E3779B9u;
-        k1 += 0xBB67AE85u;
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c.x;
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
+        c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ key.k[2 * r], (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ key.k[2 * r + 1],
+                       (uint32_t)p0);
     }
     return c;
 }
 
 // Block (c0, n, domain<<24 | sub, 0) of the draw contract.
-__device__ __forceinline__ uint4 rng_block(Key key, uint32_t c0, uint32_t n, uint32_t domain, uint32_t sub) {
+__device__ __forceinline__ uint4 rng_block(const Key& key, uint32_t c0, uint32_t n, uint32_t domain, uint32_t sub) {
     return philox10(make_uint4(c0, n, (domain << 24) | sub, 0u), key);
 }
 
@@ -195,21 +208,22 @@ __device__ __forceinline__ uint32_t side_threshold(double vl, double vr, int b) 
     return (uint32_t)floor(p * ldexp(1.0, 32 - b));
 }
 
-// The same two quantities with the O(1) transcendental part in fp32 (the large common
-// offset stays fp64): |error| <~ 3e-7 in log V and ~1e-7 in p, well inside the 1e-6
-// decision window of the parity contract.  Used for the in-tile levels of k_pass1.
-__device__ __forceinline__ double log_pair_mean_fast(double a, double b) {
-    const double c = a > b ? a : b;
-    if (c == -CUDART_INF) return -CUDART_INF;
-    const float dlt = (float)((a > b ? b : a) - c);  // <= 0, possibly -inf
-    return c + (double)(log1pf(expf(dlt)) - 0.693147180559945309f);
-}
-
-__device__ __forceinline__ uint32_t side_threshold_fast(double vl, double vr, int b) {
-    float p;
-    if (vl == -CUDART_INF && vr == -CUDART_INF) p = 0.5f;
-    else p = 1.0f / (1.0f + expf((float)(vr - vl)));
-    return (uint32_t)floorf(p * __int_as_float((127 + 32 - b) << 23));  // p * 2^(32-b), exact scaling
+// The same two quantities for the in-tile levels of k_pass1: the large common offset stays
+// fp64, the O(1) part uses the MUFU exp2/log2/rcp (|error| ~3e-7 in log V and in p, inside
+// the 1e-6 decision window of the parity contract).  One exp serves both outputs.
+__device__ __forceinline__ void pair_level_fast(double vl, double vr, int b, double* v, uint32_t* P) {
+    const double mx = vl > vr ? vl : vr, mn = vl > vr ? vr : vl;
+    if (mx == -CUDART_INF) {  // both halves dead: V = 0, p = 1/2
+        *v = -CUDART_INF;
+        *P = 1u << (31 - b);
+        return;
+    }
+    const float t = exp2f((float)(mn - mx) * 1.4426950408889634f);  // e^{mn - mx} in [0, 1]
+    const float op = 1.0f + t;
+    *v = mx + (double)(__log2f(op) * 0.6931471805599453f - 0.6931471805599453f);
+    const float q = __frcp_rn(op);
+    const float p = vl >= vr ? q : t * q;
+    *P = (uint32_t)(p * __int_as_float((127 + 32 - b) << 23));  // floor(p 2^(32-b)), p 2^(32-b) >= 0
 }
 
 }  // namespace pfk

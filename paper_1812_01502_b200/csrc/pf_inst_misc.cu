@@ -53,13 +53,4 @@ void launch_debug_compose(const LaunchCfg& c, const int32_t* anc, uint64_t N, ui
     k_debug_compose<0><<<c.grid, c.threads, 0, c.stream>>>(anc, N, S, A);
 }
 
-void launch_gather(int D, const LaunchCfg& c, const float* x, const int32_t* A, uint64_t N, float* out) {
-    switch (D) {
-        case 1: k_gather<1><<<c.grid, c.threads, 0, c.stream>>>(x, A, N, out); break;
-        case 2: k_gather<2><<<c.grid, c.threads, 0, c.stream>>>(x, A, N, out); break;
-        case 4: k_gather<4><<<c.grid, c.threads, 0, c.stream>>>(x, A, N, out); break;
-        default: k_gather<8><<<c.grid, c.threads, 0, c.stream>>>(x, A, N, out); break;
-    }
-}
-
 }  // namespace pfk

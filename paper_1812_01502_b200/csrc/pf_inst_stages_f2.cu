@@ -1,0 +1,4 @@
+// k_stages instantiations for the float2 state payload (body: pf_inst_stages.inc).
+#define STAGES_T float2
+#define STAGES_LAUNCHER launch_stages_f2
+#include "pf_inst_stages.inc"

@@ -1,0 +1,4 @@
+// k_stages instantiations for the float4 state payload (body: pf_inst_stages.inc).
+#define STAGES_T float4
+#define STAGES_LAUNCHER launch_stages_f4
+#include "pf_inst_stages.inc"

@@ -1,0 +1,4 @@
+// k_stages instantiations for the State8 state payload (body: pf_inst_stages.inc).
+#define STAGES_T State8
+#define STAGES_LAUNCHER launch_stages_f8
+#include "pf_inst_stages.inc"

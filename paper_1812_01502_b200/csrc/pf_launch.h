@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include "pf_kernels.cuh"
+#include "pf_stages.cuh"
 
 namespace pfk {
 
@@ -13,25 +14,33 @@ struct LaunchCfg {
     cudaStream_t stream;
 };
 
-enum ComposePayload { kPayloadIdent = 0, kPayloadIndex = 1, kPayloadF1 = 2, kPayloadF2 = 3, kPayloadF4 = 4, kPayloadF8 = 5 };
+enum StatePayload { kPayloadF1 = 2, kPayloadF2 = 3, kPayloadF4 = 4, kPayloadF8 = 5 };
 
 // 8-float particle state moved as one payload element (d = 8).
 struct __align__(16) State8 {
     float4 a, b;
 };
 
-void launch_pass1_d1(int kind, bool gather, bool dbg, int qpt, const LaunchCfg& c, const Pass1Args& a);
-void launch_pass1_d2(int kind, bool gather, bool dbg, int qpt, const LaunchCfg& c, const Pass1Args& a);
-void launch_pass1_d4(int kind, bool gather, bool dbg, int qpt, const LaunchCfg& c, const Pass1Args& a);
-void launch_pass1_d8(int kind, bool gather, bool dbg, int qpt, const LaunchCfg& c, const Pass1Args& a);
-void launch_compose_nodbg(int payload, int qpt, const LaunchCfg& c, const ComposeArgs& a);
-void launch_compose_dbg(int payload, int qpt, const LaunchCfg& c, const ComposeArgs& a);
-void launch_move(int payload, bool dbg, int qpt, const LaunchCfg& c, const ComposeArgs& a);
+void launch_pass1_d1(int kind, int tb, bool dbg, int qpt, const LaunchCfg& c, const Pass1Args& a);
+void launch_pass1_d2(int kind, int tb, bool dbg, int qpt, const LaunchCfg& c, const Pass1Args& a);
+void launch_pass1_d4(int kind, int tb, bool dbg, int qpt, const LaunchCfg& c, const Pass1Args& a);
+void launch_pass1_d8(int kind, int tb, bool dbg, int qpt, const LaunchCfg& c, const Pass1Args& a);
+void launch_stages_f1(int tb, bool dbg, int qpt, const LaunchCfg& c, const StageArgs& a);
+void launch_stages_f2(int tb, bool dbg, int qpt, const LaunchCfg& c, const StageArgs& a);
+void launch_stages_f4(int tb, bool dbg, int qpt, const LaunchCfg& c, const StageArgs& a);
+void launch_stages_f8(int tb, bool dbg, int qpt, const LaunchCfg& c, const StageArgs& a);
+inline void launch_stages(int D, int tb, bool dbg, int qpt, const LaunchCfg& c, const StageArgs& a) {
+    switch (D) {
+        case 1: launch_stages_f1(tb, dbg, qpt, c, a); break;
+        case 2: launch_stages_f2(tb, dbg, qpt, c, a); break;
+        case 4: launch_stages_f4(tb, dbg, qpt, c, a); break;
+        default: launch_stages_f8(tb, dbg, qpt, c, a); break;
+    }
+}
 void launch_cascade(int D, const LaunchCfg& c, const CascadeArgs& a);
 void launch_init(int D, int kind, const LaunchCfg& c, const InitArgs& a);
 void launch_top(int D, const LaunchCfg& c, const TopArgs& a);
 void launch_cross(int payload, bool dbg, const LaunchCfg& c, const CrossArgs& a);
 void launch_debug_compose(const LaunchCfg& c, const int32_t* anc, uint64_t N, uint32_t S, int32_t* A);
-void launch_gather(int D, const LaunchCfg& c, const float* x, const int32_t* A, uint64_t N, float* out);
 
 }  // namespace pfk

@@ -1,0 +1,502 @@
+// pf_pass1.cuh -- k_pass1: one CTA per tile of T1 = 2^k1 consecutive groups (P1 = T1 M
+// particles, T1 <= 64):
+//
+//   load xhat_{n-1} (coalesced) -> mutate (Alg. 1 l.303) -> log g_n
+//    -> stage 1 over the pairs (2p, 2p+1) (Alg. 3 l.346-349): pair max,
+//   weights c = exp(lw - max), warp-shuffle segmented inclusive scan, branch-free binary
+//   searches of the inverse CDF -> V level 1 per pair; then every warp redundantly builds
+//   the tile's V levels 2..k1 and side thresholds in its lanes (log-domain pair means,
+//   eq. V_defn_proofs) -> draws of stages 2..k1 into per-stage tables ->
+//   each output walks its ancestry back through the tables and writes its state, already
+//   moved to its stage-k1 position (composition licensed by Lemma facts_about_Vs (a),
+//   PAPER.md:645).
+//
+// Barriers: B (stage-1 tables, pair V_1 and per-warp estimate partials in shared memory),
+// D (all stage tables complete); pairs wider than one warp (M > 64) add two for the
+// cross-warp max and scan.
+//
+// Table entries (TB = 1, M <= 128): stage 1 stores the pool index a in [0, 2M) (the source
+// is pair base + a); stage s >= 2 stores side << 7 | index.  TB = 2: the 16-bit tile
+// position of the source.
+#pragma once
+#include <cstdint>
+
+#include "pf_device.cuh"
+
+namespace pfk {
+
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr uint32_t kPass1MaxGroups = 64;  // T1 <= 64: the V tree of a tile fits one warp's lanes
+
+struct Pass1Smem {
+    uint32_t xs, w, L1, tab, chunk, lv1, red, total;
+};
+__host__ __device__ inline Pass1Smem pass1_smem(int D, uint32_t P1, uint32_t M, uint32_t k1, uint32_t threads,
+                                                uint32_t tb) {
+    Pass1Smem s;
+    uint32_t off = 0;
+    auto take = [&](uint32_t bytes) {
+        const uint32_t o = off;
+        off += (bytes + 15u) & ~15u;
+        return o;
+    };
+    const uint32_t T1 = P1 / M;
+    s.xs = take(P1 * 4u * (uint32_t)D);
+    s.w = take(P1 * 4u);
+    s.L1 = take(P1 * tb);
+    s.tab = take(k1 >= 2 ? (k1 - 1u) * P1 * tb : 0u);
+    s.chunk = take(M > 64 ? (P1 / 128u) * 4u : 0u);  // per-warp-chunk maxima / totals
+    s.lv1 = take((T1 / 2) * 8u);
+    s.red = take((threads / 32u) * (2u + 4u * (uint32_t)D) * 4u);
+    s.total = off;
+    return s;
+}
+
+struct Pass1Args {
+    ModelParams mp;
+    Key key;
+    uint32_t n;
+    int do_mutate;
+    const float* y_dev;  // if non-null, y is read from device memory
+    float y[8];
+    uint64_t N;           // particles of this shard
+    uint32_t pos0;        // global index of the shard's first particle (RNG counters)
+    uint32_t m, M, b, S, k1, P1, T1;
+    Pass1Smem sl;         // shared-memory layout (pass1_smem)
+    const float* x_in;    // xhat_{n-1} (or x_0)
+    float* x_out;         // particles moved to their stage-k1 positions
+    double* logV;         // level table (m - 1)
+    uint32_t* thr;        // threshold table (m - 1)
+    double* part;         // per-tile estimate partials, (2 + 4D) doubles each
+    float* dbg_x;
+    float* dbg_lw;
+    int32_t* dbg_anc;
+};
+
+// Sum of NV = 2^v values over the 32 lanes of a warp by recursive halving: after the
+// call, lane l holds the total of value (l >> (5 - v)) in v[0].
+template <int NV>
+__device__ __forceinline__ float warp_sum_transpose(float* v, uint32_t lane) {
+    constexpr int LV = NV == 1 ? 0 : (NV == 2 ? 1 : (NV == 4 ? 2 : (NV == 8 ? 3 : (NV == 16 ? 4 : 5))));
+    static_assert((1 << LV) == NV && LV <= 5, "NV must be a power of two <= 32");
+#pragma unroll
+    for (int t = 0; t < LV; ++t) {
+        const uint32_t o = 16u >> t;
+        const int half = NV >> (t + 1);
+        const bool upper = (lane & o) != 0u;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+            const float send = upper ? v[i] : v[half + i];
+            const float keep = upper ? v[half + i] : v[i];
+            v[i] = keep + __shfl_xor_sync(kFull, send, o);
+        }
+    }
+#pragma unroll
+    for (int t = LV; t < 5; ++t) v[0] += __shfl_xor_sync(kFull, v[0], 16u >> t);
+    return v[0];
+}
+
+template <int D, int KIND, bool DBG, int QPT, int TB>
+__global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args a) {
+    constexpr int PS = 2 + 4 * D;  // partial: max, sw, s1[D], s2[D], p1[D], p2[D]
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t threads = blockDim.x;
+    const Pass1Smem& SL = a.sl;
+    float* xs = reinterpret_cast<float*>(smem + SL.xs);
+    float* w = reinterpret_cast<float*>(smem + SL.w);
+    unsigned char* L1 = smem + SL.L1;
+    unsigned char* tab = smem + SL.tab;
+    float* chunk = reinterpret_cast<float*>(smem + SL.chunk);
+    double* lv1 = reinterpret_cast<double*>(smem + SL.lv1);
+    float* red = reinterpret_cast<float*>(smem + SL.red);
+
+    const uint32_t P1 = a.P1, M = a.M, b = a.b, nq = P1 >> 2, k1 = a.k1;
+    const uint32_t T1 = a.T1;  // groups per tile (<= 64)
+    const uint32_t tile = blockIdx.x;
+    const uint32_t base = tile * P1;  // N < 2^31
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nwarps = threads >> 5;
+    const uint32_t Z = M >> 1;  // quads per stage-1 pair (2M positions)
+    const uint32_t c0t = (a.pos0 + base) >> 2;  // Philox counter of the tile's first quad
+
+    // ---- 1. load xhat_{n-1} (all slots first: independent loads in flight) -------------
+    float xh[QPT][4 * D];
+#pragma unroll
+    for (int it = 0; it < QPT; ++it) {
+        const uint32_t q = tid + it * threads;
+        if (q >= nq) {  // tiny tiles only (P1 < 128)
+#pragma unroll
+            for (int k = 0; k < 4 * D; ++k) xh[it][k] = 0.0f;
+            continue;
+        }
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(a.x_in + (uint64_t)(base + 4u * q) * D) + c);
+            xh[it][4 * c] = t.x;
+            xh[it][4 * c + 1] = t.y;
+            xh[it][4 * c + 2] = t.z;
+            xh[it][4 * c + 3] = t.w;
+        }
+    }
+
+    float y[8];  // after the state loads: its latency overlaps theirs
+#pragma unroll
+    for (int k = 0; k < 8; ++k) y[k] = a.y_dev ? (k < a.mp.dy ? __ldg(a.y_dev + k) : 0.0f) : a.y[k];
+
+    // ---- 2. mutate, weight ---------------------------------------------------------------
+    float lw[QPT][4];
+    constexpr bool KEEPX = 4 * D * QPT <= 32;  // states stay in registers for the estimate
+    float xr[KEEPX ? QPT : 1][KEEPX ? 4 * D : 1];
+#pragma unroll
+    for (int it = 0; it < QPT; ++it) {
+        const uint32_t q = tid + it * threads;
+        const bool valid = q < nq;
+        const uint32_t i0 = base + 4u * q;
+        float x[4 * D];
+        if (a.do_mutate) {
+            float z[4 * D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const uint4 blk = rng_block(a.key, ((a.pos0 + i0) >> 2) * D + j, a.n, kDomainMutate, 0u);
+                normals4(blk, z + 4 * j);
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) mutate<D, KIND>(a.mp, xh[it] + e * D, z + e * D, x + e * D);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4 * D; ++k) x[k] = xh[it][k];
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) lw[it][e] = valid ? log_potential<D, KIND>(a.mp, y, x + e * D) : -CUDART_INF_F;
+        if constexpr (KEEPX) {
+#pragma unroll
+            for (int k = 0; k < 4 * D; ++k) xr[it][k] = valid ? x[k] : 0.0f;
+        }
+        if (!valid) continue;
+#pragma unroll
+        for (int c = 0; c < D; ++c)
+            reinterpret_cast<float4*>(xs)[q * D + c] = make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+        if constexpr (DBG) {
+#pragma unroll
+            for (int c = 0; c < D; ++c)
+                reinterpret_cast<float4*>(a.dbg_x + (uint64_t)i0 * D)[c] =
+                    make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+            reinterpret_cast<float4*>(a.dbg_lw + i0)[0] = make_float4(lw[it][0], lw[it][1], lw[it][2], lw[it][3]);
+        }
+    }
+
+    // ---- 3. stage 1: pair max, weights, segmented scan, inverse-CDF draws --------------
+    const uint32_t zw = Z < 32u ? Z : 32u;
+    float pm[QPT];
+#pragma unroll
+    for (int it = 0; it < QPT; ++it) {
+        float v = fmaxf(fmaxf(lw[it][0], lw[it][1]), fmaxf(lw[it][2], lw[it][3]));
+        for (uint32_t o = 1; o < zw; o <<= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+        pm[it] = v;
+    }
+    if (Z > 32u) {  // a pair spans several warp-chunks of 32 quads
+#pragma unroll
+        for (int it = 0; it < QPT; ++it)
+            if (lane == 0 && tid + it * threads < nq) chunk[(tid + it * threads) >> 5] = pm[it];
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < QPT; ++it) {
+            const uint32_t c0 = ((tid + it * threads) >> 5) & ~((Z >> 5) - 1u);
+            float v = -CUDART_INF_F;
+            for (uint32_t c = lane; c < (Z >> 5); c += 32u) v = fmaxf(v, chunk[c0 + c]);
+            for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+            pm[it] = v;
+        }
+        __syncthreads();
+    }
+    // stage-1 weights c = exp(lw - pair max); they also weight the estimate partial,
+    // rescaled to the thread's largest pair max (one exp per slot)
+    float mthr = -CUDART_INF_F;
+#pragma unroll
+    for (int it = 0; it < QPT; ++it)
+        if (tid + it * threads < nq) mthr = fmaxf(mthr, pm[it]);
+    float acc[PS];
+#pragma unroll
+    for (int k = 0; k < PS; ++k) acc[k] = 0.0f;
+    float run[QPT][4], incl[QPT];
+#pragma unroll
+    for (int it = 0; it < QPT; ++it) {
+        const uint32_t q = tid + it * threads;
+        const bool valid = q < nq;
+        const bool dead = pm[it] == -CUDART_INF_F;  // all of the pair's weights are zero
+        const float f = (dead || !valid) ? 0.0f : (QPT == 1 ? 1.0f : expf(pm[it] - mthr));
+        float r = 0.0f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float c = dead ? 1.0f : expf(lw[it][e] - pm[it]);
+            r += c;
+            run[it][e] = r;
+            const float wf = c * f;
+            acc[1] += wf;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                float xv;
+                if constexpr (KEEPX) xv = xr[it][e * D + k];
+                else xv = valid ? xs[(4 * q + e) * D + k] : 0.0f;
+                acc[2 + k] = fmaf(wf, xv, acc[2 + k]);
+                acc[2 + D + k] = fmaf(wf * xv, xv, acc[2 + D + k]);
+                acc[2 + 2 * D + k] += xv;
+                acc[2 + 3 * D + k] = fmaf(xv, xv, acc[2 + 3 * D + k]);
+            }
+        }
+        float v = r;  // inclusive scan of quad totals within the segment (<= 32 quads)
+        for (uint32_t o = 1; o < zw; o <<= 1) {
+            const float t = __shfl_up_sync(kFull, v, o, zw);
+            if ((lane & (zw - 1u)) >= o) v += t;
+        }
+        incl[it] = v;
+    }
+    float excl[QPT], tot[QPT];
+    if (Z <= 32u) {
+#pragma unroll
+        for (int it = 0; it < QPT; ++it) {
+            const float up = __shfl_up_sync(kFull, incl[it], 1, Z);
+            excl[it] = (lane & (Z - 1u)) ? up : 0.0f;
+            tot[it] = __shfl_sync(kFull, incl[it], lane | (Z - 1u));
+        }
+    } else {
+#pragma unroll
+        for (int it = 0; it < QPT; ++it) {
+            const float up = __shfl_up_sync(kFull, incl[it], 1);
+            excl[it] = lane ? up : 0.0f;
+            if (lane == 31 && tid + it * threads < nq) chunk[(tid + it * threads) >> 5] = incl[it];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < QPT; ++it) {
+            const uint32_t cq = (tid + it * threads) >> 5;
+            const uint32_t c0 = cq & ~((Z >> 5) - 1u);
+            float before = 0.0f, all = 0.0f;
+            for (uint32_t c = lane; c < (Z >> 5); c += 32u) {
+                const float t = chunk[c0 + c];
+                all += t;
+                if (c0 + c < cq) before += t;
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                before += __shfl_xor_sync(kFull, before, o);
+                all += __shfl_xor_sync(kFull, all, o);
+            }
+            excl[it] += before;
+            tot[it] = all;
+        }
+    }
+    const float log2M = logf((float)(2u * M));
+#pragma unroll
+    for (int it = 0; it < QPT; ++it) {
+        const uint32_t q = tid + it * threads;
+        if (q >= nq) continue;
+        reinterpret_cast<float4*>(w)[q] =
+            make_float4(excl[it] + run[it][0], excl[it] + run[it][1], excl[it] + run[it][2], excl[it] + run[it][3]);
+        if (((4u * q) & (2u * M - 1u)) == 0u)  // first quad of its pair: log V_1 of the pair
+            lv1[(4u * q) >> (b + 1)] =
+                pm[it] == -CUDART_INF_F ? -CUDART_INF : (double)pm[it] + (double)(logf(tot[it]) - log2M);
+    }
+    if (Z <= 32u) __syncwarp();  // a pair's CDF was written by this warp
+    else __syncthreads();
+    {   // all QPT x 4 branch-free binary searches advance together (independent smem loads)
+        uint32_t lo[QPT][4];
+        float tq[QPT][4];
+#pragma unroll
+        for (int it = 0; it < QPT; ++it) {
+            const uint32_t q = tid + it * threads;
+            const bool valid = q < nq;
+            const uint4 blk = rng_block(a.key, c0t + q, a.n, kDomainResample, 1u);
+            const uint32_t pb = valid ? (((4u * q) >> (b + 1)) << (b + 1)) : 0u;
+            const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                lo[it][e] = pb;
+                tq[it][e] = valid ? u01f(r[e]) * tot[it] : -1.0f;
+            }
+        }
+        for (uint32_t step = M; step >= 1u; step >>= 1) {
+#pragma unroll
+            for (int it = 0; it < QPT; ++it)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (w[lo[it][e] + step - 1u] <= tq[it][e]) lo[it][e] += step;
+        }
+#pragma unroll
+        for (int it = 0; it < QPT; ++it) {
+            const uint32_t q = tid + it * threads;
+            if (q >= nq) continue;
+            if constexpr (DBG)
+                reinterpret_cast<int4*>(a.dbg_anc + base + 4u * q)[0] =
+                    make_int4((int)(a.pos0 + base + lo[it][0]), (int)(a.pos0 + base + lo[it][1]),
+                              (int)(a.pos0 + base + lo[it][2]), (int)(a.pos0 + base + lo[it][3]));
+            if constexpr (TB == 1) {
+                const uint32_t pm2 = 2u * M - 1u;  // pool index a = lo - pair base
+                *reinterpret_cast<uint32_t*>(L1 + 4u * q) = (lo[it][0] & pm2) | ((lo[it][1] & pm2) << 8) |
+                                                             ((lo[it][2] & pm2) << 16) | ((lo[it][3] & pm2) << 24);
+            } else {
+                *reinterpret_cast<uint2*>(L1 + 8u * q) =
+                    make_uint2(lo[it][0] | (lo[it][1] << 16), lo[it][2] | (lo[it][3] << 16));
+            }
+        }
+    }
+
+    // per-warp estimate partial: rescale to the warp max, then a transposed warp sum
+    {
+        float wmax = mthr;
+        for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(kFull, wmax, o));
+        const float f = (mthr == -CUDART_INF_F) ? 0.0f : expf(mthr - wmax);
+        float sw = acc[1] * f;
+        for (int o = 16; o > 0; o >>= 1) sw += __shfl_xor_sync(kFull, sw, o);
+        float v[4 * D];
+#pragma unroll
+        for (int k = 0; k < 4 * D; ++k) v[k] = (k < 2 * D) ? acc[2 + k] * f : acc[2 + k];
+        const float tot4 = warp_sum_transpose<4 * D>(v, lane);
+        constexpr int LV = (4 * D == 4) ? 2 : ((4 * D == 8) ? 3 : ((4 * D == 16) ? 4 : 5));
+        if ((lane & ((32u >> LV) - 1u)) == 0u) red[warp * PS + 2 + (lane >> (5 - LV))] = tot4;
+        if (lane == 0) {
+            red[warp * PS] = wmax;
+            red[warp * PS + 1] = sw;
+        }
+    }
+    __syncthreads();  // B: L1, lv1, red complete
+
+    // ---- 4. V levels 2..k1 and thresholds, redundantly in every warp (lane i holds
+    //         block i << (s-2) of level s-1 before step s) -----------------------------
+    uint32_t thr[7];
+    {
+        const uint32_t npair = T1 >> 1;
+        double v = lane < npair ? lv1[lane] : -CUDART_INF;
+        if (warp == 0 && lane < npair) a.logV[level_offset(a.m, 1) + (uint64_t)tile * npair + lane] = v;
+#pragma unroll
+        for (int s = 2; s <= 6; ++s) {
+            thr[s] = 0u;
+            if ((uint32_t)s > k1) continue;
+            const uint32_t stp = 1u << (s - 2);
+            const double vr = __shfl_down_sync(kFull, v, stp);
+            const bool act = (lane & (2u * stp - 1u)) == 0u && lane < npair;
+            uint32_t Pt;
+            double nv;
+            pair_level_fast(v, vr, (int)b, &nv, &Pt);
+            thr[s] = Pt;
+            if (act) {
+                v = nv;
+                if (warp == 0) {
+                    const uint64_t at = level_offset(a.m, s) + (uint64_t)tile * (T1 >> s) + (lane >> (s - 1));
+                    a.logV[at] = nv;
+                    a.thr[at] = Pt;
+                }
+            }
+        }
+    }
+
+    // ---- 5. stages 2..k1: every draw depends only on its word and the threshold ---------
+    const uint32_t mask = M - 1u;
+#pragma unroll
+    for (int it = 0; it < QPT; ++it) {
+        const uint32_t q = tid + it * threads;
+        const bool valid = q < nq;
+        const uint32_t l0 = valid ? 4u * q : 0u;
+        const uint32_t j0 = l0 >> b, j1 = (l0 + 2u) >> b;  // quad groups (differ only when M == 2)
+#pragma unroll
+        for (int s = 2; s <= 6; ++s) {
+            if ((uint32_t)s > k1) continue;
+            const uint32_t P0 = __shfl_sync(kFull, thr[s], (j0 >> s) << (s - 1));
+            const uint32_t Pq1 = __shfl_sync(kFull, thr[s], (j1 >> s) << (s - 1));
+            if (!valid) continue;
+            const uint32_t bit = 1u << (s - 1);
+            const uint4 blk = rng_block(a.key, c0t + q, a.n, kDomainResample, (uint32_t)s);
+            const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
+            uint32_t en[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t je = e < 2 ? j0 : j1;
+                const bool hi = (r[e] >> b) >= (e < 2 ? P0 : Pq1);
+                if constexpr (TB == 1) en[e] = (r[e] & mask) | (hi ? 0x80u : 0u);
+                else en[e] = ((hi ? (je | bit) : (je & ~bit)) << b) | (r[e] & mask);
+                if constexpr (DBG) {
+                    const uint32_t src = ((hi ? (je | bit) : (je & ~bit)) << b) | (r[e] & mask);
+                    a.dbg_anc[(uint64_t)(s - 1) * a.N + base + l0 + e] = (int32_t)(a.pos0 + base + src);
+                }
+            }
+            unsigned char* Ts = tab + (uint32_t)(s - 2) * P1 * TB;
+            if constexpr (TB == 1)
+                *reinterpret_cast<uint32_t*>(Ts + l0) = en[0] | (en[1] << 8) | (en[2] << 16) | (en[3] << 24);
+            else
+                *reinterpret_cast<uint2*>(Ts + 2u * l0) = make_uint2(en[0] | (en[1] << 16), en[2] | (en[3] << 16));
+        }
+    }
+    __syncthreads();  // D: all stage tables ready
+
+    // ---- 6. compose backwards and write the tile at its stage-k1 positions ------------
+#pragma unroll
+    for (int it = 0; it < QPT; ++it) {
+        const uint32_t q = tid + it * threads;
+        if (q >= nq) continue;
+        uint32_t tp[4] = {4u * q, 4u * q + 1u, 4u * q + 2u, 4u * q + 3u};
+        for (uint32_t s = k1; s >= 2u; --s) {
+            const unsigned char* Ts = tab + (s - 2u) * P1 * TB;
+            if constexpr (TB == 1) {
+                const uint32_t sh = s - 1u + b;
+                const uint32_t keep = ~(mask | (1u << sh));
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t en = Ts[tp[e]];
+                    tp[e] = (tp[e] & keep) | (en & 0x7fu) | ((en >> 7) << sh);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) tp[e] = reinterpret_cast<const uint16_t*>(Ts)[tp[e]];
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if constexpr (TB == 1) tp[e] = (tp[e] & ~(2u * M - 1u)) | L1[tp[e]];
+            else tp[e] = reinterpret_cast<const uint16_t*>(L1)[tp[e]];
+        }
+        float v[4 * D];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if constexpr (D == 1) {
+                v[e] = xs[tp[e]];
+            } else if constexpr (D == 2) {
+                const float2 t = reinterpret_cast<const float2*>(xs)[tp[e]];
+                v[2 * e] = t.x;
+                v[2 * e + 1] = t.y;
+            } else {
+#pragma unroll
+                for (int c = 0; c < D / 4; ++c) {
+                    const float4 t = reinterpret_cast<const float4*>(xs)[tp[e] * (D / 4) + c];
+                    v[e * D + 4 * c] = t.x;
+                    v[e * D + 4 * c + 1] = t.y;
+                    v[e * D + 4 * c + 2] = t.z;
+                    v[e * D + 4 * c + 3] = t.w;
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < D; ++c)
+            reinterpret_cast<float4*>(a.x_out + (uint64_t)(base + 4u * q) * D)[c] =
+                make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+    }
+
+    // ---- 7. warp 0: the tile's estimate partial (off the critical path) ----------------
+    if (warp == 0) {
+        float tmax = -CUDART_INF_F;
+        for (uint32_t wv = 0; wv < nwarps; ++wv) tmax = fmaxf(tmax, red[wv * PS]);
+        for (uint32_t k = lane; k < (uint32_t)PS; k += 32u) {  // PS can exceed 32 (d = 8)
+            double v;
+            if (k == 0) {
+                v = (double)tmax;
+            } else {
+                v = 0.0;
+                for (uint32_t wv = 0; wv < nwarps; ++wv) {
+                    const float wm = red[wv * PS];
+                    const float f = (k < (uint32_t)(2 + 2 * D)) ? (wm == -CUDART_INF_F ? 0.0f : expf(wm - tmax)) : 1.0f;
+                    v += (double)(red[wv * PS + k] * f);
+                }
+            }
+            a.part[(uint64_t)tile * PS + k] = v;
+        }
+    }
+}
+
+}  // namespace pfk

@@ -1,0 +1,336 @@
+// pf_stages.cuh -- k_stages: butterfly stages s0 .. s0+k-1 (s0 >= 2) over one tile held in
+// shared memory, moving the particle states once per pass.
+//
+// Tile: the 2^k groups that the butterfly pairs at stages s0..s0+k-1, i.e. global groups
+//   g(j) = tlo | (j << (s0-1)) | thi,   j in [0, 2^k)   (tile-local group index j)
+// so stage s0+st pairs j with j ^ 2^st (eq. `A matrices`; pairing by
+// Lemma `facts about A`).  Tile position tp = (j << b) | i, i < M = 2^b.
+//
+//   A  the tile's states (stage s0-1) are copied global -> shared with TMA bulk copies
+//      (one per group of M contiguous particles);
+//   B  every stage's draws: a draw depends only on its Philox word and the stage's side
+//      threshold (reading R1; for s >= 2, V_{s-1} is constant over each group,
+//      SURVEY.md App. A.2), never on another stage, so all k stages are drawn without
+//      barriers into per-stage tables T_st[tp]: 1 byte (side << 7 | index) when M <= 128,
+//      else the 16-bit tile position of the source;
+//   C  each output walks its ancestry back, tp -> a_{s0+k-1}(tp) -> ... -> a_{s0}(.)
+//      (the composition of Alg. 3's stages, licensed by Lemma facts_about_Vs (a),
+//      PAPER.md:645), reads that state from shared memory and writes it coalesced.
+// The kernel is persistent and software-pipelined (see k_stages below).
+//
+// Measured and rejected: spreading a larger tile over a thread-block cluster and reading
+// the sources through DSMEM (random 16-byte remote reads ran ~4x slower than a whole
+// extra HBM pass; profiles/r1_ncu_k_stages_v1_cluster_experiment.txt).
+#pragma once
+#include <cstdint>
+
+#include "pf_kernels.cuh"
+
+namespace pfk {
+
+struct StageArgs {
+    Key key;
+    uint32_t n;
+    uint64_t N;     // particles of this shard
+    uint32_t pos0;  // global index of the shard's first particle (RNG counters)
+    uint32_t m, M, b, s0, k, P, lowbits;
+    uint32_t pipe;        // 1: software-pipelined (two buffers of everything); 0: one buffer
+    const void* pin;      // states at stage s0-1 (packed AoS, shard-local)
+    void* pout;           // states at stage s0+k-1
+    const uint32_t* thr;  // side thresholds, level-table layout (level_offset)
+    int32_t* dbg_anc;     // per-stage ancestor tables (debug) or nullptr
+};
+
+// Shared memory: two tile-state buffers, two table sets (tile t-1 is walked while tile t
+// is drawn), two threshold copies, two mbarriers; one of each when not pipelined.
+__host__ __device__ inline uint32_t stages_smem(uint32_t P, uint32_t state_bytes, uint32_t k, uint32_t tb,
+                                                uint32_t pipe = 1u) {
+    const uint32_t st = (P * state_bytes + 15u) & ~15u;
+    const uint32_t tab = (k * P * tb + 15u) & ~15u;
+    const uint32_t nb = pipe ? 2u : 1u;
+    return nb * (st + tab + 4u * (1u << k)) + 16u;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void cp_async_bytes(void* smem_dst, const void* gsrc, int bytes) {
+    const uint32_t d = smem_u32(smem_dst);
+    if (bytes == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc));
+    else if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc));
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gsrc));
+}
+
+// mbarrier + TMA bulk copy (global -> shared, completion counted in bytes on the barrier)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+struct StageTile {
+    uint32_t tlo, thi;
+};
+
+__device__ __forceinline__ StageTile stage_tile_geom(const StageArgs& a, uint32_t t) {
+    StageTile g;
+    g.tlo = t & ((1u << a.lowbits) - 1u);
+    g.thi = (t >> a.lowbits) << (a.lowbits + a.k);
+    return g;
+}
+
+// Copies of tile t's states (stage s0-1): one TMA bulk copy per group (M contiguous
+// particles) completing on `bar`, or per-thread cp.async when a group is < 16 bytes.
+template <typename T>
+__device__ __forceinline__ void stage_states_load(const StageArgs& a, const StageTile& g, T* xs, uint64_t* bar) {
+    const uint32_t b = a.b, lowbits = a.lowbits, G = 1u << a.k;
+    constexpr uint32_t SB = (uint32_t)sizeof(T);
+    const uint32_t gbytes = a.M * SB;
+    const char* gin = reinterpret_cast<const char*>(a.pin);
+    char* sdst = reinterpret_cast<char*>(xs);
+    if (gbytes >= 16u) {
+        if (threadIdx.x < 32u) {
+            if (threadIdx.x == 0) mbar_expect_tx(bar, G * gbytes);
+            __syncwarp();
+            for (uint32_t j = threadIdx.x; j < G; j += 32u) {
+                const uint64_t gg = g.tlo | (j << lowbits) | g.thi;
+                bulk_g2s(sdst + (size_t)j * gbytes, gin + (gg << b) * SB, gbytes, bar);
+            }
+        }
+    } else {  // d = 1, M = 2: 8-byte groups
+        for (uint32_t j = threadIdx.x; j < G; j += blockDim.x) {
+            const uint64_t gg = g.tlo | (j << lowbits) | g.thi;
+            cp_async_bytes(sdst + (size_t)j * gbytes, gin + (gg << b) * SB, (int)gbytes);
+        }
+    }
+}
+
+// Tile t's thresholds: stage st has 2^{k-st-1} entries at offset 2^k - 2^{k-st}.
+__device__ __forceinline__ void stage_thresholds_load(const StageArgs& a, const StageTile& g, uint32_t* ths) {
+    const uint32_t k = a.k, E = (1u << k) - 1u;
+    for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
+        const uint32_t u = (1u << k) - e;
+        const uint32_t st = k - (32u - __clz(u - 1u));
+        const uint32_t off = (1u << k) - (1u << (k - st));
+        const uint32_t s = a.s0 + st;
+        cp_async_bytes(ths + e, a.thr + level_offset(a.m, (int)s) + (g.thi >> s) + (e - off), 4);
+    }
+}
+
+// B: all k stages' draws of the thread's quads of one tile into the tables.
+template <int TB, bool DBG, int QPT>
+__device__ __forceinline__ void stage_draws(const StageArgs& a, const StageTile& g, const uint32_t* ths,
+                                            unsigned char* tabs) {
+    const uint32_t M = a.M, b = a.b, k = a.k, P = a.P, mask = M - 1u, nq = P >> 2, lowbits = a.lowbits;
+    const uint32_t tlo = g.tlo, thi = g.thi;
+#pragma unroll
+    for (int it = 0; it < QPT; ++it) {
+        const uint32_t q = threadIdx.x + it * blockDim.x;
+        if (q >= nq) break;
+        const uint32_t l0 = 4u * q;
+        if (M >= 4u) {  // the quad lies in one group: one Philox block per stage
+            const uint32_t j = l0 >> b;
+            const uint32_t gp0 = ((tlo | (j << lowbits) | thi) << b) | (l0 & mask);
+            const uint32_t c0 = (a.pos0 + gp0) >> 2;
+            uint32_t toff = 0;  // offset of stage st's thresholds
+            for (uint32_t st = 0; st < k; ++st) {
+                const uint32_t s = a.s0 + st, bit = 1u << st;
+                const uint4 blk = rng_block(a.key, c0, a.n, kDomainResample, s);
+                const uint32_t Pt = ths[toff + (j >> (st + 1))];
+                toff += (1u << k) >> (st + 1);
+                const uint32_t rw[4] = {blk.x, blk.y, blk.z, blk.w};
+                const uint32_t blo = (j & ~bit) << b, bhi = (j | bit) << b;
+                uint32_t en[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const bool hi = (rw[e] >> b) >= Pt;
+                    if constexpr (TB == 1) en[e] = (rw[e] & mask) | (hi ? 0x80u : 0u);
+                    else en[e] = (hi ? bhi : blo) | (rw[e] & mask);
+                }
+                if constexpr (TB == 1)
+                    *reinterpret_cast<uint32_t*>(tabs + st * P + l0) = en[0] | (en[1] << 8) | (en[2] << 16) | (en[3] << 24);
+                else
+                    *reinterpret_cast<uint2*>(tabs + 2u * (st * P + l0)) = make_uint2(en[0] | (en[1] << 16), en[2] | (en[3] << 16));
+                if constexpr (DBG) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const bool hi = (rw[e] >> b) >= Pt;
+                        const uint32_t jj = hi ? (j | bit) : (j & ~bit);
+                        const uint32_t gsrc = ((tlo | (jj << lowbits) | thi) << b) | (rw[e] & mask);
+                        a.dbg_anc[(uint64_t)(s - 1) * a.N + gp0 + e] = (int32_t)(a.pos0 + gsrc);
+                    }
+                }
+            }
+        } else {  // M == 2: the quad spans tile groups j0, j0+1 (two Philox blocks per stage)
+            const uint32_t j0 = l0 >> 1;
+            uint32_t gpa[2], c0[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                gpa[h] = (tlo | ((j0 + h) << lowbits) | thi) << 1;
+                c0[h] = (a.pos0 + gpa[h]) >> 2;
+            }
+            uint32_t toff = 0;
+            for (uint32_t st = 0; st < k; ++st) {
+                const uint32_t s = a.s0 + st, bit = 1u << st;
+                uint32_t en[4];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t j = j0 + h;
+                    const uint4 blk = rng_block(a.key, c0[h], a.n, kDomainResample, s);
+                    const bool upper = ((a.pos0 + gpa[h]) & 2u) != 0u;
+                    const uint32_t w0 = upper ? blk.z : blk.x, w1 = upper ? blk.w : blk.y;
+                    const uint32_t Pt = ths[toff + (j >> (st + 1))];
+                    const uint32_t w[2] = {w0, w1};
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const bool hi = (w[e] >> 1) >= Pt;
+                        if constexpr (TB == 1) en[2 * h + e] = (w[e] & 1u) | (hi ? 0x80u : 0u);
+                        else en[2 * h + e] = ((hi ? (j | bit) : (j & ~bit)) << 1) | (w[e] & 1u);
+                        if constexpr (DBG) {
+                            const uint32_t jj = hi ? (j | bit) : (j & ~bit);
+                            const uint32_t gsrc = ((tlo | (jj << lowbits) | thi) << 1) | (w[e] & 1u);
+                            a.dbg_anc[(uint64_t)(s - 1) * a.N + gpa[h] + e] = (int32_t)(a.pos0 + gsrc);
+                        }
+                    }
+                }
+                toff += (1u << k) >> (st + 1);
+                if constexpr (TB == 1)
+                    *reinterpret_cast<uint32_t*>(tabs + st * P + l0) = en[0] | (en[1] << 8) | (en[2] << 16) | (en[3] << 24);
+                else
+                    *reinterpret_cast<uint2*>(tabs + 2u * (st * P + l0)) = make_uint2(en[0] | (en[1] << 16), en[2] | (en[3] << 16));
+            }
+        }
+    }
+}
+
+// C: each of the thread's outputs walks back through the tables, reads its source state
+// and writes it coalesced.
+template <typename T, int TB, int QPT>
+__device__ __forceinline__ void stage_walk(const StageArgs& a, const StageTile& g, const T* xs,
+                                           const unsigned char* tabs) {
+    const uint32_t M = a.M, b = a.b, k = a.k, P = a.P, mask = M - 1u, nq = P >> 2, lowbits = a.lowbits;
+    T* pout = reinterpret_cast<T*>(a.pout);
+#pragma unroll
+    for (int it = 0; it < QPT; ++it) {
+        const uint32_t q = threadIdx.x + it * blockDim.x;
+        if (q >= nq) break;
+        const uint32_t l0 = 4u * q;
+        uint32_t tp[4] = {l0, l0 + 1u, l0 + 2u, l0 + 3u};
+        for (int st = (int)k - 1; st >= 0; --st) {
+            if constexpr (TB == 1) {
+                const unsigned char* Ts = tabs + (uint32_t)st * P;
+                const uint32_t sh = (uint32_t)st + b;
+                const uint32_t keep = ~(mask | (1u << sh));
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t en = Ts[tp[e]];
+                    tp[e] = (tp[e] & keep) | (en & 0x7fu) | ((en >> 7) << sh);
+                }
+            } else {
+                const uint16_t* Ts = reinterpret_cast<const uint16_t*>(tabs) + (uint32_t)st * P;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) tp[e] = Ts[tp[e]];
+            }
+        }
+        Vec4<T> v;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v.v[e] = xs[tp[e]];
+        const uint32_t j = l0 >> b;
+        const uint32_t gp0 = ((g.tlo | (j << lowbits) | g.thi) << b) | (l0 & mask);
+        if (M >= 4u) {
+            *reinterpret_cast<Vec4<T>*>(pout + gp0) = v;
+        } else {
+            const uint32_t gp1 = (g.tlo | ((j + 1u) << lowbits) | g.thi) << 1;
+            pout[gp0] = v.v[0];
+            pout[gp0 + 1] = v.v[1];
+            pout[gp1] = v.v[2];
+            pout[gp1 + 1] = v.v[3];
+        }
+    }
+}
+
+// Persistent and software-pipelined: CTA c owns tiles t_i = c + i gridDim.x.  Iteration i
+// walks and writes tile t_{i-1} (tables and states of slot (i-1) & 1) while drawing tile
+// t_i into the other table set; the states of t_i are copied (TMA bulk) during iteration
+// i and consumed in iteration i+1; the thresholds of t_{i+1} arrive during iteration i.
+// Even warps walk first and odd warps draw first, so the Philox-heavy draws and the
+// shared-memory-heavy walk overlap on every SM sub-partition.  One barrier per tile.
+template <typename T, int TB, bool DBG, int QPT>
+__global__ void __launch_bounds__(1024, 1) k_stages(const __grid_constant__ StageArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t k = a.k, P = a.P;
+    const uint32_t ntiles = (uint32_t)(a.N / P);
+    const uint32_t stb = (P * (uint32_t)sizeof(T) + 15u) & ~15u;
+    const uint32_t ttb = (k * P * TB + 15u) & ~15u;
+    const uint32_t nb = a.pipe ? 2u : 1u;
+    unsigned char* tab0 = smem + nb * stb;
+    uint32_t* th0 = reinterpret_cast<uint32_t*>(tab0 + nb * ttb);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(th0 + (nb << k));
+    auto xbuf = [&](uint32_t sl) { return reinterpret_cast<T*>(smem + sl * stb); };
+    auto tbuf = [&](uint32_t sl) { return tab0 + sl * ttb; };
+    auto thbuf = [&](uint32_t sl) { return th0 + (sl << k); };
+    const bool bulk = a.M * (uint32_t)sizeof(T) >= 16u;
+
+    const uint32_t t0 = blockIdx.x;
+    if (t0 >= ntiles) return;
+    const uint32_t nt = (ntiles - t0 + gridDim.x - 1u) / gridDim.x;  // tiles of this CTA
+    if (threadIdx.x == 0) {
+        mbar_init(bars, 1u);
+        mbar_init(bars + 1, 1u);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (!a.pipe) {  // one buffer: load, draw, walk, tile after tile
+        for (uint32_t i = 0; i < nt; ++i) {
+            const StageTile g = stage_tile_geom(a, t0 + i * gridDim.x);
+            stage_states_load<T>(a, g, xbuf(0u), bars);
+            stage_thresholds_load(a, g, thbuf(0u));
+            asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
+            __syncthreads();
+            stage_draws<TB, DBG, QPT>(a, g, thbuf(0u), tbuf(0u));
+            if (bulk) mbar_wait(bars, i & 1u);
+            __syncthreads();
+            stage_walk<T, TB, QPT>(a, g, xbuf(0u), tbuf(0u));
+            __syncthreads();
+        }
+        return;
+    }
+    stage_thresholds_load(a, stage_tile_geom(a, t0), thbuf(0u));
+    asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+
+    const bool walk_first = ((threadIdx.x >> 5) & 1u) == 0u;
+    for (uint32_t i = 0; i <= nt; ++i) {
+        const uint32_t sl = i & 1u;
+        const StageTile gi = stage_tile_geom(a, t0 + i * gridDim.x);
+        const StageTile gp = stage_tile_geom(a, t0 + (i - 1u) * gridDim.x);
+        if (i < nt) stage_states_load<T>(a, gi, xbuf(sl), bars + sl);      // consumed in iteration i+1
+        if (i + 1 < nt) stage_thresholds_load(a, stage_tile_geom(a, t0 + (i + 1) * gridDim.x), thbuf(sl ^ 1u));
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        if (i >= 1u && bulk) mbar_wait(bars + (sl ^ 1u), ((i - 1u) >> 1) & 1u);
+        if (walk_first) {
+            if (i >= 1u) stage_walk<T, TB, QPT>(a, gp, xbuf(sl ^ 1u), tbuf(sl ^ 1u));
+            if (i < nt) stage_draws<TB, DBG, QPT>(a, gi, thbuf(sl), tbuf(sl));
+        } else {
+            if (i < nt) stage_draws<TB, DBG, QPT>(a, gi, thbuf(sl), tbuf(sl));
+            if (i >= 1u) stage_walk<T, TB, QPT>(a, gp, xbuf(sl ^ 1u), tbuf(sl ^ 1u));
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+    }
+}
+
+}  // namespace pfk
