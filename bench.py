@@ -148,18 +148,12 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- ours
-def algorithmic_bytes(cfg, kernel: str, passes, index_mode: bool) -> float:
+def algorithmic_bytes(cfg, kernel: str) -> float:
     """Algorithmic HBM bytes per launch: the bytes the kernel must move
     once, with no sector amplification and no re-reads.  cfg: this rank's shard."""
     N, d = cfg.N, cfg.d
-    if kernel == "k_pass1":
-        return N * (8 * d + (4 if index_mode else 0))   # read xhat (+ ancestor), write x
-    if kernel == "k_compose":
-        if index_mode:  # first pass writes 4 B, later passes read + write 4 B
-            per = [4 if i == 0 else 8 for i in range(passes)]
-        else:
-            per = [8 * d] * passes
-        return N * sum(per) / max(passes, 1)
+    if kernel in ("k_pass1", "k_stages"):
+        return N * 8 * d   # read the tile's states once, write them once
     if kernel == "k_cross":
         return N * 8 * d + N * 4 * d  # own read + write, partner half on average
     if kernel in ("k_cascade", "k_top"):
@@ -262,9 +256,7 @@ def run_ours(args):
         dom = max(kt, key=lambda k: kt[k][0])
         dom_ms, dom_n = kt[dom]
         cfg_loc = cfg.with_sizes(cfg.M, cfg.m // world)
-        passes = kt.get("k_compose", (0, 0))[1] // max(args.steps, 1)
-        alg = algorithmic_bytes(cfg_loc, dom, passes, index_mode=(world == 1 and cfg.d >= 4 and
-                                                                  os.environ.get("PF_INDEX_MODE", "1") != "0"))
+        alg = algorithmic_bytes(cfg_loc, dom)
         achieved = alg / (dom_ms / dom_n / 1e3) / 1e9
         peak, peak_src = measured_peak()
         roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

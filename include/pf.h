@@ -182,7 +182,7 @@ int pf_last_step_launches(const pf_handle* h);
 /* --- kernel timing (bench accounting) ------------------------------------------ */
 #define PF_KERNEL_PASS1 0   /* k_pass1: mutate + weight + stages 1..k1 */
 #define PF_KERNEL_CASCADE 1 /* k_cascade: V levels, thresholds, estimates */
-#define PF_KERNEL_COMPOSE 2 /* k_compose / k_move: stages k1+1..S (S_loc when sharded) */
+#define PF_KERNEL_STAGES 2 /* k_stages: stages k1+1..S (S_loc when sharded) */
 #define PF_KERNEL_TOP 3     /* k_top: cross-shard V levels and estimate (sharded) */
 #define PF_KERNEL_CROSS 4   /* k_cross: one cross-shard stage (sharded) */
 #define PF_KERNEL_KINDS 5

@@ -500,9 +500,9 @@ static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
     // stages k1+1..S: state-moving tile passes
     int xs = dst;
     for (const StagePass& sp : p.passes) {
-        h->mark(PF_KERNEL_COMPOSE, true);
+        h->mark(PF_KERNEL_STAGES, true);
         launch_stages_k(h, sp, h->X(xs), h->X(xs ^ 1));
-        h->mark(PF_KERNEL_COMPOSE, false);
+        h->mark(PF_KERNEL_STAGES, false);
         xs ^= 1;
         ++launches;
     }

@@ -86,7 +86,7 @@ EXPORTED = ["pf_workspace_bytes", "pf_init", "pf_step", "pf_step_dev", "pf_estim
             "pf_timing_enable", "pf_timing_read", "pf_workspace_bytes_sharded", "pf_init_sharded",
             "pf_step_local", "pf_shard_record", "pf_step_top", "pf_cross_buffer", "pf_cross_stage"]
 PF_KERNEL_KINDS = 5
-KERNEL_NAMES = ("k_pass1", "k_cascade", "k_compose", "k_top", "k_cross")
+KERNEL_NAMES = ("k_pass1", "k_cascade", "k_stages", "k_top", "k_cross")
 
 
 def _check(rc: int, h=None):
