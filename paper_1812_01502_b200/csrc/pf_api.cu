@@ -20,8 +20,14 @@ using namespace pfk;
 
 namespace {
 
+// k_pass1 tile: shared-memory budget and threads per CTA.  Smaller tiles with two quads per
+// thread win for d = 4 (C4: 7.17 -> 5.62 ms per launch, one more stage moves into the
+// k_stages passes at no extra pass; profiles/r1_stage_pass_experiments.md); the other
+// dimensions keep the larger tile (C2, C3 measured slower with it).
 constexpr uint32_t kPass1SmemBudgetDefault = 64u * 1024u;
 constexpr uint32_t kPass1ThreadsDefault = 256u;
+constexpr uint32_t kPass1SmemBudgetD4 = 40000u;
+constexpr uint32_t kPass1ThreadsD4 = 128u;
 constexpr uint32_t kStageSmemDefault = 232448u;  // one persistent CTA per SM
 constexpr uint32_t kStageThreadsDefault = 1024u;
 constexpr uint32_t kSmemPerSM = 233472u;          // 228 KiB (1 KiB of it reserved per CTA)
@@ -74,8 +80,8 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, uint64
     const int S = ilog2_exact(m);
     Plan p;
     p.D = d;
-    const uint32_t budget1 = env_u32("PF_PASS1_SMEM", kPass1SmemBudgetDefault);
-    const uint32_t threads1 = env_u32("PF_PASS1_THREADS", kPass1ThreadsDefault);
+    const uint32_t budget1 = env_u32("PF_PASS1_SMEM", d == 4 ? kPass1SmemBudgetD4 : kPass1SmemBudgetDefault);
+    const uint32_t threads1 = env_u32("PF_PASS1_THREADS", d == 4 ? kPass1ThreadsD4 : kPass1ThreadsDefault);
     const uint32_t maxqpt1 = env_u32("PF_PASS1_MAXQPT", 8u);
     // pass-1 tile: the largest 2^k1 <= 64 groups (k1 <= S) whose shared memory fits the budget
     uint32_t P1 = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(N, (uint64_t)kPass1MaxGroups * M),
