@@ -55,6 +55,12 @@ def lib():
         _lib.orc_augmented_resample_sampled.argtypes = [u64, u64, u64, u32, vp, u64, vp, vp, vp, vp, vp, vp]
         _lib.orc_estimates.argtypes = [ctypes.c_int, u64, vp, vp, vp, vp, vp, vp]
         _lib.orc_step.argtypes = [vp, u64, u64, u64, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        _lib.orc_augmented_resample_partial.argtypes = [u64, u64, u64, u32, vp, ctypes.c_int, vp, vp, vp, vp]
+        _lib.orc_ess_levels.argtypes = [u64, u64, vp, vp, vp]
+        _lib.orc_stages_to_run.argtypes = [ctypes.c_int, vp, ctypes.c_double]
+        _lib.orc_stages_to_run.restype = ctypes.c_int
+        _lib.orc_step_adaptive.argtypes = [vp, u64, u64, u64, u32, vp, vp, vp, ctypes.c_double, vp, vp, vp, vp,
+                                           vp, vp, vp, vp, vp, vp, vp, vp]
     return _lib
 
 
@@ -204,3 +210,80 @@ def run_filter(params: dict, M: int, m: int, seed: int, ys: np.ndarray, x0: Opti
         means[n] = r["filter"][:d]
         x = r["xhat"].astype(np.float32)
     return means
+
+
+# ----------------------------------------------------------------------------- fully adapted
+def augmented_resample_partial(lw: np.ndarray, M: int, seed: int, n: int, S_exec: int) -> dict:
+    """Alg. 3 with only stages 1..S_exec executed (all V levels computed)."""
+    lw = np.ascontiguousarray(lw, dtype=np.float64)
+    N = lw.shape[0]
+    m = N // M
+    S = int(round(np.log2(m)))
+    a = np.zeros((S, N), np.int32)
+    delta = np.zeros((S, N), np.float32)
+    logV = np.zeros(m - 1, np.float64)
+    A = np.zeros(N, np.int64)
+    rc = lib().orc_augmented_resample_partial(N, M, seed, n, _ptr(lw), int(S_exec), _ptr(a), _ptr(delta),
+                                              _ptr(logV), _ptr(A))
+    if rc != 0:
+        raise ValueError(f"orc_augmented_resample_partial rc={rc}")
+    return dict(a=a, delta=delta, logV=logV, A=A, S=S, m=m)
+
+
+def ess_levels(lw: np.ndarray, M: int, logV: np.ndarray) -> np.ndarray:
+    """ESS of the stage weights V_0 = w, V_1, ..., V_S."""
+    lw = np.ascontiguousarray(lw, dtype=np.float64)
+    N = lw.shape[0]
+    S = int(round(np.log2(N // M)))
+    lv = np.ascontiguousarray(logV, dtype=np.float64)
+    ess = np.zeros(S + 1)
+    lib().orc_ess_levels(N, M, _ptr(lw), _ptr(lv), _ptr(ess))
+    return ess
+
+
+def stages_to_run(ess: np.ndarray, theta: float) -> int:
+    e = np.ascontiguousarray(ess, dtype=np.float64)
+    return int(lib().orc_stages_to_run(len(e) - 1, _ptr(e), float(theta)))
+
+
+def step_adaptive(params: dict, N: int, M: int, seed: int, n: int, y: np.ndarray, xin: np.ndarray,
+                  lwc_in: np.ndarray, theta: float) -> dict:
+    """One step of the fully adapted filter (orc_step_adaptive)."""
+    mdl = make_model(params)
+    d = mdl.d
+    m = N // M
+    S = int(round(np.log2(m)))
+    xin = np.ascontiguousarray(xin, dtype=np.float32).reshape(N, d)
+    lwc = np.ascontiguousarray(lwc_in, dtype=np.float64).reshape(N)
+    yy = np.ascontiguousarray(y, dtype=np.float32)
+    out = dict(x=np.zeros((N, d)), lw=np.zeros(N), a=np.zeros((S, N), np.int32), delta=np.zeros((S, N), np.float32),
+               logV=np.zeros(m - 1), A=np.zeros(N, np.int64), xhat=np.zeros((N, d)), lwc=np.zeros(N),
+               filter=np.zeros(2 * d), predict=np.zeros(2 * d), ess=np.zeros(S + 1))
+    ss = ctypes.c_int(-1)
+    rc = lib().orc_step_adaptive(ctypes.byref(mdl), N, M, seed, n, _ptr(yy), _ptr(xin), _ptr(lwc), float(theta),
+                                 _ptr(out["x"]), _ptr(out["lw"]), _ptr(out["a"]), _ptr(out["delta"]),
+                                 _ptr(out["logV"]), _ptr(out["A"]), _ptr(out["xhat"]), _ptr(out["lwc"]),
+                                 _ptr(out["filter"]), _ptr(out["predict"]), _ptr(out["ess"]), ctypes.byref(ss))
+    if rc != 0:
+        raise ValueError(f"orc_step_adaptive rc={rc}")
+    out["S"], out["m"], out["sstar"] = S, m, int(ss.value)
+    return out
+
+
+def run_filter_adaptive(params: dict, M: int, m: int, seed: int, ys: np.ndarray, theta: float,
+                        x0: Optional[np.ndarray] = None):
+    """The fully adapted filter for len(ys) steps: per-step filter means (T x d) and the
+    number of stages run at each step."""
+    N = M * m
+    d = int(params["d"])
+    x = (init(params, N, seed) if x0 is None else x0).astype(np.float32)
+    lwc = np.zeros(N)
+    means = np.zeros((len(ys), d))
+    stages = np.zeros(len(ys), np.int32)
+    for n, y in enumerate(ys):
+        r = step_adaptive(params, N, M, seed, n, y, x, lwc, theta)
+        means[n] = r["filter"][:d]
+        stages[n] = r["sstar"]
+        x = r["xhat"].astype(np.float32)
+        lwc = r["lwc"]
+    return means, stages

@@ -293,14 +293,37 @@ static double pair_cdf(const double* lw, uint64_t base, uint64_t twoM, double* C
     return mx;
 }
 
+/* Alg. 3 with only the first S_exec stages executed (0 <= S_exec <= S): the V levels are
+ * computed for every s = 1..S (they depend on the weights only, eq. V_defn_proofs), the
+ * draws and the composition for s <= S_exec.  S_exec = S is Alg. 3; S_exec < S is the
+ * early stop of the fully adapted scheme.  Stage tables of stages
+ * > S_exec are left untouched. */
+static int augmented_resample_upto(uint64_t N, uint64_t M, uint64_t seed, uint32_t n, const double* lw,
+                                   int S_exec, int32_t* a, float* delta, double* logV, int64_t* A);
+
 int orc_augmented_resample(uint64_t N, uint64_t M, uint64_t seed, uint32_t n, const double* lw,
                            int32_t* a, float* delta, double* logV, int64_t* A)
+{
+    uint64_t m = (M == 0) ? 0 : N / M;
+    int S = ilog2_exact(m);
+    if (S < 1) return ORC_EINVAL;
+    return augmented_resample_upto(N, M, seed, n, lw, S, a, delta, logV, A);
+}
+
+int orc_augmented_resample_partial(uint64_t N, uint64_t M, uint64_t seed, uint32_t n, const double* lw,
+                                   int S_exec, int32_t* a, float* delta, double* logV, int64_t* A)
+{
+    return augmented_resample_upto(N, M, seed, n, lw, S_exec, a, delta, logV, A);
+}
+
+static int augmented_resample_upto(uint64_t N, uint64_t M, uint64_t seed, uint32_t n, const double* lw,
+                                   int S_exec, int32_t* a, float* delta, double* logV, int64_t* A)
 {
     if (M == 0 || N % M != 0) return ORC_EINVAL;
     uint64_t m = N / M;
     int S = ilog2_exact(m);
     int b = ilog2_exact(M);
-    if (S < 1 || b < 0) return ORC_EINVAL;
+    if (S < 1 || b < 0 || S_exec < 0 || S_exec > S) return ORC_EINVAL;
     uint64_t twoM = 2 * M;
     double* lv = (double*)malloc(sizeof(double) * (m - 1));
     double* C = (double*)malloc(sizeof(double) * twoM);
@@ -316,7 +339,7 @@ int orc_augmented_resample(uint64_t N, uint64_t M, uint64_t seed, uint32_t n, co
         double mx = pair_cdf(lw, base, twoM, C);
         /* V_1 = (1/2M) sum_pool g  (eq. V_defn_proofs) */
         lv[level_offset(m, 1) + p] = (mx == -INFINITY) ? -INFINITY : mx + log(C[twoM - 1]) - log((double)twoM);
-        for (uint64_t j = 0; j < twoM; ++j) {
+        for (uint64_t j = 0; j < twoM && S_exec >= 1; ++j) {
             uint64_t i = base + j;
             int64_t ai;
             double dl;
@@ -331,7 +354,7 @@ int orc_augmented_resample(uint64_t N, uint64_t M, uint64_t seed, uint32_t n, co
         double* cur = lv + level_offset(m, s);
         /* V_s = A_s V_{s-1}: block b of level s is the pair mean of blocks 2b, 2b+1. */
         for (uint64_t bk = 0; bk < (m >> s); ++bk) cur[bk] = log_pair_mean(prev[2 * bk], prev[2 * bk + 1]);
-        for (uint64_t i = 0; i < N; ++i) {
+        for (uint64_t i = 0; i < N && s <= S_exec; ++i) {
             int64_t ai;
             double dl;
             stage_s_draw(M, b, s, seed, n, prev, i, &ai, &dl);
@@ -339,15 +362,15 @@ int orc_augmented_resample(uint64_t N, uint64_t M, uint64_t seed, uint32_t n, co
             if (delta) delta[(uint64_t)(s - 1) * N + i] = (float)dl;
         }
     }
-    /* Composition: xi_S^i = xi_0^{a_1(a_2(...a_S(i)))}. */
+    /* Composition: xi_{S_exec}^i = xi_0^{a_1(a_2(...a_{S_exec}(i)))}. */
     if (A) {
         for (uint64_t i = 0; i < N; ++i) {
             uint64_t j = i;
-            for (int s = S; s >= 1; --s) j = (uint64_t)as[(uint64_t)(s - 1) * N + j];
+            for (int s = S_exec; s >= 1; --s) j = (uint64_t)as[(uint64_t)(s - 1) * N + j];
             A[i] = (int64_t)j;
         }
     }
-    if (a) memcpy(a, as, sizeof(int32_t) * N * (uint64_t)S);
+    if (a) memcpy(a, as, sizeof(int32_t) * N * (uint64_t)S_exec);
     if (logV) memcpy(logV, lv, sizeof(double) * (m - 1));
     free(lv); free(C); free(as);
     return ORC_OK;
@@ -473,5 +496,102 @@ int orc_step(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t seed, uint32
         orc_estimates(d, N, lw, x, Aloc, filt, pred, resamp);
     }
     free(xprev); free(Aloc);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Fully adapted augmented resampling (AIRPF2 of PAPER.md:1279).
+ *
+ * ESS of a weight vector w over n equally sized units:
+ *     E = (n^-1 sum w)^2 / (n^-1 sum w^2)  in [1/n, 1],
+ * evaluated "after every stage of augmented resampling" on the stage
+ * weights V_s: s = 0 on the particle weights V_0 = w (N units); s >= 1 on the level-s
+ * values of the V table, which are constant over blocks of 2^s groups, so the N-particle
+ * ESS equals the ESS of the m / 2^s block values.  Log domain, shifted by the max;
+ * sequential fp64 sums.  ess[0..S]. */
+static double ess_of(const double* lv, uint64_t n)
+{
+    double L = -INFINITY;
+    for (uint64_t i = 0; i < n; ++i)
+        if (lv[i] > L) L = lv[i];
+    if (L == -INFINITY) return 1.0; /* all weights zero: no information, treat as equal */
+    double s1 = 0.0, s2 = 0.0;
+    for (uint64_t i = 0; i < n; ++i) {
+        double w = exp(lv[i] - L);
+        s1 += w;
+        s2 += w * w;
+    }
+    return s1 * s1 / ((double)n * s2);
+}
+
+void orc_ess_levels(uint64_t N, uint64_t M, const double* lw, const double* logV, double* ess)
+{
+    uint64_t m = N / M;
+    int S = ilog2_exact(m);
+    ess[0] = ess_of(lw, N);
+    for (int s = 1; s <= S; ++s) ess[s] = ess_of(logV + level_offset(m, s), m >> s);
+}
+
+/* Controller: stage s + 1 runs iff ESS after stage s is below theta (PAPER.md:574,
+ * "executes the resampling step only if E_n is below some predetermined threshold";
+ * strict rule, reading R17).  Returns S* = min{s in 0..S : ess[s] >= theta};
+ * ess[S] = 1 (V_S is constant, Lemma facts_about_Vs (c)) so S* <= S for theta <= 1. */
+int orc_stages_to_run(int S, const double* ess, double theta)
+{
+    for (int s = 0; s < S; ++s)
+        if (ess[s] >= theta) return s;
+    return S;
+}
+
+/* One step of the fully adapted filter from (xin, lwc_in): xin = the state after the
+ * previous step (resampled or not), lwc_in[i] = its carried log-weight (0 after a step
+ * that ran all S stages).  lw = lwc_in + log g_n(x); stages 1..S* run (S* from the ESS
+ * levels of lw); the particles then carry the stage-S* weights V_{S*} (Prop. 1 holds for
+ * the partial product A_{S*}...A_1: sum_i V_{S*}^i P(xi_{S*}^i = xi_0^j) = g_j), stored as
+ *   lwc_out[i] = log V_{S*}(block of i) - log V_S   (S* >= 1; block = group >> S*),
+ *   lwc_out[i] = lw[i] - log V_S                    (S* = 0),
+ * i.e. shifted by the global constant log V_S = log N^-1 sum w, which changes no
+ * normalised quantity (reading R18).  Outputs as orc_step plus ess[S+1], *sstar. */
+int orc_step_adaptive(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t seed, uint32_t n,
+                      const float* y, const float* xin, const double* lwc_in, double theta,
+                      double* x, double* lw, int32_t* a, float* delta, double* logV, int64_t* A,
+                      double* xhat_out, double* lwc_out, double* filt, double* pred, double* ess,
+                      int* sstar)
+{
+    int d = mdl->d;
+    uint64_t m = N / M;
+    int S = ilog2_exact(m);
+    if (S < 1) return ORC_EINVAL;
+    double* xprev = (double*)malloc(sizeof(double) * N * (uint64_t)d);
+    int64_t* Aloc = (int64_t*)malloc(sizeof(int64_t) * N);
+    double* lvl = (double*)malloc(sizeof(double) * (m - 1));
+    if (!xprev || !Aloc || !lvl) {
+        free(xprev); free(Aloc); free(lvl);
+        return ORC_ENOMEM;
+    }
+    for (uint64_t i = 0; i < N * (uint64_t)d; ++i) xprev[i] = (double)xin[i];
+    if (n == 0) memcpy(x, xprev, sizeof(double) * N * (uint64_t)d);
+    else orc_mutate(mdl, N, seed, n, xprev, x);
+    orc_logweight(mdl, N, y, x, lw);
+    for (uint64_t i = 0; i < N; ++i) lw[i] += lwc_in[i];
+    /* levels first (S_exec = 0), then the controller, then the stages */
+    int rc = augmented_resample_upto(N, M, seed, n, lw, 0, NULL, NULL, lvl, NULL);
+    if (rc == ORC_OK) {
+        orc_ess_levels(N, M, lw, lvl, ess);
+        int ss = orc_stages_to_run(S, ess, theta);
+        *sstar = ss;
+        rc = augmented_resample_upto(N, M, seed, n, lw, ss, a, delta, logV, Aloc);
+        if (rc == ORC_OK) {
+            double lvS = lvl[level_offset(m, S)];
+            if (A) memcpy(A, Aloc, sizeof(int64_t) * N);
+            if (xhat_out)
+                for (uint64_t i = 0; i < N; ++i)
+                    for (int k = 0; k < d; ++k) xhat_out[i * d + k] = x[(uint64_t)Aloc[i] * d + k];
+            for (uint64_t i = 0; i < N; ++i)
+                lwc_out[i] = (ss == 0) ? lw[i] - lvS : lvl[level_offset(m, ss) + ((i / M) >> ss)] - lvS;
+            orc_estimates(d, N, lw, x, Aloc, filt, pred, NULL);
+        }
+    }
+    free(xprev); free(Aloc); free(lvl);
     return rc;
 }
