@@ -63,6 +63,8 @@ typedef struct pf_handle pf_handle;
 /* pf_init flags */
 #define PF_FLAG_DEBUG 1u /* keep x_n, log-weights and every stage's ancestor table
                             (S x N int32) for pf_debug_get; test-only, costs HBM */
+#define PF_FLAG_ADAPTIVE 2u /* reserve the buffers of the fully adapted scheme
+                               (pf_set_adaptive; one GPU only): 8 N + 4 N/M + O(N/1024) bytes */
 
 /* Bytes of device workspace pf_init needs for this problem (0 if invalid). */
 size_t pf_workspace_bytes(const pf_model* model, uint64_t N, uint32_t M, uint32_t flags);
@@ -90,6 +92,22 @@ int pf_step(pf_handle* h, const float* y_host);
  * caller can keep the whole observation sequence resident in HBM.  Non-finite
  * device observations are not detected. */
 int pf_step_dev(pf_handle* h, const float* y_dev);
+
+/* --- fully adapted augmented resampling (AIRPF2) ---
+ * With theta in (0, 1], every later pf_step evaluates the ESS of the stage weights
+ *   E_s = (N^-1 sum_i V_s^i)^2 / (N^-1 sum_i (V_s^i)^2),  s = 0 (V_0 = the weights), 1..S
+ * (reading R17) after weighting -- every V_s is known then --
+ * and runs stages 1..S* only, S* = min{s : E_s >= theta} (stage s+1 runs iff E_s < theta;
+ * S* <= S since E_S = 1).  The particles then carry the weights V_{S*} into the next
+ * step (reading R18); with S* = S nothing is carried and the step equals pf_step's.
+ * theta = 0 switches back to the plain step (the carried weights are dropped).
+ * Needs a handle created with PF_FLAG_ADAPTIVE and world = 1.  pf_step synchronises the
+ * stream once per step (the host reads S* to launch only the passes it needs).
+ * Errors: PF_EINVAL (theta outside [0, 1], no PF_FLAG_ADAPTIVE, sharded handle). */
+int pf_set_adaptive(pf_handle* h, double theta);
+
+/* S* of the last completed step (S for a plain step), or -1 before the first step. */
+int pf_last_stages(const pf_handle* h);
 
 /* estimates (phi) */
 #define PF_PHI_X 1  /* phi(x) = x_k, k = 0..d-1 */
@@ -159,6 +177,7 @@ int pf_cross_stage(pf_handle* h, int t, const void* dev_partner_states);
 #define PF_DBG_XHAT 5      /* x_hat_n = x_n[A(i)], N x d fp32 */
 #define PF_DBG_LOGV 6      /* log V_s per block, all levels s = 1..S, m-1 fp64
                               (level s at offset m - m/2^{s-1}, m/2^s entries) */
+#define PF_DBG_ESS 8       /* E_0..E_S of the last adaptive step, S+1 fp64 (PF_FLAG_ADAPTIVE) */
 #define PF_DBG_THRESH 7    /* stage s >= 2 side thresholds floor(p 2^{32-b}), m-1 uint32,
                               same layout (stage s at offset m - m/2^{s-1}); entry 0.. of
                               level 1 unused */

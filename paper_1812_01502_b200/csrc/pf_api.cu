@@ -189,6 +189,7 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, uint64
 
 struct Layout {
     size_t X0, X1, logV, thr, part, scratch, est, ticket, y;
+    size_t lw0, lw1, carry_lv, ess_part, ess_chunks, ess_out, ess_lmax;  // PF_FLAG_ADAPTIVE
     size_t shard_rec, recs, top_logV, top_thr, top_scratch;
     size_t dbg_x, dbg_lw, dbg_anc, dbg_A;
     size_t total;
@@ -220,6 +221,14 @@ Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags, uint32
     L.top_logV = take((size_t)world * 8);
     L.top_thr = take((size_t)world * 4);
     L.top_scratch = take((size_t)2 * world * PS * 8);
+    const bool ad = flags & PF_FLAG_ADAPTIVE;
+    L.lw0 = take(ad ? N * 4 : 0);
+    L.lw1 = take(ad ? N * 4 : 0);
+    L.carry_lv = take(ad ? (m / 2) * 8 : 0);
+    L.ess_part = take(ad ? (size_t)p.NT * 3 * 8 : 0);
+    L.ess_chunks = take(ad ? (size_t)(p.NT / kEssChunk + 2 * m / kEssChunk + 64) * 2 * 8 : 0);
+    L.ess_out = take(ad ? (size_t)(S + 3) * 8 : 0);
+    L.ess_lmax = take(ad ? 16 : 0);
     const bool dbg = flags & PF_FLAG_DEBUG;
     L.dbg_x = take(dbg ? xb : 0);
     L.dbg_lw = take(dbg ? N * 4 : 0);
@@ -251,6 +260,13 @@ struct pf_handle {
     int cur;             // X buffer that holds the gather source / xhat for the next step
     bool have_step;
     int last_launches;
+    // fully adapted scheme (pf_set_adaptive)
+    double theta = 0.0;
+    int sstar_last = -1;
+    int lwi = 0;             // lw buffer the next weigh pass writes
+    int carry_mode = 0;      // 0 none, 1 particle (lw of the other buffer), 2 block (carry_lv)
+    uint32_t carry_shift = 0;
+    double carry_c = 0.0;
     // kernel timing
     bool timing;
     struct Rec {
@@ -409,16 +425,26 @@ static bool validate_topology(uint64_t N, uint32_t M, std::string* err) {
 
 // ---------------------------------------------------------------------------------------
 // kernel dispatch (instantiations live in pf_inst_*.cu)
-static void launch_pass1(pf_handle* h, const Pass1Args& a) {
+static void launch_pass1(pf_handle* h, const Pass1Args& a, int mode = kPass1Fused) {
     const Plan& p = h->plan;
     const LaunchCfg c{p.NT, p.pass1_threads, p.pass1_smem, h->stream};
     const bool dbg = h->flags & PF_FLAG_DEBUG;
     const int q = (int)p.pass1_qpt;
-    switch (p.D) {
-        case 1: launch_pass1_d1(h->mp.kind, (int)p.tb, dbg, q, c, a); break;
-        case 2: launch_pass1_d2(h->mp.kind, (int)p.tb, dbg, q, c, a); break;
-        case 4: launch_pass1_d4(h->mp.kind, (int)p.tb, dbg, q, c, a); break;
-        default: launch_pass1_d8(h->mp.kind, (int)p.tb, dbg, q, c, a); break;
+    const int k = h->mp.kind, tb = (int)p.tb;
+    if (mode == kPass1Fused) {
+        switch (p.D) {
+            case 1: launch_pass1_d1(k, tb, dbg, q, mode, c, a); break;
+            case 2: launch_pass1_d2(k, tb, dbg, q, mode, c, a); break;
+            case 4: launch_pass1_d4(k, tb, dbg, q, mode, c, a); break;
+            default: launch_pass1_d8(k, tb, dbg, q, mode, c, a); break;
+        }
+    } else {
+        switch (p.D) {
+            case 1: launch_pass1_ad_d1(k, tb, dbg, q, mode, c, a); break;
+            case 2: launch_pass1_ad_d2(k, tb, dbg, q, mode, c, a); break;
+            case 4: launch_pass1_ad_d4(k, tb, dbg, q, mode, c, a); break;
+            default: launch_pass1_ad_d8(k, tb, dbg, q, mode, c, a); break;
+        }
     }
 }
 
@@ -464,11 +490,26 @@ static void launch_stages_k(pf_handle* h, const StagePass& cp, const void* pin, 
     launch_stages(h->plan.D, (int)cp.tb, (h->flags & PF_FLAG_DEBUG) != 0, (int)cp.qpt, c, a);
 }
 
-static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
-    const int D = h->plan.D;
+// A k_stages pass over stages s0..s0+k-1 (k <= the plan's pass), sized like make_plan.
+static StagePass stage_pass_for(const pf_handle* h, const StagePass& sp, uint32_t k) {
+    if (k == sp.k) return sp;
+    StagePass q = sp;
+    const uint32_t sb = (uint32_t)(4 * h->plan.D);
+    q.k = k;
+    q.P = h->M << k;
+    q.threads = pick_threads(q.P / 4, env_u32("PF_STAGE_THREADS", kStageThreadsDefault), &q.qpt);
+    q.smem = stages_smem(q.P, sb, k, q.tb, q.pipe);
+    int nsm = 148, dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        nsm = 148;
+    const uint32_t per_sm = std::max(1u, std::min(kSmemPerSM / (q.smem + 1024u), 2048u / q.threads));
+    q.grid = (uint32_t)std::min<uint64_t>(h->N / q.P, (uint64_t)nsm * per_sm);
+    return q;
+}
+
+static void fill_pass1(pf_handle* h, Pass1Args& a, const float* y_host, const float* y_dev) {
     const Plan& p = h->plan;
     const bool dbg = h->flags & PF_FLAG_DEBUG;
-    Pass1Args a;
     a.mp = h->mp;
     a.key = make_key(h->seed);
     a.n = h->n;
@@ -485,15 +526,124 @@ static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
     a.P1 = p.P1;
     a.T1 = p.P1 / h->M;
     a.sl = pass1_smem(p.D, p.P1, h->M, p.k1, p.pass1_threads, p.tb);
-    const int src = h->cur, dst = h->cur ^ 1;
-    a.x_in = h->X(src);
-    a.x_out = h->X(dst);
     a.logV = h->at<double>(h->lay.logV);
     a.thr = h->at<uint32_t>(h->lay.thr);
     a.part = h->at<double>(h->lay.part);
     a.dbg_x = dbg ? h->at<float>(h->lay.dbg_x) : nullptr;
     a.dbg_lw = dbg ? h->at<float>(h->lay.dbg_lw) : nullptr;
     a.dbg_anc = dbg ? h->at<int32_t>(h->lay.dbg_anc) : nullptr;
+    a.lw_out = nullptr;
+    a.lw_in = nullptr;
+    a.carry_mode = 0;
+    a.carry_lw = nullptr;
+    a.carry_lv = nullptr;
+    a.carry_shift = 0;
+    a.carry_c = 0.0;
+    a.ess_part = nullptr;
+    a.ess_lmax = nullptr;
+}
+
+// One step of the fully adapted scheme (include/pf.h pf_set_adaptive; R17/R18):
+//   k_pass1 (weigh) -> k_cascade -> k_ess -> [host reads S*] -> k_pass1 (resample,
+//   stages 1..min(k1, S*)) -> k_stages passes up to stage S* -> carried weights.
+static int run_step_adaptive(pf_handle* h, const float* y_host, const float* y_dev) {
+    const Plan& p = h->plan;
+    const int src = h->cur, mid = h->cur ^ 1;
+    float* lw = h->at<float>(h->lwi ? h->lay.lw1 : h->lay.lw0);
+    Pass1Args a;
+    fill_pass1(h, a, y_host, y_dev);
+    a.x_in = h->X(src);
+    a.x_out = h->X(mid);  // x_n in natural order
+    a.lw_out = lw;
+    a.carry_mode = h->carry_mode;
+    a.carry_lw = h->at<float>(h->lwi ? h->lay.lw0 : h->lay.lw1);
+    a.carry_lv = h->at<double>(h->lay.carry_lv);
+    a.carry_shift = h->carry_shift;
+    a.carry_c = h->carry_c;
+    a.ess_part = h->at<double>(h->lay.ess_part);
+    a.ess_lmax = h->at<unsigned int>(h->lay.ess_lmax);
+    h->mark(PF_KERNEL_PASS1, true);
+    launch_pass1(h, a, kPass1Weigh);
+    h->mark(PF_KERNEL_PASS1, false);
+    int launches = 1;
+    h->mark(PF_KERNEL_CASCADE, true);
+    launch_cascade_k(h);
+    EssArgs e;
+    e.ess_part = h->at<double>(h->lay.ess_part);
+    e.logV = h->at<double>(h->lay.logV);
+    e.lmax = h->at<unsigned int>(h->lay.ess_lmax);
+    e.chunks = h->at<double>(h->lay.ess_chunks);
+    e.out = h->at<double>(h->lay.ess_out);
+    e.N = h->N;
+    e.NT = p.NT;
+    e.m = h->m;
+    e.S = h->S;
+    e.theta = h->theta;
+    launch_ess(LaunchCfg{0u, 0u, 0u, h->stream}, e);
+    h->mark(PF_KERNEL_CASCADE, false);
+    launches += 3;
+    double tail[2];
+    cudaError_t ce = cudaMemcpyAsync(tail, e.out + h->S + 1, sizeof(tail), cudaMemcpyDeviceToHost, h->stream);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(h->stream);
+    if (ce != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_step (adaptive): ") + cudaGetErrorString(ce));
+    const uint32_t ss = (uint32_t)tail[0];
+    const double lvS = tail[1];
+
+    int xs = mid;  // buffer holding the current states
+    if (ss >= 1u) {
+        Pass1Args r;
+        fill_pass1(h, r, y_host, y_dev);
+        r.do_mutate = 0;
+        r.x_in = h->X(mid);
+        r.x_out = h->X(mid ^ 1);
+        r.lw_in = lw;
+        r.k1 = std::min(p.k1, ss);
+        h->mark(PF_KERNEL_PASS1, true);
+        launch_pass1(h, r, kPass1Resample);
+        h->mark(PF_KERNEL_PASS1, false);
+        ++launches;
+        xs = mid ^ 1;
+        for (const StagePass& sp : p.passes) {
+            if (sp.s0 > ss) break;
+            const StagePass q = stage_pass_for(h, sp, std::min(sp.k, ss - sp.s0 + 1u));
+            h->mark(PF_KERNEL_STAGES, true);
+            launch_stages_k(h, q, h->X(xs), h->X(xs ^ 1));
+            h->mark(PF_KERNEL_STAGES, false);
+            xs ^= 1;
+            ++launches;
+        }
+    }
+    // weights carried into the next step (R18)
+    if (ss == 0u) {
+        h->carry_mode = 1;  // lw of this step, in buffer lwi (the next weigh pass writes the other)
+        h->lwi ^= 1;
+    } else if (ss < h->S) {
+        h->carry_mode = 2;
+        h->carry_shift = ss;
+        cudaMemcpyAsync(h->at<double>(h->lay.carry_lv), h->at<double>(h->lay.logV) + level_offset(h->m, (int)ss),
+                        (size_t)(h->m >> ss) * 8, cudaMemcpyDeviceToDevice, h->stream);
+    } else {
+        h->carry_mode = 0;
+    }
+    h->carry_c = lvS;
+    h->sstar_last = (int)ss;
+    h->cur = xs;
+    h->step_n = h->n;
+    h->n += 1;
+    h->have_step = true;
+    h->top_done = true;
+    h->last_launches = launches;
+    return check_cuda(h, "pf_step");
+}
+
+static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
+    if (h->theta > 0.0) return run_step_adaptive(h, y_host, y_dev);
+    const Plan& p = h->plan;
+    Pass1Args a;
+    fill_pass1(h, a, y_host, y_dev);
+    const int src = h->cur, dst = h->cur ^ 1;
+    a.x_in = h->X(src);
+    a.x_out = h->X(dst);
     h->mark(PF_KERNEL_PASS1, true);
     launch_pass1(h, a);
     h->mark(PF_KERNEL_PASS1, false);
@@ -513,6 +663,7 @@ static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
         ++launches;
     }
     h->cur = xs;
+    h->sstar_last = (int)h->S;
     h->step_n = h->n;
     h->n += 1;
     h->have_step = h->world == 1;
@@ -559,6 +710,7 @@ static int init_core(const pf_model* model, uint64_t N, uint32_t M, uint64_t see
     if (!validate_model(model, &err)) return fail(nullptr, PF_EINVAL, err);
     if (!validate_topology(N, M, &err)) return fail(nullptr, PF_EINVAL, err);
     if (!shard_geometry(N, M, rank, world, &Nloc, &err)) return fail(nullptr, PF_EINVAL, err);
+    if ((flags & PF_FLAG_ADAPTIVE) && world != 1) return fail(nullptr, PF_EINVAL, "PF_FLAG_ADAPTIVE needs world = 1");
     Plan p;
     int nsm = 148, dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
@@ -807,13 +959,18 @@ int pf_debug_ptr(pf_handle* h, int what, int stage, void** dev_out) {
         case PF_DBG_ANC_FINAL: {
             if (h->world > 1) return fail(h, PF_ESTATE, "composed ancestors span shards: use the stage tables");
             int32_t* A = h->at<int32_t>(h->lay.dbg_A);
-            launch_debug_compose(LaunchCfg{1024u, 256u, 0u, h->stream}, h->at<int32_t>(h->lay.dbg_anc), h->N, h->S, A);
+            const uint32_t sc = h->sstar_last >= 0 ? (uint32_t)h->sstar_last : h->S;  // stages run
+            launch_debug_compose(LaunchCfg{1024u, 256u, 0u, h->stream}, h->at<int32_t>(h->lay.dbg_anc), h->N, sc, A);
             *dev_out = A;
             return check_cuda(h, "pf_debug_ptr");
         }
         case PF_DBG_XHAT: *dev_out = h->X(h->cur); return PF_OK;
         case PF_DBG_LOGV: *dev_out = h->at<double>(h->lay.logV); return PF_OK;
         case PF_DBG_THRESH: *dev_out = h->at<uint32_t>(h->lay.thr); return PF_OK;
+        case PF_DBG_ESS:
+            if (!(h->flags & PF_FLAG_ADAPTIVE)) return fail(h, PF_ESTATE, "handle not created with PF_FLAG_ADAPTIVE");
+            *dev_out = h->at<double>(h->lay.ess_out);
+            return PF_OK;
     }
     return fail(h, PF_EINVAL, "unknown debug table");
 }
@@ -832,6 +989,7 @@ int pf_debug_get(pf_handle* h, int what, int stage, void* host_out, size_t bytes
         case PF_DBG_ANC_FINAL: need = (size_t)h->N * 4; break;
         case PF_DBG_LOGV: need = (size_t)(h->m - 1) * 8; break;
         case PF_DBG_THRESH: need = (size_t)(h->m - 1) * 4; break;
+        case PF_DBG_ESS: need = (size_t)(h->S + 1) * 8; break;
     }
     if (!host_out || bytes < need) return fail(h, PF_EINVAL, "host buffer too small");
     cudaError_t e = cudaMemcpyAsync(host_out, p, need, cudaMemcpyDeviceToHost, h->stream);
@@ -847,7 +1005,21 @@ int pf_debug_set_state(pf_handle* h, const float* host_xhat, uint32_t n) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_debug_set_state: ") + cudaGetErrorString(e));
     h->n = n;
+    h->carry_mode = 0;  // the given state is unweighted
     return PF_OK;
 }
+
+int pf_set_adaptive(pf_handle* h, double theta) {
+    if (!h) return fail(h, PF_EINVAL, "NULL handle");
+    if (!(theta >= 0.0 && theta <= 1.0)) return fail(h, PF_EINVAL, "theta must lie in [0, 1]");
+    if (theta > 0.0 && !(h->flags & PF_FLAG_ADAPTIVE))
+        return fail(h, PF_EINVAL, "handle not created with PF_FLAG_ADAPTIVE");
+    if (theta > 0.0 && h->world != 1) return fail(h, PF_EINVAL, "the fully adapted scheme needs world = 1");
+    h->theta = theta;
+    if (theta == 0.0) h->carry_mode = 0;
+    return PF_OK;
+}
+
+int pf_last_stages(const pf_handle* h) { return h ? h->sstar_last : -1; }
 
 }  // extern "C"

@@ -3,6 +3,82 @@
 
 namespace pfk {
 
+// The ESS kernels (declarations and EssArgs in pf_kernels.cuh) live in this unit only.
+__device__ __forceinline__ float float_from_order_bits(unsigned int u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+__global__ void __launch_bounds__(kEssThreads) k_ess_chunks(const __grid_constant__ EssArgs a) {
+    __shared__ double r1[kEssThreads], r2[kEssThreads];
+    uint32_t c = blockIdx.x, s = 0, nc;
+    for (;; ++s) {  // which level, which chunk of it
+        nc = (ess_level_count(a, s) + kEssChunk - 1) / kEssChunk;
+        if (c < nc) break;
+        c -= nc;
+    }
+    const double L = (double)float_from_order_bits(*a.lmax);
+    const uint32_t n = ess_level_count(a, s), j0 = c * kEssChunk, j1 = min(n, j0 + kEssChunk);
+    double s1 = 0.0, s2 = 0.0;
+    if (L != -CUDART_INF) {
+        for (uint32_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+            if (s == 0) {
+                const double* t = a.ess_part + (uint64_t)j * 3;
+                if (t[0] == -CUDART_INF) continue;
+                const double f = exp(t[0] - L);
+                s1 += t[1] * f;
+                s2 += t[2] * f * f;
+            } else {
+                const double f = exp(a.logV[level_offset(a.m, (int)s) + j] - L);
+                s1 += f;
+                s2 += f * f;
+            }
+        }
+    }
+    r1[threadIdx.x] = s1;
+    r2[threadIdx.x] = s2;
+    __syncthreads();
+    for (uint32_t h = blockDim.x / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h) {
+            r1[threadIdx.x] += r1[threadIdx.x + h];
+            r2[threadIdx.x] += r2[threadIdx.x + h];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        a.chunks[2 * blockIdx.x] = r1[0];
+        a.chunks[2 * blockIdx.x + 1] = r2[0];
+    }
+}
+
+__global__ void k_ess_final(const __grid_constant__ EssArgs a) {
+    const uint32_t s = threadIdx.x;
+    if (s <= a.S) {
+        uint32_t c0 = 0;
+        for (uint32_t t = 0; t < s; ++t) c0 += (ess_level_count(a, t) + kEssChunk - 1) / kEssChunk;
+        const uint32_t nc = (ess_level_count(a, s) + kEssChunk - 1) / kEssChunk;
+        double s1 = 0.0, s2 = 0.0;
+        for (uint32_t c = 0; c < nc; ++c) {
+            s1 += a.chunks[2 * (c0 + c)];
+            s2 += a.chunks[2 * (c0 + c) + 1];
+        }
+        const double units = s == 0 ? (double)a.N : (double)(a.m >> s);
+        a.out[s] = (s2 > 0.0) ? s1 * s1 / (units * s2) : 1.0;  // no weight at all: equal
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t ss = a.S;
+        for (uint32_t t = 0; t < a.S; ++t)
+            if (a.out[t] >= a.theta) {
+                ss = t;
+                break;
+            }
+        a.out[a.S + 1] = (double)ss;
+        a.out[a.S + 2] = a.logV[level_offset(a.m, (int)a.S)];
+        *a.lmax = 0u;
+    }
+}
+
+
 void launch_cascade(int D, const LaunchCfg& c, const CascadeArgs& a) {
     switch (D) {
         case 1: k_cascade<1><<<c.grid, c.threads, 0, c.stream>>>(a); break;
@@ -10,6 +86,11 @@ void launch_cascade(int D, const LaunchCfg& c, const CascadeArgs& a) {
         case 4: k_cascade<4><<<c.grid, c.threads, 0, c.stream>>>(a); break;
         default: k_cascade<8><<<c.grid, c.threads, 0, c.stream>>>(a); break;
     }
+}
+
+void launch_ess(const LaunchCfg& chunks, const EssArgs& a) {
+    k_ess_chunks<<<ess_chunks_total(a), kEssThreads, 0, chunks.stream>>>(a);
+    k_ess_final<<<1, ((a.S + 1 + 31) / 32) * 32, 0, chunks.stream>>>(a);
 }
 
 void launch_init(int D, int kind, const LaunchCfg& c, const InitArgs& a) {

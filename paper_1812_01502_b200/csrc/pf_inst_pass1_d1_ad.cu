@@ -1,0 +1,6 @@
+// k_pass1 instantiations for d = 1, fully adapted modes (body: pf_inst_pass1.inc).
+#define PASS1_D 1
+#define PASS1_SV 1
+#define PASS1_ADAPTIVE 1
+#define PASS1_LAUNCHER launch_pass1_ad_d1
+#include "pf_inst_pass1.inc"

@@ -1,5 +1,6 @@
-// k_pass1 instantiations for d = 8 (body: pf_inst_pass1.inc).
+// k_pass1 instantiations for d = 8, fused mode (body: pf_inst_pass1.inc).
 #define PASS1_D 8
 #define PASS1_SV 0
+#define PASS1_ADAPTIVE 0
 #define PASS1_LAUNCHER launch_pass1_d8
 #include "pf_inst_pass1.inc"

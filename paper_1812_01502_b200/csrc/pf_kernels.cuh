@@ -239,6 +239,38 @@ __global__ void __launch_bounds__(kCascadeThreads) k_cascade(const __grid_consta
 }
 
 // -------------------------------------------------------------------------------------
+// Fully adapted scheme (R17): the ESS of the stage weights V_0 = w, V_1, ..., V_S
+// and the number of stages to run, S* = min{s : E_s >= theta}.
+//   k_ess_chunks  one CTA per chunk of kEssChunk entries of one level: level 0 = the tile
+//                 partials {max, sum w, sum w^2} of k_pass1 (kPass1Weigh), level s >= 1 =
+//                 the m / 2^s values of the V table; sums of e^{v - L}, e^{2(v - L)} with L
+//                 the global max of lw (V_s <= max w, so no term overflows); fixed order
+//   k_ess_final   one thread per level sums its chunks in order -> E_s; thread 0 -> S*,
+//                 log V_S; resets the running max for the next step
+constexpr uint32_t kEssChunk = 4096;
+constexpr int kEssThreads = 256;
+
+struct EssArgs {
+    const double* ess_part;  // NT x 3
+    const double* logV;      // level table (m - 1)
+    unsigned int* lmax;      // running max of lw (float_order_bits), reset by k_ess_final
+    double* chunks;          // 2 per chunk
+    double* out;             // E_0..E_S, S*, log V_S
+    uint64_t N;
+    uint32_t NT, m, S;
+    double theta;
+};
+
+__host__ __device__ inline uint32_t ess_level_count(const EssArgs& a, uint32_t s) {
+    return s == 0 ? a.NT : (a.m >> s);
+}
+__host__ __device__ inline uint32_t ess_chunks_total(const EssArgs& a) {
+    uint32_t t = 0;
+    for (uint32_t s = 0; s <= a.S; ++s) t += (ess_level_count(a, s) + kEssChunk - 1) / kEssChunk;
+    return t;
+}
+
+// -------------------------------------------------------------------------------------
 template <typename T>
 struct __align__(4 * sizeof(T) <= 16 ? 4 * sizeof(T) : 16) Vec4 {
     T v[4];

@@ -21,10 +21,14 @@ struct __align__(16) State8 {
     float4 a, b;
 };
 
-void launch_pass1_d1(int kind, int tb, bool dbg, int qpt, const LaunchCfg& c, const Pass1Args& a);
-void launch_pass1_d2(int kind, int tb, bool dbg, int qpt, const LaunchCfg& c, const Pass1Args& a);
-void launch_pass1_d4(int kind, int tb, bool dbg, int qpt, const LaunchCfg& c, const Pass1Args& a);
-void launch_pass1_d8(int kind, int tb, bool dbg, int qpt, const LaunchCfg& c, const Pass1Args& a);
+void launch_pass1_d1(int kind, int tb, bool dbg, int qpt, int mode, const LaunchCfg& c, const Pass1Args& a);
+void launch_pass1_d2(int kind, int tb, bool dbg, int qpt, int mode, const LaunchCfg& c, const Pass1Args& a);
+void launch_pass1_d4(int kind, int tb, bool dbg, int qpt, int mode, const LaunchCfg& c, const Pass1Args& a);
+void launch_pass1_d8(int kind, int tb, bool dbg, int qpt, int mode, const LaunchCfg& c, const Pass1Args& a);
+void launch_pass1_ad_d1(int kind, int tb, bool dbg, int qpt, int mode, const LaunchCfg& c, const Pass1Args& a);
+void launch_pass1_ad_d2(int kind, int tb, bool dbg, int qpt, int mode, const LaunchCfg& c, const Pass1Args& a);
+void launch_pass1_ad_d4(int kind, int tb, bool dbg, int qpt, int mode, const LaunchCfg& c, const Pass1Args& a);
+void launch_pass1_ad_d8(int kind, int tb, bool dbg, int qpt, int mode, const LaunchCfg& c, const Pass1Args& a);
 void launch_stages_f1(int tb, bool dbg, int qpt, const LaunchCfg& c, const StageArgs& a);
 void launch_stages_f2(int tb, bool dbg, int qpt, const LaunchCfg& c, const StageArgs& a);
 void launch_stages_f4(int tb, bool dbg, int qpt, const LaunchCfg& c, const StageArgs& a);
@@ -38,6 +42,7 @@ inline void launch_stages(int D, int tb, bool dbg, int qpt, const LaunchCfg& c, 
     }
 }
 void launch_cascade(int D, const LaunchCfg& c, const CascadeArgs& a);
+void launch_ess(const LaunchCfg& chunks, const EssArgs& a);
 void launch_init(int D, int kind, const LaunchCfg& c, const InitArgs& a);
 void launch_top(int D, const LaunchCfg& c, const TopArgs& a);
 void launch_cross(int payload, bool dbg, const LaunchCfg& c, const CrossArgs& a);

@@ -20,6 +20,7 @@
 // position of the source.
 #pragma once
 #include <cstdint>
+#include <cstring>
 
 #include "pf_device.cuh"
 
@@ -29,7 +30,7 @@ constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kPass1MaxGroups = 64;  // T1 <= 64: the V tree of a tile fits one warp's lanes
 
 struct Pass1Smem {
-    uint32_t xs, w, L1, tab, chunk, lv1, red, total;
+    uint32_t xs, w, L1, tab, chunk, lv1, red, ess, total;
 };
 __host__ __device__ inline Pass1Smem pass1_smem(int D, uint32_t P1, uint32_t M, uint32_t k1, uint32_t threads,
                                                 uint32_t tb) {
@@ -48,6 +49,7 @@ __host__ __device__ inline Pass1Smem pass1_smem(int D, uint32_t P1, uint32_t M, 
     s.chunk = take(M > 64 ? (P1 / 128u) * 4u : 0u);  // per-warp-chunk maxima / totals
     s.lv1 = take((T1 / 2) * 8u);
     s.red = take((threads / 32u) * (2u + 4u * (uint32_t)D) * 4u);
+    s.ess = take((threads / 32u) * 4u);  // per-warp sum of squared weights (kPass1Weigh)
     s.total = off;
     return s;
 }
@@ -71,7 +73,37 @@ struct Pass1Args {
     float* dbg_x;
     float* dbg_lw;
     int32_t* dbg_anc;
+    // fully adapted scheme (R17/R18; modes below)
+    float* lw_out;          // kPass1Weigh: log-weights lw = carry + log g (N fp32)
+    const float* lw_in;     // kPass1Resample: the same log-weights, read back
+    int carry_mode;         // 0 none, 1 particle carry lw_prev[i] - c, 2 block carry lvl[g >> shift] - c
+    const float* carry_lw;  // previous step's lw (carry_mode 1)
+    const double* carry_lv; // previous step's level-S* values (carry_mode 2)
+    uint32_t carry_shift;   // S* of the previous step (carry_mode 2)
+    double carry_c;         // log V_S of the previous step
+    double* ess_part;       // kPass1Weigh: per tile {max lw, sum e^{lw-max}, sum e^{2(lw-max)}}
+    unsigned int* ess_lmax; // kPass1Weigh: running max of lw (order-preserving float bits)
 };
+
+// Order-preserving map of float bits to unsigned (atomicMax of floats).
+__host__ __device__ inline unsigned int float_order_bits(float f) {
+#ifdef __CUDA_ARCH__
+    const unsigned int u = __float_as_uint(f);
+#else
+    unsigned int u;
+    memcpy(&u, &f, 4);
+#endif
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// k_pass1 modes: the fused step (mutate, weight, stages 1..k1, tile written moved) or the
+// two halves of a fully adapted step, which must know every ESS before its first draw:
+//   kPass1Weigh    mutate, weight (+ carried weight), V levels 1..k1 and thresholds,
+//                  estimate and ESS partials; writes x_n (natural order) and lw
+//   kPass1Resample stage 1 and stages 2..k1 from x_n and lw (no mutation, no weighting)
+constexpr int kPass1Fused = 0;
+constexpr int kPass1Weigh = 1;
+constexpr int kPass1Resample = 2;
 
 // Sum of NV = 2^v values over the 32 lanes of a warp by recursive halving: after the
 // call, lane l holds the total of value (l >> (5 - v)) in v[0].
@@ -96,7 +128,7 @@ __device__ __forceinline__ float warp_sum_transpose(float* v, uint32_t lane) {
     return v[0];
 }
 
-template <int D, int KIND, bool DBG, int QPT, int TB>
+template <int D, int KIND, bool DBG, int QPT, int TB, int MODE = kPass1Fused>
 __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args a) {
     constexpr int PS = 2 + 4 * D;  // partial: max, sw, s1[D], s2[D], p1[D], p2[D]
     extern __shared__ __align__(16) unsigned char smem[];
@@ -109,6 +141,7 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
     float* chunk = reinterpret_cast<float*>(smem + SL.chunk);
     double* lv1 = reinterpret_cast<double*>(smem + SL.lv1);
     float* red = reinterpret_cast<float*>(smem + SL.red);
+    float* essw = reinterpret_cast<float*>(smem + SL.ess);
 
     const uint32_t P1 = a.P1, M = a.M, b = a.b, nq = P1 >> 2, k1 = a.k1;
     const uint32_t T1 = a.T1;  // groups per tile (<= 64)
@@ -165,8 +198,42 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
 #pragma unroll
             for (int k = 0; k < 4 * D; ++k) x[k] = xh[it][k];
         }
+        if constexpr (MODE == kPass1Resample) {
+            const float4 t = valid ? __ldg(reinterpret_cast<const float4*>(a.lw_in + i0))
+                                   : make_float4(-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F);
+            lw[it][0] = t.x;
+            lw[it][1] = t.y;
+            lw[it][2] = t.z;
+            lw[it][3] = t.w;
+        } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) lw[it][e] = valid ? log_potential<D, KIND>(a.mp, y, x + e * D) : -CUDART_INF_F;
+            for (int e = 0; e < 4; ++e) lw[it][e] = valid ? log_potential<D, KIND>(a.mp, y, x + e * D) : -CUDART_INF_F;
+        }
+        if constexpr (MODE == kPass1Weigh) {  // carried weight of the previous step (R18)
+            if (valid && a.carry_mode != 0) {
+                float cw[4];
+                if (a.carry_mode == 1) {
+                    const float4 t = __ldg(reinterpret_cast<const float4*>(a.carry_lw + i0));
+                    cw[0] = (float)((double)t.x - a.carry_c);
+                    cw[1] = (float)((double)t.y - a.carry_c);
+                    cw[2] = (float)((double)t.z - a.carry_c);
+                    cw[3] = (float)((double)t.w - a.carry_c);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        cw[e] = (float)(__ldg(a.carry_lv + ((((uint64_t)a.pos0 + i0 + e) >> b) >> a.carry_shift)) - a.carry_c);
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) lw[it][e] += cw[e];
+            }
+            if (valid) {
+                reinterpret_cast<float4*>(a.lw_out + i0)[0] = make_float4(lw[it][0], lw[it][1], lw[it][2], lw[it][3]);
+#pragma unroll
+                for (int c = 0; c < D; ++c)
+                    reinterpret_cast<float4*>(a.x_out + (uint64_t)i0 * D)[c] =
+                        make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+            }
+        }
         if constexpr (KEEPX) {
 #pragma unroll
             for (int k = 0; k < 4 * D; ++k) xr[it][k] = valid ? x[k] : 0.0f;
@@ -214,7 +281,7 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
 #pragma unroll
     for (int it = 0; it < QPT; ++it)
         if (tid + it * threads < nq) mthr = fmaxf(mthr, pm[it]);
-    float acc[PS];
+    float acc[PS], accsq = 0.0f;
 #pragma unroll
     for (int k = 0; k < PS; ++k) acc[k] = 0.0f;
     float run[QPT][4], incl[QPT];
@@ -232,6 +299,7 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
             run[it][e] = r;
             const float wf = c * f;
             acc[1] += wf;
+            if constexpr (MODE == kPass1Weigh) accsq = fmaf(wf, wf, accsq);
 #pragma unroll
             for (int k = 0; k < D; ++k) {
                 float xv;
@@ -297,7 +365,7 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
     }
     if (Z <= 32u) __syncwarp();  // a pair's CDF was written by this warp
     else __syncthreads();
-    {   // all QPT x 4 branch-free binary searches advance together (independent smem loads)
+    if constexpr (MODE != kPass1Weigh) {  // all QPT x 4 branch-free binary searches advance together
         uint32_t lo[QPT][4];
         float tq[QPT][4];
 #pragma unroll
@@ -356,6 +424,11 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
             red[warp * PS] = wmax;
             red[warp * PS + 1] = sw;
         }
+        if constexpr (MODE == kPass1Weigh) {
+            float sq = accsq * f * f;
+            for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(kFull, sq, o);
+            if (lane == 0) essw[warp] = sq;
+        }
     }
     __syncthreads();  // B: L1, lv1, red complete
 
@@ -388,6 +461,7 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
         }
     }
 
+    if constexpr (MODE != kPass1Weigh) {  // sections 5-6: the draws and the walk
     // ---- 5. stages 2..k1: every draw depends only on its word and the threshold ---------
     const uint32_t mask = M - 1u;
 #pragma unroll
@@ -477,6 +551,7 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
             reinterpret_cast<float4*>(a.x_out + (uint64_t)(base + 4u * q) * D)[c] =
                 make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
     }
+    }
 
     // ---- 7. warp 0: the tile's estimate partial (off the critical path) ----------------
     if (warp == 0) {
@@ -495,6 +570,21 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
                 }
             }
             a.part[(uint64_t)tile * PS + k] = v;
+        }
+        if constexpr (MODE == kPass1Weigh) {  // ESS partial {max, sum w, sum w^2} (R17)
+            if (lane == 0) {
+                double sw = 0.0, sq = 0.0;
+                for (uint32_t wv = 0; wv < nwarps; ++wv) {
+                    const float wm = red[wv * PS];
+                    const double f = (wm == -CUDART_INF_F) ? 0.0 : exp((double)wm - (double)tmax);
+                    sw += (double)red[wv * PS + 1] * f;
+                    sq += (double)essw[wv] * f * f;
+                }
+                a.ess_part[(uint64_t)tile * 3] = (double)tmax;
+                a.ess_part[(uint64_t)tile * 3 + 1] = sw;
+                a.ess_part[(uint64_t)tile * 3 + 2] = sq;
+                atomicMax(a.ess_lmax, float_order_bits(tmax));
+            }
         }
     }
 }
