@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--theta", type=float, default=0.0,
+                    help="ESS threshold of the fully adapted scheme (0: plain augmented resampling)")
     return ap.parse_args()
 
 
@@ -187,6 +189,8 @@ def ncu_traffic(cfg, kernel):
 
 
 def run_ours(args):
+    if args.theta > 0 and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        raise SystemExit("--theta (fully adapted scheme) runs on one GPU only")
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -209,7 +213,7 @@ def run_ours(args):
     with torch.cuda.stream(stream):
         y_dev = torch.tensor(np.asarray(ys, np.float32), device=dev)
         if world == 1:
-            f = pf.ParticleFilter(params, cfg.N, cfg.M, args.seed, stream=stream)
+            f = pf.ParticleFilter(params, cfg.N, cfg.M, args.seed, stream=stream, theta=args.theta)
 
             def step(k, yd=None):
                 f.step_dev(y_dev[k % T] if yd is None else yd)
@@ -238,9 +242,12 @@ def run_ours(args):
         clocks.start()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        stages = []
         e0.record(stream)
         for k in range(args.steps):
             step(args.warmup + k)
+            if args.theta > 0:
+                stages.append(f.last_stages())  # the adaptive step has synchronised already
         e1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -301,7 +308,10 @@ def run_ours(args):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": config_dict(cfg, world, "single" if world == 1 else f"groups sharded over {world} GPUs"),
+                "config": dict(config_dict(cfg, world, "single" if world == 1 else f"groups sharded over {world} GPUs"),
+                               **({"theta": args.theta, "stages_run_mean": float(np.mean(stages)),
+                                   "stages_run_hist": np.bincount(stages, minlength=cfg.S + 1).tolist()}
+                                  if args.theta > 0 else {})),
                 "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line))
