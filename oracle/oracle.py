@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "pf_oracle.c")
 _LIB = os.path.join(_HERE, "libpforacle.so")
 
-INIT, MUTATE, RESAMPLE = 1, 2, 3
+INIT, MUTATE, RESAMPLE, WITHIN, ISLAND = 1, 2, 3, 4, 5
 
 
 def build(force: bool = False) -> str:
@@ -59,6 +59,10 @@ def lib():
         _lib.orc_ess_levels.argtypes = [u64, u64, vp, vp, vp]
         _lib.orc_stages_to_run.argtypes = [ctypes.c_int, vp, ctypes.c_double]
         _lib.orc_stages_to_run.restype = ctypes.c_int
+        _lib.orc_within_island.argtypes = [u64, u64, u64, u32, vp, vp, vp, vp]
+        _lib.orc_island_resample.argtypes = [u64, u64, u32, vp, ctypes.c_int, vp, vp, vp, vp]
+        _lib.orc_step_airpf.argtypes = [vp, u64, u64, u64, u32, vp, vp, ctypes.c_int, vp, vp, vp, vp, vp, vp,
+                                        vp, vp, vp, vp, vp]
         _lib.orc_step_adaptive.argtypes = [vp, u64, u64, u64, u32, vp, vp, vp, ctypes.c_double, vp, vp, vp, vp,
                                            vp, vp, vp, vp, vp, vp, vp, vp]
     return _lib
@@ -287,3 +291,68 @@ def run_filter_adaptive(params: dict, M: int, m: int, seed: int, ys: np.ndarray,
         x = r["xhat"].astype(np.float32)
         lwc = r["lwc"]
     return means, stages
+
+
+# ----------------------------------------------------------------------------- AIRPF
+def within_island(lw: np.ndarray, M: int, seed: int, n: int) -> dict:
+    """Alg. 5: within-island multinomial draws a_w (N), deltas, log island means (m)."""
+    lw = np.ascontiguousarray(lw, dtype=np.float64)
+    N = lw.shape[0]
+    a_w = np.zeros(N, np.int64)
+    delta = np.zeros(N, np.float32)
+    logW = np.zeros(N // M)
+    rc = lib().orc_within_island(N, M, seed, n, _ptr(lw), _ptr(a_w), _ptr(delta), _ptr(logW))
+    if rc != 0:
+        raise ValueError(f"orc_within_island rc={rc}")
+    return dict(a_w=a_w, delta=delta, logW=logW)
+
+
+def island_resample(logW: np.ndarray, seed: int, n: int, modified: bool = True) -> dict:
+    """Alg. 6 / Alg. 7 over m island log-weights: src (S, m), deltas, levels, Aisl (m)."""
+    lw = np.ascontiguousarray(logW, dtype=np.float64)
+    m = lw.shape[0]
+    S = int(round(np.log2(m)))
+    src = np.zeros((S, m), np.int32)
+    delta = np.zeros((S, m), np.float32)
+    lv = np.zeros(m - 1)
+    A = np.zeros(m, np.int64)
+    rc = lib().orc_island_resample(m, seed, n, _ptr(lw), int(bool(modified)), _ptr(src), _ptr(delta), _ptr(lv),
+                                   _ptr(A))
+    if rc != 0:
+        raise ValueError(f"orc_island_resample rc={rc}")
+    return dict(src=src, delta=delta, logVbar=lv, Aisl=A, S=S)
+
+
+def step_airpf(params: dict, N: int, M: int, seed: int, n: int, y: np.ndarray, xin: np.ndarray,
+               modified: bool = True) -> dict:
+    mdl = make_model(params)
+    d = mdl.d
+    m = N // M
+    S = int(round(np.log2(m)))
+    xin = np.ascontiguousarray(xin, dtype=np.float32).reshape(N, d)
+    yy = np.ascontiguousarray(y, dtype=np.float32)
+    out = dict(x=np.zeros((N, d)), lw=np.zeros(N), a_w=np.zeros(N, np.int64), wdelta=np.zeros(N, np.float32),
+               logW=np.zeros(m), src=np.zeros((S, m), np.int32), idelta=np.zeros((S, m), np.float32),
+               logVbar=np.zeros(m - 1), Aisl=np.zeros(m, np.int64), xhat=np.zeros((N, d)),
+               filter=np.zeros(2 * d), predict=np.zeros(2 * d))
+    rc = lib().orc_step_airpf(ctypes.byref(mdl), N, M, seed, n, _ptr(yy), _ptr(xin), int(bool(modified)),
+                              _ptr(out["x"]), _ptr(out["lw"]), _ptr(out["a_w"]), _ptr(out["wdelta"]),
+                              _ptr(out["logW"]), _ptr(out["src"]), _ptr(out["idelta"]), _ptr(out["logVbar"]),
+                              _ptr(out["Aisl"]), _ptr(out["xhat"]), _ptr(out["filter"]), _ptr(out["predict"]))
+    if rc != 0:
+        raise ValueError(f"orc_step_airpf rc={rc}")
+    out["S"], out["m"] = S, m
+    return out
+
+
+def run_filter_airpf(params: dict, M: int, m: int, seed: int, ys: np.ndarray, modified: bool = True,
+                     x0: Optional[np.ndarray] = None):
+    N = M * m
+    d = int(params["d"])
+    x = (init(params, N, seed) if x0 is None else x0).astype(np.float32)
+    means = np.zeros((len(ys), d))
+    for n, y in enumerate(ys):
+        r = step_airpf(params, N, M, seed, n, y, x, modified)
+        means[n] = r["filter"][:d]
+        x = r["xhat"].astype(np.float32)
+    return means

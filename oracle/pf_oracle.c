@@ -37,6 +37,8 @@
 #define ORC_DOMAIN_INIT 1u
 #define ORC_DOMAIN_MUTATE 2u
 #define ORC_DOMAIN_RESAMPLE 3u
+#define ORC_DOMAIN_WITHIN 4u /* AIRPF within-island draws (reading R19) */
+#define ORC_DOMAIN_ISLAND 5u /* AIRPF island side draws (reading R20) */
 
 /* ------------------------------------------------------------------------- */
 /* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11, "Parallel random numbers:
@@ -594,4 +596,149 @@ int orc_step_adaptive(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t see
     }
     free(xprev); free(Aloc); free(lvl);
     return rc;
+}
+
+/* ------------------------------------------------------------------------- */
+/* AIRPF: the augmented island resampling particle filter (Alg. 4)
+ * with the within-island resample (Alg. 5) and the augmented
+ * island resampling (Alg. 6) or its modified form (Alg. 7,
+ * PAPER.md:1137-1160).  Draw contract: DESIGN.md readings R19-R21. */
+
+/* Alg. 5: every output i of island k (particles kM..kM+M-1) draws its source from the
+ * island's M particles with probability g_j / sum_island g (the rows of A = I_m (x)
+ * 1_{1/M} restricted to the island); W_out = the island mean of g (eq. out weight,
+ * PAPER.md:918-922), returned as logW[k].  Inverse CDF with the island's particles in
+ * ascending order, u = (r >> 8) 2^-24 from word (i & 3) of block (i >> 2, n,
+ * WITHIN << 24), a_w(i) = kM + #{c < M-1 : C_c <= u C_{M-1}}; delta as for stage 1. */
+int orc_within_island(uint64_t N, uint64_t M, uint64_t seed, uint32_t n, const double* lw,
+                      int64_t* a_w, float* delta, double* logW)
+{
+    if (M == 0 || N % M != 0) return ORC_EINVAL;
+    uint64_t m = N / M;
+    double* C = (double*)malloc(sizeof(double) * M);
+    if (!C) return ORC_ENOMEM;
+    for (uint64_t k = 0; k < m; ++k) {
+        uint64_t base = k * M;
+        double mx = -INFINITY;
+        for (uint64_t j = 0; j < M; ++j)
+            if (lw[base + j] > mx) mx = lw[base + j];
+        double acc = 0.0;
+        for (uint64_t j = 0; j < M; ++j) {
+            acc += (mx == -INFINITY) ? 1.0 : exp(lw[base + j] - mx);
+            C[j] = acc;
+        }
+        logW[k] = (mx == -INFINITY) ? -INFINITY : mx + log(C[M - 1]) - log((double)M);
+        for (uint64_t j = 0; j < M; ++j) {
+            uint64_t i = base + j;
+            double u = u01(rng_word(seed, (uint32_t)(i >> 2), n, ORC_DOMAIN_WITHIN, 0u, (int)(i & 3u)));
+            double t = u * C[M - 1];
+            uint64_t c = 0;
+            for (uint64_t kk = 0; kk + 1 < M; ++kk)
+                if (C[kk] <= t) ++c;
+            a_w[i] = (int64_t)(base + c);
+            if (delta) {
+                double dmin = INFINITY;
+                for (uint64_t kk = 0; kk + 1 < M; ++kk) {
+                    double dd = fabs(u - C[kk] / C[M - 1]);
+                    if (dd < dmin) dmin = dd;
+                }
+                delta[i] = (float)dmin;
+            }
+        }
+    }
+    free(C);
+    return ORC_OK;
+}
+
+/* Alg. 6 (modified = 0) / Alg. 7 (modified = 1) on the island log-weights logW (m):
+ *   V_bar_0 = W, V_bar_s = A_bar_s V_bar_{s-1} (pair means; stored in logVbar with the
+ *   level layout of orc_augmented_resample, levels 1..S);
+ *   at stage s island i draws its whole block from island j in {i, i ^ 2^{s-1}} with
+ *   probability V_bar_{s-1}^j / (V_bar_{s-1}^L + V_bar_{s-1}^R) (line 'sampling aug
+ *   island'): word (i & 3) of block (i >> 2, n, ISLAND << 24 | s), side L iff
+ *   (r >> 1) < floor(p 2^31), p = V_L / (V_L + V_R) (reading R20);
+ *   Alg. 7: a pure exchange of a pair (L took R's block and R took L's) is undone
+ *   (lines 'loop'/'exchange'; reading R21).
+ * src[(s-1) m + i] = the island whose stage-(s-1) block island i holds after stage s;
+ * delta as for stage s >= 2; Aisl[i] = src_1(src_2(...src_S(i))). */
+int orc_island_resample(uint64_t m, uint64_t seed, uint32_t n, const double* logW, int modified,
+                        int32_t* src, float* delta, double* logVbar, int64_t* Aisl)
+{
+    int S = ilog2_exact(m);
+    if (S < 1) return ORC_EINVAL;
+    double* lv = (double*)malloc(sizeof(double) * (m - 1));
+    int32_t* sr = (int32_t*)malloc(sizeof(int32_t) * m * (uint64_t)S);
+    if (!lv || !sr) {
+        free(lv); free(sr);
+        return ORC_ENOMEM;
+    }
+    const double scale = ldexp(1.0, 31);
+    for (int s = 1; s <= S; ++s) {
+        const double* prev = (s == 1) ? logW : lv + level_offset(m, s - 1);
+        double* cur = lv + level_offset(m, s);
+        for (uint64_t bk = 0; bk < (m >> s); ++bk) cur[bk] = log_pair_mean(prev[2 * bk], prev[2 * bk + 1]);
+        uint64_t bit = 1ull << (s - 1);
+        for (uint64_t i = 0; i < m; ++i) {
+            uint64_t h = i ^ bit;
+            uint64_t L = i < h ? i : h, R = i < h ? h : i;
+            double vl = prev[L >> (s - 1)], vr = prev[R >> (s - 1)];
+            double p = (vl == -INFINITY && vr == -INFINITY) ? 0.5 : 1.0 / (1.0 + exp(vr - vl));
+            uint64_t P = (uint64_t)floor(p * scale);
+            uint32_t r = rng_word(seed, (uint32_t)(i >> 2), n, ORC_DOMAIN_ISLAND, (uint32_t)s, (int)(i & 3u));
+            uint64_t hi = (uint64_t)(r >> 1);
+            sr[(uint64_t)(s - 1) * m + i] = (int32_t)((hi < P) ? L : R);
+            if (delta) delta[(uint64_t)(s - 1) * m + i] = (float)fabs(p - (double)(hi + 1) / scale);
+        }
+        if (modified) {
+            for (uint64_t L = 0; L < m; ++L) {
+                if (L & bit) continue;
+                uint64_t R = L | bit;
+                int32_t* sl = &sr[(uint64_t)(s - 1) * m + L];
+                int32_t* sR = &sr[(uint64_t)(s - 1) * m + R];
+                if (*sl == (int32_t)R && *sR == (int32_t)L) {
+                    *sl = (int32_t)L;
+                    *sR = (int32_t)R;
+                }
+            }
+        }
+    }
+    for (uint64_t i = 0; i < m; ++i) {
+        uint64_t c = i;
+        for (int s = S; s >= 1; --s) c = (uint64_t)sr[(uint64_t)(s - 1) * m + c];
+        Aisl[i] = (int64_t)c;
+    }
+    if (src) memcpy(src, sr, sizeof(int32_t) * m * (uint64_t)S);
+    if (logVbar) memcpy(logVbar, lv, sizeof(double) * (m - 1));
+    free(lv); free(sr);
+    return ORC_OK;
+}
+
+/* One AIRPF step (Alg. 4 rotated like Alg. 1, reading R7): mutate xin (n >= 1), weight,
+ * estimates (before resampling, as orc_step), within-island resample (Alg. 5), augmented
+ * island resample (Alg. 6/7) of the island blocks; xhat[i M + j] = x[a_w(Aisl(i) M + j)]. */
+int orc_step_airpf(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t seed, uint32_t n,
+                   const float* y, const float* xin, int modified, double* x, double* lw, int64_t* a_w,
+                   float* wdelta, double* logW, int32_t* src, float* idelta, double* logVbar, int64_t* Aisl,
+                   double* xhat_out, double* filt, double* pred)
+{
+    int d = mdl->d;
+    uint64_t m = N / M;
+    double* xprev = (double*)malloc(sizeof(double) * N * (uint64_t)d);
+    if (!xprev) return ORC_ENOMEM;
+    for (uint64_t i = 0; i < N * (uint64_t)d; ++i) xprev[i] = (double)xin[i];
+    if (n == 0) memcpy(x, xprev, sizeof(double) * N * (uint64_t)d);
+    else orc_mutate(mdl, N, seed, n, xprev, x);
+    free(xprev);
+    orc_logweight(mdl, N, y, x, lw);
+    orc_estimates(d, N, lw, x, NULL, filt, pred, NULL);
+    int rc = orc_within_island(N, M, seed, n, lw, a_w, wdelta, logW);
+    if (rc != ORC_OK) return rc;
+    rc = orc_island_resample(m, seed, n, logW, modified, src, idelta, logVbar, Aisl);
+    if (rc != ORC_OK) return rc;
+    for (uint64_t i = 0; i < m; ++i)
+        for (uint64_t j = 0; j < M; ++j) {
+            uint64_t a = (uint64_t)a_w[(uint64_t)Aisl[i] * M + j];
+            for (int k = 0; k < d; ++k) xhat_out[(i * M + j) * d + k] = x[a * d + k];
+        }
+    return ORC_OK;
 }
