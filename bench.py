@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--theta", type=float, default=0.0,
                     help="ESS threshold of the fully adapted scheme (0: plain augmented resampling)")
+    ap.add_argument("--airpf", type=int, default=0, choices=[0, 1, 2],
+                    help="AIRPF (Alg. 4) with Alg. 7 (1) or Alg. 6 (2) instead of augmented resampling")
     return ap.parse_args()
 
 
@@ -189,8 +191,8 @@ def ncu_traffic(cfg, kernel):
 
 
 def run_ours(args):
-    if args.theta > 0 and int(os.environ.get("WORLD_SIZE", "1")) > 1:
-        raise SystemExit("--theta (fully adapted scheme) runs on one GPU only")
+    if (args.theta > 0 or args.airpf) and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        raise SystemExit("--theta / --airpf run on one GPU only")
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -213,7 +215,8 @@ def run_ours(args):
     with torch.cuda.stream(stream):
         y_dev = torch.tensor(np.asarray(ys, np.float32), device=dev)
         if world == 1:
-            f = pf.ParticleFilter(params, cfg.N, cfg.M, args.seed, stream=stream, theta=args.theta)
+            f = pf.ParticleFilter(params, cfg.N, cfg.M, args.seed, stream=stream, theta=args.theta,
+                                  airpf=args.airpf)
 
             def step(k, yd=None):
                 f.step_dev(y_dev[k % T] if yd is None else yd)
@@ -311,7 +314,9 @@ def run_ours(args):
                 "config": dict(config_dict(cfg, world, "single" if world == 1 else f"groups sharded over {world} GPUs"),
                                **({"theta": args.theta, "stages_run_mean": float(np.mean(stages)),
                                    "stages_run_hist": np.bincount(stages, minlength=cfg.S + 1).tolist()}
-                                  if args.theta > 0 else {})),
+                                  if args.theta > 0 else {}),
+                               **({"algorithm": {1: "AIRPF (Alg. 4 + 5 + 7)", 2: "AIRPF (Alg. 4 + 5 + 6)"}[args.airpf]}
+                                  if args.airpf else {})),
                 "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line))

@@ -66,6 +66,9 @@ typedef struct pf_handle pf_handle;
 #define PF_FLAG_ADAPTIVE 2u /* reserve the buffers of the fully adapted scheme
                                (pf_set_adaptive; one GPU only): 8 N + 4 N/M + O(N/1024) bytes */
 
+#define PF_FLAG_AIRPF 4u /* reserve the island buffers of AIRPF (pf_set_airpf; one GPU, M >= 4):
+                            13 N/M + S N/(4M) bytes */
+
 /* Bytes of device workspace pf_init needs for this problem (0 if invalid). */
 size_t pf_workspace_bytes(const pf_model* model, uint64_t N, uint32_t M, uint32_t flags);
 
@@ -108,6 +111,17 @@ int pf_set_adaptive(pf_handle* h, double theta);
 
 /* S* of the last completed step (S for a plain step), or -1 before the first step. */
 int pf_last_stages(const pf_handle* h);
+
+/* --- AIRPF: augmented island resampling particle filter (Alg. 4) ---
+ * mode 1: Alg. 4 with the within-island resample (Alg. 5) and the modified augmented
+ * island resampling (Alg. 7: pure pairwise exchanges undone); mode 2: with Alg. 6; 0: back
+ * to Alg. 1 + Alg. 3 (pf_step).  Each later pf_step mutates the island blocks named by the
+ * previous step's island map, weights, resamples every island within itself (pool of M,
+ * R19) and composes the S island stages over whole blocks of M (R20, R21); pf_estimate
+ * gives the same estimates as for pf_step (before resampling).  Needs a handle created
+ * with PF_FLAG_AIRPF, world = 1, M >= 4; exclusive with pf_set_adaptive.  Errors:
+ * PF_EINVAL. */
+int pf_set_airpf(pf_handle* h, int mode);
 
 /* estimates (phi) */
 #define PF_PHI_X 1  /* phi(x) = x_k, k = 0..d-1 */
@@ -178,6 +192,10 @@ int pf_cross_stage(pf_handle* h, int t, const void* dev_partner_states);
 #define PF_DBG_LOGV 6      /* log V_s per block, all levels s = 1..S, m-1 fp64
                               (level s at offset m - m/2^{s-1}, m/2^s entries) */
 #define PF_DBG_ESS 8       /* E_0..E_S of the last adaptive step, S+1 fp64 (PF_FLAG_ADAPTIVE) */
+#define PF_DBG_ISLAND_A 9  /* AIRPF island map A_isl (block held by island g), m int32 */
+#define PF_DBG_ISLAND_CHOICE 10 /* AIRPF stage-s choices: ceil(m/4) bytes, bit e of byte q set =
+                                   island 4q+e took its partner's block (after Alg. 7's rule) */
+#define PF_DBG_ISLAND_LOGW 11   /* AIRPF log island means (W_out of Alg. 5), m fp64 */
 #define PF_DBG_THRESH 7    /* stage s >= 2 side thresholds floor(p 2^{32-b}), m-1 uint32,
                               same layout (stage s at offset m - m/2^{s-1}); entry 0.. of
                               level 1 unused */

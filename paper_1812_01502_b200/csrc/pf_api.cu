@@ -190,6 +190,7 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, uint64
 struct Layout {
     size_t X0, X1, logV, thr, part, scratch, est, ticket, y;
     size_t lw0, lw1, carry_lv, ess_part, ess_chunks, ess_out, ess_lmax;  // PF_FLAG_ADAPTIVE
+    size_t isl_A, isl_choice, isl_logW;                                  // PF_FLAG_AIRPF
     size_t shard_rec, recs, top_logV, top_thr, top_scratch;
     size_t dbg_x, dbg_lw, dbg_anc, dbg_A;
     size_t total;
@@ -229,6 +230,10 @@ Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags, uint32
     L.ess_chunks = take(ad ? (size_t)(p.NT / kEssChunk + 2 * m / kEssChunk + 64) * 2 * 8 : 0);
     L.ess_out = take(ad ? (size_t)(S + 3) * 8 : 0);
     L.ess_lmax = take(ad ? 16 : 0);
+    const bool air = flags & PF_FLAG_AIRPF;
+    L.isl_A = take(air ? m * 4 : 0);
+    L.isl_choice = take(air ? (size_t)S * ((m + 3) / 4) : 0);
+    L.isl_logW = take(air ? m * 8 : 0);
     const bool dbg = flags & PF_FLAG_DEBUG;
     L.dbg_x = take(dbg ? xb : 0);
     L.dbg_lw = take(dbg ? N * 4 : 0);
@@ -267,6 +272,9 @@ struct pf_handle {
     int carry_mode = 0;      // 0 none, 1 particle (lw of the other buffer), 2 block (carry_lv)
     uint32_t carry_shift = 0;
     double carry_c = 0.0;
+    // AIRPF (pf_set_airpf)
+    int airpf = 0;           // 0 off, 1 Alg. 7 (modified), 2 Alg. 6 (plain)
+    bool isl_valid = false;  // X(cur) is a within-resampled sample read through the island map
     // kernel timing
     bool timing;
     struct Rec {
@@ -462,7 +470,7 @@ static void launch_cascade_k(pf_handle* h) {
     c.m = h->m;
     c.S = h->S;
     c.k1 = p.k1;
-    c.b = h->b;
+    c.b = h->airpf ? 1u : h->b;  // AIRPF: 31-bit island thresholds (R20)
     c.NT = p.NT;
     c.LPC = p.LPC;
     launch_cascade(p.D, LaunchCfg{p.cascade_grid, (uint32_t)kCascadeThreads, 0u, h->stream}, c);
@@ -541,6 +549,8 @@ static void fill_pass1(pf_handle* h, Pass1Args& a, const float* y_host, const fl
     a.carry_c = 0.0;
     a.ess_part = nullptr;
     a.ess_lmax = nullptr;
+    a.isl_src = nullptr;
+    a.logW = nullptr;
 }
 
 // One step of the fully adapted scheme (include/pf.h pf_set_adaptive; R17/R18):
@@ -636,8 +646,48 @@ static int run_step_adaptive(pf_handle* h, const float* y_host, const float* y_d
     return check_cuda(h, "pf_step");
 }
 
+// One AIRPF step (Alg. 4 rotated like Alg. 1; R19-R21):
+//   k_pass1 (AIRPF mode: read the island blocks named by the previous island map, mutate,
+//   weight, within-island resample, island levels 1..k1) -> k_cascade (levels k1+1..S,
+//   island thresholds) -> k_island_draw -> k_island_compose (the new island map).
+// x_hat is never materialised: the next step reads block A_isl[g] for island g.
+static int run_step_airpf(pf_handle* h, const float* y_host, const float* y_dev) {
+    Pass1Args a;
+    fill_pass1(h, a, y_host, y_dev);
+    a.x_in = h->X(h->cur);
+    a.x_out = h->X(h->cur ^ 1);
+    a.isl_src = h->isl_valid ? h->at<int32_t>(h->lay.isl_A) : nullptr;
+    a.logW = h->at<double>(h->lay.isl_logW);
+    h->mark(PF_KERNEL_PASS1, true);
+    launch_pass1(h, a, kPass1Airpf);
+    h->mark(PF_KERNEL_PASS1, false);
+    h->mark(PF_KERNEL_CASCADE, true);
+    launch_cascade_k(h);
+    IslandArgs ia;
+    ia.key = make_key(h->seed);
+    ia.n = h->n;
+    ia.m = h->m;
+    ia.S = h->S;
+    ia.modified = h->airpf == 1;
+    ia.thr = h->at<uint32_t>(h->lay.thr);
+    ia.choice = h->at<uint8_t>(h->lay.isl_choice);
+    ia.A = h->at<int32_t>(h->lay.isl_A);
+    launch_island(h->stream, ia);
+    h->mark(PF_KERNEL_CASCADE, false);
+    h->cur ^= 1;
+    h->isl_valid = true;
+    h->sstar_last = (int)h->S;
+    h->step_n = h->n;
+    h->n += 1;
+    h->have_step = true;
+    h->top_done = true;
+    h->last_launches = 4;
+    return check_cuda(h, "pf_step (AIRPF)");
+}
+
 static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
     if (h->theta > 0.0) return run_step_adaptive(h, y_host, y_dev);
+    if (h->airpf) return run_step_airpf(h, y_host, y_dev);
     const Plan& p = h->plan;
     Pass1Args a;
     fill_pass1(h, a, y_host, y_dev);
@@ -711,6 +761,8 @@ static int init_core(const pf_model* model, uint64_t N, uint32_t M, uint64_t see
     if (!validate_topology(N, M, &err)) return fail(nullptr, PF_EINVAL, err);
     if (!shard_geometry(N, M, rank, world, &Nloc, &err)) return fail(nullptr, PF_EINVAL, err);
     if ((flags & PF_FLAG_ADAPTIVE) && world != 1) return fail(nullptr, PF_EINVAL, "PF_FLAG_ADAPTIVE needs world = 1");
+    if ((flags & PF_FLAG_AIRPF) && (world != 1 || M < 4u))
+        return fail(nullptr, PF_EINVAL, "PF_FLAG_AIRPF needs world = 1 and M >= 4");
     Plan p;
     int nsm = 148, dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
@@ -964,7 +1016,26 @@ int pf_debug_ptr(pf_handle* h, int what, int stage, void** dev_out) {
             *dev_out = A;
             return check_cuda(h, "pf_debug_ptr");
         }
-        case PF_DBG_XHAT: *dev_out = h->X(h->cur); return PF_OK;
+        case PF_DBG_XHAT:
+            if (h->airpf && h->isl_valid) {  // materialise x_hat = the island blocks (into the free buffer)
+                launch_block_gather(h->stream, h->X(h->cur), h->X(h->cur ^ 1), h->at<int32_t>(h->lay.isl_A), h->N, h->b,
+                                    (uint32_t)D);
+                *dev_out = h->X(h->cur ^ 1);
+                return check_cuda(h, "pf_debug_ptr");
+            }
+            *dev_out = h->X(h->cur);
+            return PF_OK;
+        case PF_DBG_ISLAND_A:
+        case PF_DBG_ISLAND_CHOICE:
+        case PF_DBG_ISLAND_LOGW:
+            if (!(h->flags & PF_FLAG_AIRPF) || !h->isl_valid) return fail(h, PF_ESTATE, "no AIRPF step");
+            if (what == PF_DBG_ISLAND_A) *dev_out = h->at<int32_t>(h->lay.isl_A);
+            else if (what == PF_DBG_ISLAND_LOGW) *dev_out = h->at<double>(h->lay.isl_logW);
+            else {
+                if (stage < 1 || stage > (int)h->S) return fail(h, PF_EINVAL, "stage out of range");
+                *dev_out = h->at<uint8_t>(h->lay.isl_choice) + (size_t)(stage - 1) * ((h->m + 3) / 4);
+            }
+            return PF_OK;
         case PF_DBG_LOGV: *dev_out = h->at<double>(h->lay.logV); return PF_OK;
         case PF_DBG_THRESH: *dev_out = h->at<uint32_t>(h->lay.thr); return PF_OK;
         case PF_DBG_ESS:
@@ -990,6 +1061,9 @@ int pf_debug_get(pf_handle* h, int what, int stage, void* host_out, size_t bytes
         case PF_DBG_LOGV: need = (size_t)(h->m - 1) * 8; break;
         case PF_DBG_THRESH: need = (size_t)(h->m - 1) * 4; break;
         case PF_DBG_ESS: need = (size_t)(h->S + 1) * 8; break;
+        case PF_DBG_ISLAND_A: need = (size_t)h->m * 4; break;
+        case PF_DBG_ISLAND_CHOICE: need = (size_t)(h->m + 3) / 4; break;
+        case PF_DBG_ISLAND_LOGW: need = (size_t)h->m * 8; break;
     }
     if (!host_out || bytes < need) return fail(h, PF_EINVAL, "host buffer too small");
     cudaError_t e = cudaMemcpyAsync(host_out, p, need, cudaMemcpyDeviceToHost, h->stream);
@@ -1006,7 +1080,23 @@ int pf_debug_set_state(pf_handle* h, const float* host_xhat, uint32_t n) {
     if (e != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_debug_set_state: ") + cudaGetErrorString(e));
     h->n = n;
     h->carry_mode = 0;  // the given state is unweighted
+    h->isl_valid = false;  // and holds x_hat itself
     return PF_OK;
+}
+
+int pf_set_airpf(pf_handle* h, int mode) {
+    if (!h) return fail(h, PF_EINVAL, "NULL handle");
+    if (mode < 0 || mode > 2) return fail(h, PF_EINVAL, "mode must be 0 (off), 1 (Alg. 7) or 2 (Alg. 6)");
+    if (mode && !(h->flags & PF_FLAG_AIRPF)) return fail(h, PF_EINVAL, "handle not created with PF_FLAG_AIRPF");
+    if (mode && h->theta > 0.0) return fail(h, PF_EINVAL, "AIRPF and the fully adapted scheme are exclusive");
+    if (!mode && h->isl_valid) {  // back to augmented resampling: materialise x_hat first
+        launch_block_gather(h->stream, h->X(h->cur), h->X(h->cur ^ 1), h->at<int32_t>(h->lay.isl_A), h->N, h->b,
+                            (uint32_t)h->plan.D);
+        h->cur ^= 1;
+        h->isl_valid = false;
+    }
+    h->airpf = mode;
+    return check_cuda(h, "pf_set_airpf");
 }
 
 int pf_set_adaptive(pf_handle* h, double theta) {
@@ -1015,6 +1105,7 @@ int pf_set_adaptive(pf_handle* h, double theta) {
     if (theta > 0.0 && !(h->flags & PF_FLAG_ADAPTIVE))
         return fail(h, PF_EINVAL, "handle not created with PF_FLAG_ADAPTIVE");
     if (theta > 0.0 && h->world != 1) return fail(h, PF_EINVAL, "the fully adapted scheme needs world = 1");
+    if (theta > 0.0 && h->airpf) return fail(h, PF_EINVAL, "AIRPF and the fully adapted scheme are exclusive");
     h->theta = theta;
     if (theta == 0.0) h->carry_mode = 0;
     return PF_OK;

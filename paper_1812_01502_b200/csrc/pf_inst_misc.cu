@@ -79,6 +79,80 @@ __global__ void k_ess_final(const __grid_constant__ EssArgs a) {
 }
 
 
+// Side draws of the four islands of quad c4 at stage s: bit e set = island 4 c4 + e takes
+// its partner's block (before Alg. 7's exchange rule).
+__device__ __forceinline__ uint32_t island_takes(const IslandArgs& a, uint32_t c4, uint32_t s) {
+    const uint4 blk = rng_block(a.key, c4, a.n, kDomainIsland, s);
+    const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
+    const uint32_t bit = 1u << (s - 1);
+    uint32_t take = 0u;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const uint32_t i = 4u * c4 + (uint32_t)e;
+        if (i >= a.m) break;
+        const uint32_t P = a.thr[level_offset(a.m, (int)s) + (i >> s)];
+        const bool left = (r[e] >> 1) < P;   // the pair's lower island is chosen
+        const bool i_is_left = (i & bit) == 0u;
+        if (left != i_is_left) take |= 1u << e;
+    }
+    return take;
+}
+
+__global__ void __launch_bounds__(256) k_island_draw(const __grid_constant__ IslandArgs a) {
+    const uint32_t nq = (a.m + 3u) >> 2;
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t >= (uint64_t)nq * a.S) return;
+    const uint32_t s = (uint32_t)(t / nq) + 1u, c4 = (uint32_t)(t % nq);
+    uint32_t take = island_takes(a, c4, s);
+    if (a.modified) {  // Alg. 7: a pair that swapped blocks keeps its own
+        const uint32_t bit = 1u << (s - 1);
+        const uint32_t p4 = (bit >= 4u) ? (c4 ^ (bit >> 2)) : c4;
+        const uint32_t ptake = (p4 == c4) ? take : island_takes(a, p4, s);
+        uint32_t keep = 0u;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t i = 4u * c4 + (uint32_t)e;
+            const uint32_t h = i ^ bit;
+            const uint32_t eh = h & 3u;
+            if (((take >> e) & 1u) && ((ptake >> eh) & 1u)) keep |= 1u << e;
+        }
+        take &= ~keep;
+    }
+    a.choice[(uint64_t)(s - 1) * nq + c4] = (uint8_t)take;
+}
+
+__global__ void __launch_bounds__(256) k_island_compose(const __grid_constant__ IslandArgs a) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= a.m) return;
+    const uint32_t nq = (a.m + 3u) >> 2;
+    uint32_t c = g;
+    for (uint32_t s = a.S; s >= 1u; --s) {
+        const uint32_t take = (__ldg(a.choice + (uint64_t)(s - 1) * nq + (c >> 2)) >> (c & 3u)) & 1u;
+        c ^= take << (s - 1);
+    }
+    a.A[g] = (int32_t)c;
+}
+
+void launch_island(cudaStream_t st, const IslandArgs& a) {
+    const uint64_t work = (uint64_t)((a.m + 3u) >> 2) * a.S;
+    k_island_draw<<<(uint32_t)((work + 255) / 256), 256, 0, st>>>(a);
+    k_island_compose<<<(a.m + 255) / 256, 256, 0, st>>>(a);
+}
+
+// x_hat of an AIRPF step for the debug interface: out[g M + j] = in[A[g] M + j].
+__global__ void k_block_gather(const float* in, float* out, const int32_t* A, uint64_t N, uint32_t b, uint32_t D) {
+    for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < N * D; f += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = f / D, k = f % D;
+        const uint64_t src = ((uint64_t)A[i >> b] << b) | (i & ((1ull << b) - 1ull));
+        out[f] = in[src * D + k];
+    }
+}
+
+void launch_block_gather(cudaStream_t st, const float* in, float* out, const int32_t* A, uint64_t N, uint32_t b,
+                         uint32_t D) {
+    k_block_gather<<<1184, 256, 0, st>>>(in, out, A, N, b, D);
+}
+
 void launch_cascade(int D, const LaunchCfg& c, const CascadeArgs& a) {
     switch (D) {
         case 1: k_cascade<1><<<c.grid, c.threads, 0, c.stream>>>(a); break;

@@ -271,6 +271,23 @@ __host__ __device__ inline uint32_t ess_chunks_total(const EssArgs& a) {
 }
 
 // -------------------------------------------------------------------------------------
+// AIRPF island stages (Alg. 6 / Alg. 7; R20, R21).
+//   k_island_draw     thread per (stage s, quad of islands): the four islands' side draws
+//                     (Philox block (quad, n, ISLAND<<24 | s)), side L iff (r >> 1) <
+//                     thr_s[pair]; Alg. 7 undoes a pure exchange (needs the partner quad's
+//                     block when the partner lies in another quad); writes one nibble per
+//                     quad: bit e = island 4 quad + e takes its partner's block
+//   k_island_compose  thread per island: walks stages S..1 through the nibbles -> A_isl
+struct IslandArgs {
+    Key key;
+    uint32_t n, m, S;
+    int modified;
+    const uint32_t* thr;   // side thresholds, level-table layout (stage s at level_offset(m, s))
+    uint8_t* choice;       // S x nq nibbles (nq = ceil(m / 4))
+    int32_t* A;            // m: island map
+};
+
+// -------------------------------------------------------------------------------------
 template <typename T>
 struct __align__(4 * sizeof(T) <= 16 ? 4 * sizeof(T) : 16) Vec4 {
     T v[4];

@@ -43,6 +43,9 @@ inline void launch_stages(int D, int tb, bool dbg, int qpt, const LaunchCfg& c, 
 }
 void launch_cascade(int D, const LaunchCfg& c, const CascadeArgs& a);
 void launch_ess(const LaunchCfg& chunks, const EssArgs& a);
+void launch_island(cudaStream_t st, const IslandArgs& a);
+void launch_block_gather(cudaStream_t st, const float* in, float* out, const int32_t* A, uint64_t N, uint32_t b,
+                         uint32_t D);
 void launch_init(int D, int kind, const LaunchCfg& c, const InitArgs& a);
 void launch_top(int D, const LaunchCfg& c, const TopArgs& a);
 void launch_cross(int payload, bool dbg, const LaunchCfg& c, const CrossArgs& a);

@@ -47,7 +47,7 @@ __host__ __device__ inline Pass1Smem pass1_smem(int D, uint32_t P1, uint32_t M, 
     s.L1 = take(P1 * tb);
     s.tab = take(k1 >= 2 ? (k1 - 1u) * P1 * tb : 0u);
     s.chunk = take(M > 64 ? (P1 / 128u) * 4u : 0u);  // per-warp-chunk maxima / totals
-    s.lv1 = take((T1 / 2) * 8u);
+    s.lv1 = take(T1 * 8u);  // pair (or, AIRPF, island) log-means
     s.red = take((threads / 32u) * (2u + 4u * (uint32_t)D) * 4u);
     s.ess = take((threads / 32u) * 4u);  // per-warp sum of squared weights (kPass1Weigh)
     s.total = off;
@@ -83,6 +83,9 @@ struct Pass1Args {
     double carry_c;         // log V_S of the previous step
     double* ess_part;       // kPass1Weigh: per tile {max lw, sum e^{lw-max}, sum e^{2(lw-max)}}
     unsigned int* ess_lmax; // kPass1Weigh: running max of lw (order-preserving float bits)
+    // AIRPF (kPass1Airpf; R19-R21)
+    const int32_t* isl_src; // previous step's island map A_isl (group g reads block isl_src[g]); null = identity
+    double* logW;           // log island means (m)
 };
 
 // Order-preserving map of float bits to unsigned (atomicMax of floats).
@@ -104,6 +107,12 @@ __host__ __device__ inline unsigned int float_order_bits(float f) {
 constexpr int kPass1Fused = 0;
 constexpr int kPass1Weigh = 1;
 constexpr int kPass1Resample = 2;
+//   kPass1Airpf    AIRPF (Alg. 4): mutate the island blocks named by the previous island
+//                  map, weight, within-island resample (Alg. 5: pool = the island's M
+//                  particles, WITHIN draws), island log-means, island levels 1..k1 and the
+//                  island side thresholds (31-bit, R20); writes the within-resampled
+//                  sample in natural order (the island stages run in k_island_*)
+constexpr int kPass1Airpf = 3;
 
 // Sum of NV = 2^v values over the 32 lanes of a warp by recursive halving: after the
 // call, lane l holds the total of value (l >> (5 - v)) in v[0].
@@ -148,7 +157,9 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
     const uint32_t tile = blockIdx.x;
     const uint32_t base = tile * P1;  // N < 2^31
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nwarps = threads >> 5;
-    const uint32_t Z = M >> 1;  // quads per stage-1 pair (2M positions)
+    constexpr bool AIR = MODE == kPass1Airpf;
+    const uint32_t Z = AIR ? (M >> 2) : (M >> 1);  // quads per stage-1 pool (2M positions; AIRPF: one island of M)
+    const uint32_t pool_sh = AIR ? b : b + 1u;      // log2 of the pool size
     const uint32_t c0t = (a.pos0 + base) >> 2;  // Philox counter of the tile's first quad
 
     // ---- 1. load xhat_{n-1} (all slots first: independent loads in flight) -------------
@@ -161,9 +172,12 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
             for (int k = 0; k < 4 * D; ++k) xh[it][k] = 0.0f;
             continue;
         }
+        uint32_t src_q = base + 4u * q;  // AIRPF: the quad's position inside the island block it reads
+        if constexpr (AIR)
+            if (a.isl_src) src_q = ((uint32_t)a.isl_src[src_q >> b] << b) | (src_q & (M - 1u));
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-            const float4 t = __ldg(reinterpret_cast<const float4*>(a.x_in + (uint64_t)(base + 4u * q) * D) + c);
+            const float4 t = __ldg(reinterpret_cast<const float4*>(a.x_in + (uint64_t)src_q * D) + c);
             xh[it][4 * c] = t.x;
             xh[it][4 * c + 1] = t.y;
             xh[it][4 * c + 2] = t.z;
@@ -352,16 +366,18 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
             tot[it] = all;
         }
     }
-    const float log2M = logf((float)(2u * M));
+    const float log2M = logf((float)(4u * Z));  // log of the pool size
 #pragma unroll
     for (int it = 0; it < QPT; ++it) {
         const uint32_t q = tid + it * threads;
         if (q >= nq) continue;
         reinterpret_cast<float4*>(w)[q] =
             make_float4(excl[it] + run[it][0], excl[it] + run[it][1], excl[it] + run[it][2], excl[it] + run[it][3]);
-        if (((4u * q) & (2u * M - 1u)) == 0u)  // first quad of its pair: log V_1 of the pair
-            lv1[(4u * q) >> (b + 1)] =
-                pm[it] == -CUDART_INF_F ? -CUDART_INF : (double)pm[it] + (double)(logf(tot[it]) - log2M);
+        if (((4u * q) & ((1u << pool_sh) - 1u)) == 0u) {  // first quad of its pool: log mean of the pool
+            const double lm = pm[it] == -CUDART_INF_F ? -CUDART_INF : (double)pm[it] + (double)(logf(tot[it]) - log2M);
+            lv1[(4u * q) >> pool_sh] = lm;
+            if constexpr (AIR) a.logW[((uint64_t)base >> b) + ((4u * q) >> b)] = lm;
+        }
     }
     if (Z <= 32u) __syncwarp();  // a pair's CDF was written by this warp
     else __syncthreads();
@@ -372,8 +388,9 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
         for (int it = 0; it < QPT; ++it) {
             const uint32_t q = tid + it * threads;
             const bool valid = q < nq;
-            const uint4 blk = rng_block(a.key, c0t + q, a.n, kDomainResample, 1u);
-            const uint32_t pb = valid ? (((4u * q) >> (b + 1)) << (b + 1)) : 0u;
+            const uint4 blk = AIR ? rng_block(a.key, c0t + q, a.n, kDomainWithin, 0u)
+                                  : rng_block(a.key, c0t + q, a.n, kDomainResample, 1u);
+            const uint32_t pb = valid ? (((4u * q) >> pool_sh) << pool_sh) : 0u;
             const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -381,7 +398,7 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
                 tq[it][e] = valid ? u01f(r[e]) * tot[it] : -1.0f;
             }
         }
-        for (uint32_t step = M; step >= 1u; step >>= 1) {
+        for (uint32_t step = 2u * Z; step >= 1u; step >>= 1) {
 #pragma unroll
             for (int it = 0; it < QPT; ++it)
 #pragma unroll
@@ -397,7 +414,7 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
                     make_int4((int)(a.pos0 + base + lo[it][0]), (int)(a.pos0 + base + lo[it][1]),
                               (int)(a.pos0 + base + lo[it][2]), (int)(a.pos0 + base + lo[it][3]));
             if constexpr (TB == 1) {
-                const uint32_t pm2 = 2u * M - 1u;  // pool index a = lo - pair base
+                const uint32_t pm2 = 4u * Z - 1u;  // pool index a = lo - pool base
                 *reinterpret_cast<uint32_t*>(L1 + 4u * q) = (lo[it][0] & pm2) | ((lo[it][1] & pm2) << 8) |
                                                              ((lo[it][2] & pm2) << 16) | ((lo[it][3] & pm2) << 24);
             } else {
@@ -437,7 +454,17 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
     uint32_t thr[7];
     {
         const uint32_t npair = T1 >> 1;
-        double v = lane < npair ? lv1[lane] : -CUDART_INF;
+        const int tb_bits = AIR ? 1 : (int)b;  // threshold resolution 2^-(32-tb_bits) (R1; AIRPF R20)
+        double v;
+        if constexpr (AIR) {  // level 1 = pair means of the island log-means; stage-1 island thresholds
+            double nv = -CUDART_INF;
+            uint32_t Pt = 0u;
+            if (lane < npair) pair_level_fast(lv1[2u * lane], lv1[2u * lane + 1u], 1, &nv, &Pt);
+            v = nv;
+            if (warp == 0 && lane < npair) a.thr[level_offset(a.m, 1) + (uint64_t)tile * npair + lane] = Pt;
+        } else {
+            v = lane < npair ? lv1[lane] : -CUDART_INF;
+        }
         if (warp == 0 && lane < npair) a.logV[level_offset(a.m, 1) + (uint64_t)tile * npair + lane] = v;
 #pragma unroll
         for (int s = 2; s <= 6; ++s) {
@@ -448,7 +475,7 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
             const bool act = (lane & (2u * stp - 1u)) == 0u && lane < npair;
             uint32_t Pt;
             double nv;
-            pair_level_fast(v, vr, (int)b, &nv, &Pt);
+            pair_level_fast(v, vr, tb_bits, &nv, &Pt);
             thr[s] = Pt;
             if (act) {
                 v = nv;
@@ -464,6 +491,7 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
     if constexpr (MODE != kPass1Weigh) {  // sections 5-6: the draws and the walk
     // ---- 5. stages 2..k1: every draw depends only on its word and the threshold ---------
     const uint32_t mask = M - 1u;
+    if constexpr (!AIR) {
 #pragma unroll
     for (int it = 0; it < QPT; ++it) {
         const uint32_t q = tid + it * threads;
@@ -499,6 +527,7 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
         }
     }
     __syncthreads();  // D: all stage tables ready
+    }  // !AIR
 
     // ---- 6. compose backwards and write the tile at its stage-k1 positions ------------
 #pragma unroll
@@ -506,7 +535,7 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
         const uint32_t q = tid + it * threads;
         if (q >= nq) continue;
         uint32_t tp[4] = {4u * q, 4u * q + 1u, 4u * q + 2u, 4u * q + 3u};
-        for (uint32_t s = k1; s >= 2u; --s) {
+        for (uint32_t s = AIR ? 1u : k1; s >= 2u; --s) {  // AIRPF: the within-island draw only
             const unsigned char* Ts = tab + (s - 2u) * P1 * TB;
             if constexpr (TB == 1) {
                 const uint32_t sh = s - 1u + b;
@@ -523,7 +552,7 @@ __global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args
         }
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            if constexpr (TB == 1) tp[e] = (tp[e] & ~(2u * M - 1u)) | L1[tp[e]];
+            if constexpr (TB == 1) tp[e] = (tp[e] & ~(4u * Z - 1u)) | L1[tp[e]];
             else tp[e] = reinterpret_cast<const uint16_t*>(L1)[tp[e]];
         }
         float v[4 * D];

@@ -22,10 +22,12 @@ PF_OK, PF_EINVAL, PF_EWORKSPACE, PF_ECUDA, PF_EOBS, PF_ESTATE = 0, -1, -2, -3, -
 PF_LG, PF_SV = 1, 2
 PF_FLAG_DEBUG = 1
 PF_FLAG_ADAPTIVE = 2
+PF_FLAG_AIRPF = 4
 PF_PHI_X, PF_PHI_X2 = 1, 2
 PF_EST_FILTER, PF_EST_PREDICT = 1, 2
 PF_DBG_X, PF_DBG_LOGW, PF_DBG_ANC_STAGE, PF_DBG_ANC_FINAL, PF_DBG_XHAT, PF_DBG_LOGV, PF_DBG_THRESH = 1, 2, 3, 4, 5, 6, 7
 PF_DBG_ESS = 8
+PF_DBG_ISLAND_A, PF_DBG_ISLAND_CHOICE, PF_DBG_ISLAND_LOGW = 9, 10, 11
 
 
 class PFError(RuntimeError):
@@ -81,6 +83,7 @@ def lib() -> ctypes.CDLL:
         L.pf_cross_stage.argtypes = [vp, ctypes.c_int, vp]
         L.pf_set_adaptive.argtypes = [vp, ctypes.c_double]
         L.pf_last_stages.argtypes = [vp]
+        L.pf_set_airpf.argtypes = [vp, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -89,7 +92,7 @@ EXPORTED = ["pf_workspace_bytes", "pf_init", "pf_step", "pf_step_dev", "pf_estim
             "pf_last_error", "pf_debug_get", "pf_debug_ptr", "pf_debug_set_state", "pf_last_step_launches",
             "pf_timing_enable", "pf_timing_read", "pf_workspace_bytes_sharded", "pf_init_sharded",
             "pf_step_local", "pf_shard_record", "pf_step_top", "pf_cross_buffer", "pf_cross_stage",
-            "pf_set_adaptive", "pf_last_stages"]
+            "pf_set_adaptive", "pf_last_stages", "pf_set_airpf"]
 PF_KERNEL_KINDS = 5
 KERNEL_NAMES = ("k_pass1", "k_cascade", "k_stages", "k_top", "k_cross")
 
@@ -159,6 +162,10 @@ def pf_set_adaptive(h, theta: float):
     _check(lib().pf_set_adaptive(h, float(theta)), h)
 
 
+def pf_set_airpf(h, mode: int):
+    _check(lib().pf_set_airpf(h, int(mode)), h)
+
+
 def pf_last_stages(h) -> int:
     return int(lib().pf_last_stages(h))
 
@@ -172,9 +179,10 @@ class ParticleFilter:
     """One filter on one GPU: workspace in a torch uint8 tensor, work on a torch stream."""
 
     def __init__(self, params: dict, N: int, M: int, seed: int, debug: bool = False, device: str = "cuda",
-                 stream=None, theta: float = 0.0):
+                 stream=None, theta: float = 0.0, airpf: int = 0):
         """theta > 0: fully adapted augmented resampling with ESS threshold theta
-        (pf_set_adaptive); the handle then reserves the adaptive buffers."""
+        (pf_set_adaptive); airpf = 1 (Alg. 7) or 2 (Alg. 6): AIRPF (pf_set_airpf).  The
+        handle then reserves the buffers of that scheme."""
         import torch
 
         self.torch = torch
@@ -184,7 +192,8 @@ class ParticleFilter:
         self.dy = int(params["dy"])
         self.m = self.N // self.M
         self.S = int(round(np.log2(self.m)))
-        self.flags = (PF_FLAG_DEBUG if debug else 0) | (PF_FLAG_ADAPTIVE if theta > 0 else 0)
+        self.flags = ((PF_FLAG_DEBUG if debug else 0) | (PF_FLAG_ADAPTIVE if theta > 0 else 0) |
+                      (PF_FLAG_AIRPF if airpf else 0))
         self.device = torch.device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         nbytes = pf_workspace_bytes(params, self.N, self.M, self.flags)
@@ -198,6 +207,8 @@ class ParticleFilter:
         self.h = pf_init(params, self.N, self.M, self.seed, self.flags, self.ws_ptr, nbytes, self.stream.cuda_stream)
         if theta > 0:
             pf_set_adaptive(self.h, theta)
+        if airpf:
+            pf_set_airpf(self.h, airpf)
 
     def last_stages(self) -> int:
         """S* of the last step (S for a plain step)."""
@@ -254,6 +265,12 @@ class ParticleFilter:
             n, dt, shape = (self.m - 1) * 4, torch.int32, (self.m - 1,)
         elif what == PF_DBG_ESS:
             n, dt, shape = (self.S + 1) * 8, torch.float64, (self.S + 1,)
+        elif what == PF_DBG_ISLAND_A:
+            n, dt, shape = self.m * 4, torch.int32, (self.m,)
+        elif what == PF_DBG_ISLAND_CHOICE:
+            n, dt, shape = (self.m + 3) // 4, torch.uint8, ((self.m + 3) // 4,)
+        elif what == PF_DBG_ISLAND_LOGW:
+            n, dt, shape = self.m * 8, torch.float64, (self.m,)
         else:
             raise ValueError(what)
         return self.ws[off: off + n].view(dt).view(shape)
