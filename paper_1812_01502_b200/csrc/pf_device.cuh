@@ -91,9 +91,19 @@ __device__ __forceinline__ float neg2_log_u1(uint32_t a) {
 // u1 = ((a>>8)+1) 2^-24 in (0,1] and u2 = (b>>8) 2^-24 in [0,1).
 // The square root uses MUFU.RSQ and the angle the MUFU sin/cos on [-pi, pi):
 // cos(2 pi u2) = -cos(th), sin(2 pi u2) = -sin(th) with th = 2 pi u2 - pi.
-// Absolute error <= ~3e-6.
+// Absolute error <= ~3e-6.  -2 ln u1 takes the MUFU lg2 unless u1 is within
+// 2^-10 of 1 (kFastLogLimit).
+// Fast branch of -2 ln u1: MUFU lg2 has absolute error <= 2^-22.6 on [0.5, 1) and relative
+// error <= 2^-22 below, so for u1 < 1 - 2^-10 the radius R = sqrt(-2 ln u1) is within
+// ~2.5e-6 of exact (worst case at the limit, R ~ 0.045); above the limit (probability
+// 2^-10 per pair) the precise neg2_log_u1 runs.
+constexpr uint32_t kFastLogLimit = (1u << 24) - (1u << 14);  // u1 = n 2^-24 < 1 - 2^-10
+
 __device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
-    const float r2 = neg2_log_u1(a);
+    const uint32_t na = (a >> 8) + 1u;
+    float r2;
+    if (na < kFastLogLimit) r2 = -1.3862943611198906f * __log2f((float)na * 0x1p-24f);  // -2 ln 2 lg2(u1)
+    else r2 = neg2_log_u1(a);
     const float rad = r2 * rsqrtf(fmaxf(r2, 1e-30f));
     const float th = fmaf((float)(b >> 8), 6.28318530717958647692f * 0x1p-24f, -3.14159265358979323846f);
     float s, c;
