@@ -37,7 +37,8 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
     const char* v = getenv(name);
     return (v && *v) ? (uint32_t)strtoul(v, nullptr, 10) : dflt;
 }
-constexpr uint32_t kLPC = 2048u;
+constexpr uint32_t kLPC = 2048u;    // max cascade CTAs (and max leaves per CTA)
+constexpr uint32_t kLPCMin = 64u;   // min leaves per cascade CTA
 
 struct StagePass {
     uint32_t s0, k, P, threads, qpt, smem, tb, grid, pipe;
@@ -132,7 +133,14 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, uint64
         return false;
     }
     p.NT = (uint32_t)(N / P1);
-    p.LPC = std::min<uint32_t>(p.NT, kLPC);
+    // leaves per cascade CTA: as few as keep the CTA subtrees in one wave on the SMs (one
+    // CTA walking the whole tree dominated small configurations; more than a wave of CTAs
+    // or a wide top tree for the last CTA slows large ones), within [kLPCMin, kLPC]
+    {
+        uint32_t lpc = kLPCMin;
+        while (lpc < kLPC && (uint64_t)lpc * nsm < p.NT) lpc <<= 1;
+        p.LPC = std::min<uint32_t>(p.NT, lpc);
+    }
     p.cascade_grid = p.NT / p.LPC;
     if (p.cascade_grid > kLPC) {
         *err = "too many pass-1 tiles for the cascade tree";
