@@ -138,7 +138,7 @@ __device__ __forceinline__ float warp_sum_transpose(float* v, uint32_t lane) {
 }
 
 template <int D, int KIND, bool DBG, int QPT, int TB, int MODE = kPass1Fused>
-__global__ void __launch_bounds__(512) k_pass1(const __grid_constant__ Pass1Args a) {
+__global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : 1) k_pass1(const __grid_constant__ Pass1Args a) {
     constexpr int PS = 2 + 4 * D;  // partial: max, sw, s1[D], s2[D], p1[D], p2[D]
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t threads = blockDim.x;
