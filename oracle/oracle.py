@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "pf_oracle.c")
 _LIB = os.path.join(_HERE, "libpforacle.so")
 
-INIT, MUTATE, RESAMPLE, WITHIN, ISLAND = 1, 2, 3, 4, 5
+INIT, MUTATE, RESAMPLE, WITHIN, ISLAND, MULTI = 1, 2, 3, 4, 5, 6
 
 
 def build(force: bool = False) -> str:
@@ -63,6 +63,8 @@ def lib():
         _lib.orc_island_resample.argtypes = [u64, u64, u32, vp, ctypes.c_int, vp, vp, vp, vp]
         _lib.orc_step_airpf.argtypes = [vp, u64, u64, u64, u32, vp, vp, ctypes.c_int, vp, vp, vp, vp, vp, vp,
                                         vp, vp, vp, vp, vp]
+        _lib.orc_multinomial.argtypes = [u64, u64, u32, vp, vp, vp]
+        _lib.orc_step_multinomial.argtypes = [vp, u64, u64, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         _lib.orc_step_adaptive.argtypes = [vp, u64, u64, u64, u32, vp, vp, vp, ctypes.c_double, vp, vp, vp, vp,
                                            vp, vp, vp, vp, vp, vp, vp, vp]
     return _lib
@@ -353,6 +355,45 @@ def run_filter_airpf(params: dict, M: int, m: int, seed: int, ys: np.ndarray, mo
     means = np.zeros((len(ys), d))
     for n, y in enumerate(ys):
         r = step_airpf(params, N, M, seed, n, y, x, modified)
+        means[n] = r["filter"][:d]
+        x = r["xhat"].astype(np.float32)
+    return means
+
+
+# ----------------------------------------------------------------------------- Alg. 2
+def multinomial(lw: np.ndarray, seed: int, n: int) -> dict:
+    """Alg. 2 over the whole population: ancestors a (N) and boundary distances."""
+    lw = np.ascontiguousarray(lw, dtype=np.float64)
+    N = lw.shape[0]
+    a = np.zeros(N, np.int64)
+    delta = np.zeros(N, np.float32)
+    rc = lib().orc_multinomial(N, seed, n, _ptr(lw), _ptr(a), _ptr(delta))
+    if rc != 0:
+        raise ValueError(f"orc_multinomial rc={rc}")
+    return dict(a=a, delta=delta)
+
+
+def step_multinomial(params: dict, N: int, seed: int, n: int, y: np.ndarray, xin: np.ndarray) -> dict:
+    mdl = make_model(params)
+    d = mdl.d
+    xin = np.ascontiguousarray(xin, dtype=np.float32).reshape(N, d)
+    yy = np.ascontiguousarray(y, dtype=np.float32)
+    out = dict(x=np.zeros((N, d)), lw=np.zeros(N), a=np.zeros(N, np.int64), delta=np.zeros(N, np.float32),
+               xhat=np.zeros((N, d)), filter=np.zeros(2 * d), predict=np.zeros(2 * d))
+    rc = lib().orc_step_multinomial(ctypes.byref(mdl), N, seed, n, _ptr(yy), _ptr(xin), _ptr(out["x"]),
+                                    _ptr(out["lw"]), _ptr(out["a"]), _ptr(out["delta"]), _ptr(out["xhat"]),
+                                    _ptr(out["filter"]), _ptr(out["predict"]))
+    if rc != 0:
+        raise ValueError(f"orc_step_multinomial rc={rc}")
+    return out
+
+
+def run_filter_multinomial(params: dict, N: int, seed: int, ys: np.ndarray, x0: Optional[np.ndarray] = None):
+    d = int(params["d"])
+    x = (init(params, N, seed) if x0 is None else x0).astype(np.float32)
+    means = np.zeros((len(ys), d))
+    for n, y in enumerate(ys):
+        r = step_multinomial(params, N, seed, n, y, x)
         means[n] = r["filter"][:d]
         x = r["xhat"].astype(np.float32)
     return means

@@ -39,6 +39,7 @@
 #define ORC_DOMAIN_RESAMPLE 3u
 #define ORC_DOMAIN_WITHIN 4u /* AIRPF within-island draws (reading R19) */
 #define ORC_DOMAIN_ISLAND 5u /* AIRPF island side draws (reading R20) */
+#define ORC_DOMAIN_MULTI 6u  /* Alg. 2 multinomial draws (reading R22) */
 
 /* ------------------------------------------------------------------------- */
 /* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11, "Parallel random numbers:
@@ -740,5 +741,69 @@ int orc_step_airpf(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t seed, 
             uint64_t a = (uint64_t)a_w[(uint64_t)Aisl[i] * M + j];
             for (int k = 0; k < d; ++k) xhat_out[(i * M + j) * d + k] = x[a * d + k];
         }
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Alg. 2, multinomial resampling: every output i draws its source from
+ * all N particles with probability g_j / sum g.  Inverse CDF over the whole population in
+ * ascending order (reading R22): C_k = sum_{j<=k} e^{lw_j - L} (sequential, L = max lw),
+ * u = (r >> 8) 2^-24 from word (i & 3) of block (i >> 2, n, MULTI << 24),
+ * a(i) = #{k < N-1 : C_k <= u C_{N-1}}, found by bisection of the non-decreasing C (the
+ * count, pinned against the literal count in tests); delta = distance of u to the nearest
+ * C_k / C_{N-1}. */
+int orc_multinomial(uint64_t N, uint64_t seed, uint32_t n, const double* lw, int64_t* a, float* delta)
+{
+    if (N == 0) return ORC_EINVAL;
+    double* C = (double*)malloc(sizeof(double) * N);
+    if (!C) return ORC_ENOMEM;
+    double L = -INFINITY;
+    for (uint64_t j = 0; j < N; ++j)
+        if (lw[j] > L) L = lw[j];
+    double acc = 0.0;
+    for (uint64_t j = 0; j < N; ++j) {
+        acc += (L == -INFINITY) ? 1.0 : exp(lw[j] - L);
+        C[j] = acc;
+    }
+    const double total = C[N - 1];
+    for (uint64_t i = 0; i < N; ++i) {
+        double u = u01(rng_word(seed, (uint32_t)(i >> 2), n, ORC_DOMAIN_MULTI, 0u, (int)(i & 3u)));
+        double t = u * total;
+        /* smallest k in [0, N-1] with C_k > t, restricted to k < N-1: the count of C_k <= t */
+        uint64_t lo = 0, hi = N - 1; /* answer in [0, N-1] */
+        while (lo < hi) {
+            uint64_t mid = lo + (hi - lo) / 2;
+            if (C[mid] <= t) lo = mid + 1;
+            else hi = mid;
+        }
+        a[i] = (int64_t)lo;
+        if (delta) {
+            double d1 = (lo < N - 1) ? fabs(u - C[lo] / total) : INFINITY;
+            double d0 = (lo > 0) ? fabs(u - C[lo - 1] / total) : INFINITY;
+            delta[i] = (float)(d0 < d1 ? d0 : d1);
+        }
+    }
+    free(C);
+    return ORC_OK;
+}
+
+/* One step of Alg. 1 with Alg. 2 (rotated as orc_step). */
+int orc_step_multinomial(const orc_model* mdl, uint64_t N, uint64_t seed, uint32_t n, const float* y,
+                         const float* xin, double* x, double* lw, int64_t* a, float* delta, double* xhat_out,
+                         double* filt, double* pred)
+{
+    int d = mdl->d;
+    double* xprev = (double*)malloc(sizeof(double) * N * (uint64_t)d);
+    if (!xprev) return ORC_ENOMEM;
+    for (uint64_t i = 0; i < N * (uint64_t)d; ++i) xprev[i] = (double)xin[i];
+    if (n == 0) memcpy(x, xprev, sizeof(double) * N * (uint64_t)d);
+    else orc_mutate(mdl, N, seed, n, xprev, x);
+    free(xprev);
+    orc_logweight(mdl, N, y, x, lw);
+    orc_estimates(d, N, lw, x, NULL, filt, pred, NULL);
+    int rc = orc_multinomial(N, seed, n, lw, a, delta);
+    if (rc != ORC_OK) return rc;
+    for (uint64_t i = 0; i < N; ++i)
+        for (int k = 0; k < d; ++k) xhat_out[i * d + k] = x[(uint64_t)a[i] * d + k];
     return ORC_OK;
 }
