@@ -46,6 +46,8 @@ def parse():
                     help="ESS threshold of the fully adapted scheme (0: plain augmented resampling)")
     ap.add_argument("--airpf", type=int, default=0, choices=[0, 1, 2],
                     help="AIRPF (Alg. 4) with Alg. 7 (1) or Alg. 6 (2) instead of augmented resampling")
+    ap.add_argument("--multinomial", action="store_true",
+                    help="the plain BPF (Alg. 2, multinomial resampling) instead of augmented resampling")
     return ap.parse_args()
 
 
@@ -191,8 +193,8 @@ def ncu_traffic(cfg, kernel):
 
 
 def run_ours(args):
-    if (args.theta > 0 or args.airpf) and int(os.environ.get("WORLD_SIZE", "1")) > 1:
-        raise SystemExit("--theta / --airpf run on one GPU only")
+    if (args.theta > 0 or args.airpf or args.multinomial) and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        raise SystemExit("--theta / --airpf / --multinomial run on one GPU only")
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -216,7 +218,7 @@ def run_ours(args):
         y_dev = torch.tensor(np.asarray(ys, np.float32), device=dev)
         if world == 1:
             f = pf.ParticleFilter(params, cfg.N, cfg.M, args.seed, stream=stream, theta=args.theta,
-                                  airpf=args.airpf)
+                                  airpf=args.airpf, multinomial=args.multinomial)
 
             def step(k, yd=None):
                 f.step_dev(y_dev[k % T] if yd is None else yd)
@@ -316,7 +318,8 @@ def run_ours(args):
                                    "stages_run_hist": np.bincount(stages, minlength=cfg.S + 1).tolist()}
                                   if args.theta > 0 else {}),
                                **({"algorithm": {1: "AIRPF (Alg. 4 + 5 + 7)", 2: "AIRPF (Alg. 4 + 5 + 6)"}[args.airpf]}
-                                  if args.airpf else {})),
+                                  if args.airpf else {}),
+                               **({"algorithm": "plain BPF (Alg. 1 + 2, multinomial)"} if args.multinomial else {})),
                 "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line))

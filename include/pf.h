@@ -66,6 +66,8 @@ typedef struct pf_handle pf_handle;
 #define PF_FLAG_ADAPTIVE 2u /* reserve the buffers of the fully adapted scheme
                                (pf_set_adaptive; one GPU only): 8 N + 4 N/M + O(N/1024) bytes */
 
+#define PF_FLAG_MULTINOMIAL 8u /* reserve the buffers of multinomial resampling (pf_set_multinomial;
+                                   one GPU): 8 N bytes + O(N/1024) */
 #define PF_FLAG_AIRPF 4u /* reserve the island buffers of AIRPF (pf_set_airpf; one GPU, M >= 4):
                             13 N/M + S N/(4M) bytes */
 
@@ -122,6 +124,15 @@ int pf_last_stages(const pf_handle* h);
  * with PF_FLAG_AIRPF, world = 1, M >= 4; exclusive with pf_set_adaptive.  Errors:
  * PF_EINVAL. */
 int pf_set_airpf(pf_handle* h, int mode);
+
+/* --- plain BPF: multinomial resampling (Alg. 2) -------------------
+ * on != 0: every later pf_step resamples the N particles multinomially over the whole
+ * population (reading R22: inverse CDF in ascending order, MULTI draws) instead of running
+ * the butterfly stages -- the paper's baseline, for comparison.  The draw searches a global
+ * CDF (fp32 per 1024-particle tile, fp64 tile offsets) and gathers the states at random.
+ * Needs PF_FLAG_MULTINOMIAL, world = 1; exclusive with the other schemes.  PF_DBG_ANC_FINAL
+ * returns the drawn ancestors (debug handles).  Errors: PF_EINVAL. */
+int pf_set_multinomial(pf_handle* h, int on);
 
 /* estimates (phi) */
 #define PF_PHI_X 1  /* phi(x) = x_k, k = 0..d-1 */

@@ -199,6 +199,7 @@ struct Layout {
     size_t X0, X1, logV, thr, part, scratch, est, ticket, y;
     size_t lw0, lw1, carry_lv, ess_part, ess_chunks, ess_out, ess_lmax;  // PF_FLAG_ADAPTIVE
     size_t isl_A, isl_choice, isl_logW;                                  // PF_FLAG_AIRPF
+    size_t mn_cdf, mn_cdf32, mn_trec, mn_off;                            // PF_FLAG_MULTINOMIAL
     size_t shard_rec, recs, top_logV, top_thr, top_scratch;
     size_t dbg_x, dbg_lw, dbg_anc, dbg_A;
     size_t total;
@@ -231,13 +232,19 @@ Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags, uint32
     L.top_thr = take((size_t)world * 4);
     L.top_scratch = take((size_t)2 * world * PS * 8);
     const bool ad = flags & PF_FLAG_ADAPTIVE;
-    L.lw0 = take(ad ? N * 4 : 0);
+    const bool mn = flags & PF_FLAG_MULTINOMIAL;
+    L.lw0 = take((ad || mn) ? N * 4 : 0);
     L.lw1 = take(ad ? N * 4 : 0);
     L.carry_lv = take(ad ? (m / 2) * 8 : 0);
-    L.ess_part = take(ad ? (size_t)p.NT * 3 * 8 : 0);
+    L.ess_part = take((ad || mn) ? (size_t)p.NT * 3 * 8 : 0);
     L.ess_chunks = take(ad ? (size_t)(p.NT / kEssChunk + 2 * m / kEssChunk + 64) * 2 * 8 : 0);
     L.ess_out = take(ad ? (size_t)(S + 3) * 8 : 0);
-    L.ess_lmax = take(ad ? 16 : 0);
+    L.ess_lmax = take((ad || mn) ? 16 : 0);
+    const size_t nt_mn = (N + kMnTile - 1) / kMnTile;
+    L.mn_cdf = take(mn ? N * 4 : 0);
+    L.mn_cdf32 = take(mn ? nt_mn * (kMnTile / 32) * 4 : 0);
+    L.mn_trec = take(mn ? nt_mn * 16 : 0);
+    L.mn_off = take(mn ? (nt_mn + 1) * 8 : 0);
     const bool air = flags & PF_FLAG_AIRPF;
     L.isl_A = take(air ? m * 4 : 0);
     L.isl_choice = take(air ? (size_t)S * ((m + 3) / 4) : 0);
@@ -283,6 +290,9 @@ struct pf_handle {
     // AIRPF (pf_set_airpf)
     int airpf = 0;           // 0 off, 1 Alg. 7 (modified), 2 Alg. 6 (plain)
     bool isl_valid = false;  // X(cur) is a within-resampled sample read through the island map
+    // multinomial resampling, Alg. 2 (pf_set_multinomial)
+    bool multinomial = false;
+    bool anc_ready = false;  // dbg_A holds the ancestors of the last (multinomial) step
     // kernel timing
     bool timing;
     struct Rec {
@@ -697,8 +707,54 @@ static int run_step_airpf(pf_handle* h, const float* y_host, const float* y_dev)
     return check_cuda(h, "pf_step (AIRPF)");
 }
 
+// One step of the plain BPF (Alg. 1 with Alg. 2): k_pass1 (weigh) -> k_cascade (the
+// estimates) -> k_mn_tile_cdf -> k_mn_offsets -> k_mn_draw (search + gather).
+static int run_step_multinomial(pf_handle* h, const float* y_host, const float* y_dev) {
+    const int src = h->cur, mid = h->cur ^ 1;
+    float* lw = h->at<float>(h->lay.lw0);
+    Pass1Args a;
+    fill_pass1(h, a, y_host, y_dev);
+    a.x_in = h->X(src);
+    a.x_out = h->X(mid);
+    a.lw_out = lw;
+    a.ess_part = h->at<double>(h->lay.ess_part);
+    a.ess_lmax = h->at<unsigned int>(h->lay.ess_lmax);
+    h->mark(PF_KERNEL_PASS1, true);
+    launch_pass1(h, a, kPass1Weigh);
+    h->mark(PF_KERNEL_PASS1, false);
+    h->mark(PF_KERNEL_CASCADE, true);
+    launch_cascade_k(h);
+    h->mark(PF_KERNEL_CASCADE, false);
+    MultinomialArgs mn;
+    mn.key = make_key(h->seed);
+    mn.n = h->n;
+    mn.N = h->N;
+    mn.NT = (uint32_t)((h->N + kMnTile - 1) / kMnTile);
+    mn.cdf = h->at<float>(h->lay.mn_cdf);
+    mn.cdf32 = h->at<float>(h->lay.mn_cdf32);
+    mn.trec = h->at<double>(h->lay.mn_trec);
+    mn.off = h->at<double>(h->lay.mn_off);
+    mn.lmax = h->at<unsigned int>(h->lay.ess_lmax);
+    mn.x = h->X(mid);
+    mn.xhat = h->X(src);
+    mn.dbg_anc = (h->flags & PF_FLAG_DEBUG) ? h->at<int32_t>(h->lay.dbg_A) : nullptr;
+    h->mark(PF_KERNEL_STAGES, true);
+    launch_multinomial(h->plan.D, h->stream, mn, lw);
+    h->mark(PF_KERNEL_STAGES, false);
+    cudaMemsetAsync(h->at<unsigned int>(h->lay.ess_lmax), 0, 4, h->stream);  // running max for the next step
+    h->anc_ready = mn.dbg_anc != nullptr;
+    h->sstar_last = (int)h->S;
+    h->step_n = h->n;
+    h->n += 1;
+    h->have_step = true;
+    h->top_done = true;
+    h->last_launches = 5;
+    return check_cuda(h, "pf_step (multinomial)");
+}
+
 static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
     if (h->theta > 0.0) return run_step_adaptive(h, y_host, y_dev);
+    if (h->multinomial) return run_step_multinomial(h, y_host, y_dev);
     if (h->airpf) return run_step_airpf(h, y_host, y_dev);
     const Plan& p = h->plan;
     Pass1Args a;
@@ -773,6 +829,7 @@ static int init_core(const pf_model* model, uint64_t N, uint32_t M, uint64_t see
     if (!validate_topology(N, M, &err)) return fail(nullptr, PF_EINVAL, err);
     if (!shard_geometry(N, M, rank, world, &Nloc, &err)) return fail(nullptr, PF_EINVAL, err);
     if ((flags & PF_FLAG_ADAPTIVE) && world != 1) return fail(nullptr, PF_EINVAL, "PF_FLAG_ADAPTIVE needs world = 1");
+    if ((flags & PF_FLAG_MULTINOMIAL) && world != 1) return fail(nullptr, PF_EINVAL, "PF_FLAG_MULTINOMIAL needs world = 1");
     if ((flags & PF_FLAG_AIRPF) && (world != 1 || M < 4u))
         return fail(nullptr, PF_EINVAL, "PF_FLAG_AIRPF needs world = 1 and M >= 4");
     Plan p;
@@ -1022,6 +1079,10 @@ int pf_debug_ptr(pf_handle* h, int what, int stage, void** dev_out) {
             return PF_OK;
         case PF_DBG_ANC_FINAL: {
             if (h->world > 1) return fail(h, PF_ESTATE, "composed ancestors span shards: use the stage tables");
+            if (h->multinomial && h->anc_ready) {  // Alg. 2: the draws are the ancestors
+                *dev_out = h->at<int32_t>(h->lay.dbg_A);
+                return PF_OK;
+            }
             int32_t* A = h->at<int32_t>(h->lay.dbg_A);
             const uint32_t sc = h->sstar_last >= 0 ? (uint32_t)h->sstar_last : h->S;  // stages run
             launch_debug_compose(LaunchCfg{1024u, 256u, 0u, h->stream}, h->at<int32_t>(h->lay.dbg_anc), h->N, sc, A);
@@ -1100,7 +1161,7 @@ int pf_set_airpf(pf_handle* h, int mode) {
     if (!h) return fail(h, PF_EINVAL, "NULL handle");
     if (mode < 0 || mode > 2) return fail(h, PF_EINVAL, "mode must be 0 (off), 1 (Alg. 7) or 2 (Alg. 6)");
     if (mode && !(h->flags & PF_FLAG_AIRPF)) return fail(h, PF_EINVAL, "handle not created with PF_FLAG_AIRPF");
-    if (mode && h->theta > 0.0) return fail(h, PF_EINVAL, "AIRPF and the fully adapted scheme are exclusive");
+    if (mode && (h->theta > 0.0 || h->multinomial)) return fail(h, PF_EINVAL, "one resampling scheme at a time");
     if (!mode && h->isl_valid) {  // back to augmented resampling: materialise x_hat first
         launch_block_gather(h->stream, h->X(h->cur), h->X(h->cur ^ 1), h->at<int32_t>(h->lay.isl_A), h->N, h->b,
                             (uint32_t)h->plan.D);
@@ -1117,12 +1178,21 @@ int pf_set_adaptive(pf_handle* h, double theta) {
     if (theta > 0.0 && !(h->flags & PF_FLAG_ADAPTIVE))
         return fail(h, PF_EINVAL, "handle not created with PF_FLAG_ADAPTIVE");
     if (theta > 0.0 && h->world != 1) return fail(h, PF_EINVAL, "the fully adapted scheme needs world = 1");
-    if (theta > 0.0 && h->airpf) return fail(h, PF_EINVAL, "AIRPF and the fully adapted scheme are exclusive");
+    if (theta > 0.0 && (h->airpf || h->multinomial)) return fail(h, PF_EINVAL, "one resampling scheme at a time");
     h->theta = theta;
     if (theta == 0.0) h->carry_mode = 0;
     return PF_OK;
 }
 
 int pf_last_stages(const pf_handle* h) { return h ? h->sstar_last : -1; }
+
+int pf_set_multinomial(pf_handle* h, int on) {
+    if (!h) return fail(h, PF_EINVAL, "NULL handle");
+    if (on && !(h->flags & PF_FLAG_MULTINOMIAL)) return fail(h, PF_EINVAL, "handle not created with PF_FLAG_MULTINOMIAL");
+    if (on && (h->theta > 0.0 || h->airpf)) return fail(h, PF_EINVAL, "one resampling scheme at a time");
+    h->multinomial = on != 0;
+    h->anc_ready = false;
+    return PF_OK;
+}
 
 }  // extern "C"

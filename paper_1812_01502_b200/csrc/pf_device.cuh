@@ -18,6 +18,7 @@ constexpr uint32_t kDomainMutate = 2u;
 constexpr uint32_t kDomainResample = 3u;
 constexpr uint32_t kDomainWithin = 4u;  // AIRPF within-island draws (R19)
 constexpr uint32_t kDomainIsland = 5u;  // AIRPF island side draws (R20)
+constexpr uint32_t kDomainMulti = 6u;   // Alg. 2 multinomial draws (R22)
 
 // Offset of V level s (s >= 1) in the (m - 1)-entry level tables: level s has m / 2^s
 // entries (blocks of 2^s groups).

@@ -288,6 +288,24 @@ struct IslandArgs {
 };
 
 // -------------------------------------------------------------------------------------
+// Multinomial resampling, Alg. 2 (kernels in pf_multinomial.cu).
+constexpr uint32_t kMnTile = 1024;  // particles per CDF tile (one CTA of 1024 threads)
+
+struct MultinomialArgs {
+    Key key;
+    uint32_t n, NT;              // NT: CDF tiles of kMnTile particles
+    uint64_t N;
+    float* cdf;                  // N: per-tile local CDFs
+    float* cdf32;                // N / 32: the local CDF at every 32nd particle (chunk ends)
+    double* trec;                // NT x {tile max, tile total}
+    double* off;                 // NT + 1: tile offsets in the global CDF, off[NT] = C
+    const unsigned int* lmax;    // max lw (order-preserving bits; from the weigh pass)
+    const float* x;              // x_n (N x d)
+    float* xhat;                 // x_hat_n (N x d)
+    int32_t* dbg_anc;            // ancestors (debug) or nullptr
+};
+
+// -------------------------------------------------------------------------------------
 template <typename T>
 struct __align__(4 * sizeof(T) <= 16 ? 4 * sizeof(T) : 16) Vec4 {
     T v[4];

@@ -23,6 +23,7 @@ PF_LG, PF_SV = 1, 2
 PF_FLAG_DEBUG = 1
 PF_FLAG_ADAPTIVE = 2
 PF_FLAG_AIRPF = 4
+PF_FLAG_MULTINOMIAL = 8
 PF_PHI_X, PF_PHI_X2 = 1, 2
 PF_EST_FILTER, PF_EST_PREDICT = 1, 2
 PF_DBG_X, PF_DBG_LOGW, PF_DBG_ANC_STAGE, PF_DBG_ANC_FINAL, PF_DBG_XHAT, PF_DBG_LOGV, PF_DBG_THRESH = 1, 2, 3, 4, 5, 6, 7
@@ -84,6 +85,7 @@ def lib() -> ctypes.CDLL:
         L.pf_set_adaptive.argtypes = [vp, ctypes.c_double]
         L.pf_last_stages.argtypes = [vp]
         L.pf_set_airpf.argtypes = [vp, ctypes.c_int]
+        L.pf_set_multinomial.argtypes = [vp, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -92,7 +94,7 @@ EXPORTED = ["pf_workspace_bytes", "pf_init", "pf_step", "pf_step_dev", "pf_estim
             "pf_last_error", "pf_debug_get", "pf_debug_ptr", "pf_debug_set_state", "pf_last_step_launches",
             "pf_timing_enable", "pf_timing_read", "pf_workspace_bytes_sharded", "pf_init_sharded",
             "pf_step_local", "pf_shard_record", "pf_step_top", "pf_cross_buffer", "pf_cross_stage",
-            "pf_set_adaptive", "pf_last_stages", "pf_set_airpf"]
+            "pf_set_adaptive", "pf_last_stages", "pf_set_airpf", "pf_set_multinomial"]
 PF_KERNEL_KINDS = 5
 KERNEL_NAMES = ("k_pass1", "k_cascade", "k_stages", "k_top", "k_cross")
 
@@ -166,6 +168,10 @@ def pf_set_airpf(h, mode: int):
     _check(lib().pf_set_airpf(h, int(mode)), h)
 
 
+def pf_set_multinomial(h, on: bool):
+    _check(lib().pf_set_multinomial(h, 1 if on else 0), h)
+
+
 def pf_last_stages(h) -> int:
     return int(lib().pf_last_stages(h))
 
@@ -179,10 +185,11 @@ class ParticleFilter:
     """One filter on one GPU: workspace in a torch uint8 tensor, work on a torch stream."""
 
     def __init__(self, params: dict, N: int, M: int, seed: int, debug: bool = False, device: str = "cuda",
-                 stream=None, theta: float = 0.0, airpf: int = 0):
+                 stream=None, theta: float = 0.0, airpf: int = 0, multinomial: bool = False):
         """theta > 0: fully adapted augmented resampling with ESS threshold theta
-        (pf_set_adaptive); airpf = 1 (Alg. 7) or 2 (Alg. 6): AIRPF (pf_set_airpf).  The
-        handle then reserves the buffers of that scheme."""
+        (pf_set_adaptive); airpf = 1 (Alg. 7) or 2 (Alg. 6): AIRPF (pf_set_airpf);
+        multinomial: the plain BPF, Alg. 2 (pf_set_multinomial).  The handle then reserves
+        the buffers of that scheme."""
         import torch
 
         self.torch = torch
@@ -193,7 +200,7 @@ class ParticleFilter:
         self.m = self.N // self.M
         self.S = int(round(np.log2(self.m)))
         self.flags = ((PF_FLAG_DEBUG if debug else 0) | (PF_FLAG_ADAPTIVE if theta > 0 else 0) |
-                      (PF_FLAG_AIRPF if airpf else 0))
+                      (PF_FLAG_AIRPF if airpf else 0) | (PF_FLAG_MULTINOMIAL if multinomial else 0))
         self.device = torch.device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         nbytes = pf_workspace_bytes(params, self.N, self.M, self.flags)
@@ -209,6 +216,8 @@ class ParticleFilter:
             pf_set_adaptive(self.h, theta)
         if airpf:
             pf_set_airpf(self.h, airpf)
+        if multinomial:
+            pf_set_multinomial(self.h, True)
 
     def last_stages(self) -> int:
         """S* of the last step (S for a plain step)."""
