@@ -67,6 +67,8 @@ def lib():
         _lib.orc_step_multinomial.argtypes = [vp, u64, u64, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         _lib.orc_step_adaptive.argtypes = [vp, u64, u64, u64, u32, vp, vp, vp, ctypes.c_double, vp, vp, vp, vp,
                                            vp, vp, vp, vp, vp, vp, vp, vp]
+        _lib.orc_step_adaptive_rot.argtypes = [vp, u64, u64, u64, u32, vp, vp, vp, ctypes.c_double, ctypes.c_int,
+                                               vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     return _lib
 
 
@@ -253,8 +255,9 @@ def stages_to_run(ess: np.ndarray, theta: float) -> int:
 
 
 def step_adaptive(params: dict, N: int, M: int, seed: int, n: int, y: np.ndarray, xin: np.ndarray,
-                  lwc_in: np.ndarray, theta: float) -> dict:
-    """One step of the fully adapted filter (orc_step_adaptive)."""
+                  lwc_in: np.ndarray, theta: float, rotate: bool = False) -> dict:
+    """One step of the fully adapted filter (orc_step_adaptive_rot); rotate: stage rotation
+    (reading R23) -- xhat and lwc come back in the next step's layout."""
     mdl = make_model(params)
     d = mdl.d
     m = N // M
@@ -266,8 +269,8 @@ def step_adaptive(params: dict, N: int, M: int, seed: int, n: int, y: np.ndarray
                logV=np.zeros(m - 1), A=np.zeros(N, np.int64), xhat=np.zeros((N, d)), lwc=np.zeros(N),
                filter=np.zeros(2 * d), predict=np.zeros(2 * d), ess=np.zeros(S + 1))
     ss = ctypes.c_int(-1)
-    rc = lib().orc_step_adaptive(ctypes.byref(mdl), N, M, seed, n, _ptr(yy), _ptr(xin), _ptr(lwc), float(theta),
-                                 _ptr(out["x"]), _ptr(out["lw"]), _ptr(out["a"]), _ptr(out["delta"]),
+    rc = lib().orc_step_adaptive_rot(ctypes.byref(mdl), N, M, seed, n, _ptr(yy), _ptr(xin), _ptr(lwc),
+                                     float(theta), int(bool(rotate)), _ptr(out["x"]), _ptr(out["lw"]), _ptr(out["a"]), _ptr(out["delta"]),
                                  _ptr(out["logV"]), _ptr(out["A"]), _ptr(out["xhat"]), _ptr(out["lwc"]),
                                  _ptr(out["filter"]), _ptr(out["predict"]), _ptr(out["ess"]), ctypes.byref(ss))
     if rc != 0:
@@ -277,7 +280,7 @@ def step_adaptive(params: dict, N: int, M: int, seed: int, n: int, y: np.ndarray
 
 
 def run_filter_adaptive(params: dict, M: int, m: int, seed: int, ys: np.ndarray, theta: float,
-                        x0: Optional[np.ndarray] = None):
+                        x0: Optional[np.ndarray] = None, rotate: bool = False):
     """The fully adapted filter for len(ys) steps: per-step filter means (T x d) and the
     number of stages run at each step."""
     N = M * m
@@ -287,7 +290,7 @@ def run_filter_adaptive(params: dict, M: int, m: int, seed: int, ys: np.ndarray,
     means = np.zeros((len(ys), d))
     stages = np.zeros(len(ys), np.int32)
     for n, y in enumerate(ys):
-        r = step_adaptive(params, N, M, seed, n, y, x, lwc, theta)
+        r = step_adaptive(params, N, M, seed, n, y, x, lwc, theta, rotate)
         means[n] = r["filter"][:d]
         stages[n] = r["sstar"]
         x = r["xhat"].astype(np.float32)

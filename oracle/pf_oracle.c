@@ -555,11 +555,42 @@ int orc_stages_to_run(int S, const double* ess, double theta)
  *   lwc_out[i] = lw[i] - log V_S                    (S* = 0),
  * i.e. shifted by the global constant log V_S = log N^-1 sum w, which changes no
  * normalised quantity (reading R18).  Outputs as orc_step plus ess[S+1], *sstar. */
+int orc_step_adaptive_rot(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t seed, uint32_t n,
+                          const float* y, const float* xin, const double* lwc_in, double theta, int rotate,
+                          double* x, double* lw, int32_t* a, float* delta, double* logV, int64_t* A,
+                          double* xhat_out, double* lwc_out, double* filt, double* pred, double* ess,
+                          int* sstar);
+
+/* Stage rotation: the next step starts at the stage after the last one
+ * executed.  Realised as a relabelling of the groups (reading R23): the particle arrays
+ * are kept in the current layout, where the stage at position t pairs bit t-1 of the
+ * layout group index g' = rotr_S(g, rho) (g the natural group, rho the rotation offset);
+ * after a step that ran S* >= 1 stages, rho += S* and the outputs move to the next
+ * layout, group g' -> rotr_S(g', S*).  All draws are keyed by layout positions.  rotate =
+ * 0 leaves the layout fixed (every step starts at stage 1). */
+static uint64_t rotr_bits(uint64_t g, int k, int S)
+{
+    k %= S;
+    if (k == 0) return g;
+    uint64_t mask = (S >= 64) ? ~0ull : ((1ull << S) - 1);
+    return ((g >> k) | (g << (S - k))) & mask;
+}
+
 int orc_step_adaptive(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t seed, uint32_t n,
                       const float* y, const float* xin, const double* lwc_in, double theta,
                       double* x, double* lw, int32_t* a, float* delta, double* logV, int64_t* A,
                       double* xhat_out, double* lwc_out, double* filt, double* pred, double* ess,
                       int* sstar)
+{
+    return orc_step_adaptive_rot(mdl, N, M, seed, n, y, xin, lwc_in, theta, 0, x, lw, a, delta, logV, A, xhat_out,
+                                 lwc_out, filt, pred, ess, sstar);
+}
+
+int orc_step_adaptive_rot(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t seed, uint32_t n,
+                          const float* y, const float* xin, const double* lwc_in, double theta, int rotate,
+                          double* x, double* lw, int32_t* a, float* delta, double* logV, int64_t* A,
+                          double* xhat_out, double* lwc_out, double* filt, double* pred, double* ess,
+                          int* sstar)
 {
     int d = mdl->d;
     uint64_t m = N / M;
@@ -593,6 +624,24 @@ int orc_step_adaptive(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t see
             for (uint64_t i = 0; i < N; ++i)
                 lwc_out[i] = (ss == 0) ? lw[i] - lvS : lvl[level_offset(m, ss) + ((i / M) >> ss)] - lvS;
             orc_estimates(d, N, lw, x, Aloc, filt, pred, NULL);
+            if (rotate && ss >= 1 && (ss % S) != 0) {  /* move to the next layout (R23) */
+                double* tx = (double*)malloc(sizeof(double) * N * (uint64_t)d);
+                double* tc = (double*)malloc(sizeof(double) * N);
+                if (!tx || !tc) {
+                    free(tx); free(tc);
+                    rc = ORC_ENOMEM;
+                } else {
+                    for (uint64_t i = 0; i < N; ++i) {
+                        uint64_t g = i / M, j = i % M;
+                        uint64_t dst = rotr_bits(g, ss, S) * M + j;
+                        for (int k = 0; k < d; ++k) tx[dst * d + k] = xhat_out[i * d + k];
+                        tc[dst] = lwc_out[i];
+                    }
+                    memcpy(xhat_out, tx, sizeof(double) * N * (uint64_t)d);
+                    memcpy(lwc_out, tc, sizeof(double) * N);
+                    free(tx); free(tc);
+                }
+            }
         }
     }
     free(xprev); free(Aloc); free(lvl);
