@@ -46,6 +46,8 @@ def parse():
                     help="ESS threshold of the fully adapted scheme (0: plain augmented resampling)")
     ap.add_argument("--airpf", type=int, default=0, choices=[0, 1, 2],
                     help="AIRPF (Alg. 4) with Alg. 7 (1) or Alg. 6 (2) instead of augmented resampling")
+    ap.add_argument("--rotate", action="store_true",
+                    help="with --theta: stage rotation (PAPER.md:1309)")
     ap.add_argument("--multinomial", action="store_true",
                     help="the plain BPF (Alg. 2, multinomial resampling) instead of augmented resampling")
     return ap.parse_args()
@@ -218,7 +220,7 @@ def run_ours(args):
         y_dev = torch.tensor(np.asarray(ys, np.float32), device=dev)
         if world == 1:
             f = pf.ParticleFilter(params, cfg.N, cfg.M, args.seed, stream=stream, theta=args.theta,
-                                  airpf=args.airpf, multinomial=args.multinomial)
+                                  airpf=args.airpf, multinomial=args.multinomial, rotate=args.rotate)
 
             def step(k, yd=None):
                 f.step_dev(y_dev[k % T] if yd is None else yd)
@@ -314,7 +316,8 @@ def run_ours(args):
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": dict(config_dict(cfg, world, "single" if world == 1 else f"groups sharded over {world} GPUs"),
-                               **({"theta": args.theta, "stages_run_mean": float(np.mean(stages)),
+                               **({"theta": args.theta, "stage_rotation": bool(args.rotate),
+                                   "stages_run_mean": float(np.mean(stages)),
                                    "stages_run_hist": np.bincount(stages, minlength=cfg.S + 1).tolist()}
                                   if args.theta > 0 else {}),
                                **({"algorithm": {1: "AIRPF (Alg. 4 + 5 + 7)", 2: "AIRPF (Alg. 4 + 5 + 6)"}[args.airpf]}

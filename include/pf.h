@@ -114,6 +114,17 @@ int pf_set_adaptive(pf_handle* h, double theta);
 /* S* of the last completed step (S for a plain step), or -1 before the first step. */
 int pf_last_stages(const pf_handle* h);
 
+/* Stage rotation with the fully adapted scheme: on != 0 makes every later
+ * adaptive step start at the stage after the last one executed.  Realised as a group
+ * relabelling (reading R23): the states live in a layout whose group index is
+ * rotr_S(g, rho); a step that ran S* >= 1 stages writes its outputs to the next layout
+ * (rho += S*).  Estimates are unaffected; debug tables of a step are in its own layout and
+ * x_hat in the next one.  Needs PF_FLAG_ADAPTIVE and M >= 4.  Errors: PF_EINVAL. */
+int pf_set_rotation(pf_handle* h, int on);
+
+/* Current rotation offset rho (0 without rotation), or -1 for NULL. */
+int pf_rotation_offset(const pf_handle* h);
+
 /* --- AIRPF: augmented island resampling particle filter (Alg. 4) ---
  * mode 1: Alg. 4 with the within-island resample (Alg. 5) and the modified augmented
  * island resampling (Alg. 7: pure pairwise exchanges undone); mode 2: with Alg. 6; 0: back

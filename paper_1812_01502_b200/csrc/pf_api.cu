@@ -292,6 +292,9 @@ struct pf_handle {
     bool isl_valid = false;  // X(cur) is a within-resampled sample read through the island map
     // multinomial resampling, Alg. 2 (pf_set_multinomial)
     bool multinomial = false;
+    bool rotate = false;     // stage rotation with the fully adapted scheme (pf_set_rotation)
+    uint32_t carry_mask = 0xffffffffu;
+    uint32_t rho = 0;        // current rotation offset (bookkeeping for pf_last_stages users)
     bool anc_ready = false;  // dbg_A holds the ancestors of the last (multinomial) step
     // kernel timing
     bool timing;
@@ -494,7 +497,7 @@ static void launch_cascade_k(pf_handle* h) {
     launch_cascade(p.D, LaunchCfg{p.cascade_grid, (uint32_t)kCascadeThreads, 0u, h->stream}, c);
 }
 
-static void launch_stages_k(pf_handle* h, const StagePass& cp, const void* pin, void* pout) {
+static void launch_stages_k(pf_handle* h, const StagePass& cp, const void* pin, void* pout, uint32_t out_rot = 0u) {
     StageArgs a;
     a.key = make_key(h->seed);
     a.n = h->n;
@@ -508,6 +511,8 @@ static void launch_stages_k(pf_handle* h, const StagePass& cp, const void* pin, 
     a.P = cp.P;
     a.lowbits = cp.s0 - 1;
     a.pipe = cp.pipe;
+    a.out_rot = out_rot;
+    a.out_S = h->S;
     a.pin = pin;
     a.pout = pout;
     a.thr = h->at<uint32_t>(h->lay.thr);
@@ -569,6 +574,8 @@ static void fill_pass1(pf_handle* h, Pass1Args& a, const float* y_host, const fl
     a.ess_lmax = nullptr;
     a.isl_src = nullptr;
     a.logW = nullptr;
+    a.carry_mask = 0xffffffffu;
+    a.out_rot = 0u;
 }
 
 // One step of the fully adapted scheme (include/pf.h pf_set_adaptive; R17/R18):
@@ -587,6 +594,7 @@ static int run_step_adaptive(pf_handle* h, const float* y_host, const float* y_d
     a.carry_lw = h->at<float>(h->lwi ? h->lay.lw0 : h->lay.lw1);
     a.carry_lv = h->at<double>(h->lay.carry_lv);
     a.carry_shift = h->carry_shift;
+    a.carry_mask = h->carry_mask;
     a.carry_c = h->carry_c;
     a.ess_part = h->at<double>(h->lay.ess_part);
     a.ess_lmax = h->at<unsigned int>(h->lay.ess_lmax);
@@ -618,6 +626,8 @@ static int run_step_adaptive(pf_handle* h, const float* y_host, const float* y_d
     const double lvS = tail[1];
 
     int xs = mid;  // buffer holding the current states
+    // stage rotation (R23): the last kernel of the step writes the next layout
+    const uint32_t rot = (h->rotate && ss >= 1u && ss < h->S) ? ss : 0u;
     if (ss >= 1u) {
         Pass1Args r;
         fill_pass1(h, r, y_host, y_dev);
@@ -626,6 +636,7 @@ static int run_step_adaptive(pf_handle* h, const float* y_host, const float* y_d
         r.x_out = h->X(mid ^ 1);
         r.lw_in = lw;
         r.k1 = std::min(p.k1, ss);
+        r.out_rot = (ss <= p.k1) ? rot : 0u;
         h->mark(PF_KERNEL_PASS1, true);
         launch_pass1(h, r, kPass1Resample);
         h->mark(PF_KERNEL_PASS1, false);
@@ -633,21 +644,27 @@ static int run_step_adaptive(pf_handle* h, const float* y_host, const float* y_d
         xs = mid ^ 1;
         for (const StagePass& sp : p.passes) {
             if (sp.s0 > ss) break;
-            const StagePass q = stage_pass_for(h, sp, std::min(sp.k, ss - sp.s0 + 1u));
+            const uint32_t kk = std::min(sp.k, ss - sp.s0 + 1u);
+            const StagePass q = stage_pass_for(h, sp, kk);
+            const bool last = sp.s0 + kk - 1u == ss;
             h->mark(PF_KERNEL_STAGES, true);
-            launch_stages_k(h, q, h->X(xs), h->X(xs ^ 1));
+            launch_stages_k(h, q, h->X(xs), h->X(xs ^ 1), last ? rot : 0u);
             h->mark(PF_KERNEL_STAGES, false);
             xs ^= 1;
             ++launches;
         }
     }
+    if (rot) h->rho = (h->rho + rot) % h->S;
     // weights carried into the next step (R18)
     if (ss == 0u) {
         h->carry_mode = 1;  // lw of this step, in buffer lwi (the next weigh pass writes the other)
         h->lwi ^= 1;
     } else if (ss < h->S) {
         h->carry_mode = 2;
-        h->carry_shift = ss;
+        // block of level S* containing group g: g >> S* in this layout; after the rotation
+        // by S* bits the same block is the low S - S* bits of the new group index
+        h->carry_shift = rot ? 0u : ss;
+        h->carry_mask = rot ? ((1u << (h->S - ss)) - 1u) : 0xffffffffu;
         cudaMemcpyAsync(h->at<double>(h->lay.carry_lv), h->at<double>(h->lay.logV) + level_offset(h->m, (int)ss),
                         (size_t)(h->m >> ss) * 8, cudaMemcpyDeviceToDevice, h->stream);
     } else {
@@ -1185,6 +1202,16 @@ int pf_set_adaptive(pf_handle* h, double theta) {
 }
 
 int pf_last_stages(const pf_handle* h) { return h ? h->sstar_last : -1; }
+
+int pf_set_rotation(pf_handle* h, int on) {
+    if (!h) return fail(h, PF_EINVAL, "NULL handle");
+    if (on && (!(h->flags & PF_FLAG_ADAPTIVE) || h->M < 4u))
+        return fail(h, PF_EINVAL, "stage rotation needs PF_FLAG_ADAPTIVE and M >= 4");
+    h->rotate = on != 0;
+    return PF_OK;
+}
+
+int pf_rotation_offset(const pf_handle* h) { return h ? (int)h->rho : -1; }
 
 int pf_set_multinomial(pf_handle* h, int on) {
     if (!h) return fail(h, PF_EINVAL, "NULL handle");

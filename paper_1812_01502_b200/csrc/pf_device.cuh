@@ -20,6 +20,14 @@ constexpr uint32_t kDomainWithin = 4u;  // AIRPF within-island draws (DESIGN.md 
 constexpr uint32_t kDomainIsland = 5u;  // AIRPF island side draws (R20)
 constexpr uint32_t kDomainMulti = 6u;   // Alg. 2 multinomial draws (R22)
 
+// Stage rotation (R23): group g of the current layout lands in group
+// rotr_S(g, k) of the next one.
+__host__ __device__ inline uint32_t rotr_group(uint32_t g, uint32_t k, uint32_t S) {
+    if (k == 0u || S == 0u) return g;
+    const uint32_t mask = S >= 32u ? 0xffffffffu : ((1u << S) - 1u);
+    return ((g >> k) | (g << (S - k))) & mask;
+}
+
 // Offset of V level s (s >= 1) in the (m - 1)-entry level tables: level s has m / 2^s
 // entries (blocks of 2^s groups).
 __host__ __device__ inline uint64_t level_offset(uint64_t m, int s) { return m - (m >> (s - 1)); }

@@ -79,7 +79,10 @@ struct Pass1Args {
     int carry_mode;         // 0 none, 1 particle carry lw_prev[i] - c, 2 block carry lvl[g >> shift] - c
     const float* carry_lw;  // previous step's lw (carry_mode 1)
     const double* carry_lv; // previous step's level-S* values (carry_mode 2)
-    uint32_t carry_shift;   // S* of the previous step (carry_mode 2)
+    uint32_t carry_shift;   // block index of group g: (g >> carry_shift) & carry_mask (carry_mode 2)
+    uint32_t carry_mask;
+    uint32_t out_rot;       // stage rotation (R23): the tile is written to the next layout,
+                            // group g -> rotr_S(g, out_rot); 0 = no move (needs M >= 4)
     double carry_c;         // log V_S of the previous step
     double* ess_part;       // kPass1Weigh: per tile {max lw, sum e^{lw-max}, sum e^{2(lw-max)}}
     unsigned int* ess_lmax; // kPass1Weigh: running max of lw (order-preserving float bits)
@@ -235,7 +238,8 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : 1) 
                 } else {
 #pragma unroll
                     for (int e = 0; e < 4; ++e)
-                        cw[e] = (float)(__ldg(a.carry_lv + ((((uint64_t)a.pos0 + i0 + e) >> b) >> a.carry_shift)) - a.carry_c);
+                        cw[e] = (float)(__ldg(a.carry_lv + (((((uint64_t)a.pos0 + i0 + e) >> b) >> a.carry_shift) &
+                                                            a.carry_mask)) - a.carry_c);
                 }
 #pragma unroll
                 for (int e = 0; e < 4; ++e) lw[it][e] += cw[e];
@@ -575,9 +579,11 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : 1) 
                 }
             }
         }
+        uint32_t dst = base + 4u * q;
+        if (a.out_rot) dst = (rotr_group(dst >> b, a.out_rot, a.S) << b) | (dst & (M - 1u));
 #pragma unroll
         for (int c = 0; c < D; ++c)
-            reinterpret_cast<float4*>(a.x_out + (uint64_t)(base + 4u * q) * D)[c] =
+            reinterpret_cast<float4*>(a.x_out + (uint64_t)dst * D)[c] =
                 make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
     }
     }

@@ -35,6 +35,8 @@ struct StageArgs {
     uint32_t pos0;  // global index of the shard's first particle (RNG counters)
     uint32_t m, M, b, s0, k, P, lowbits;
     uint32_t pipe;        // 1: software-pipelined (two buffers of everything); 0: one buffer
+    uint32_t out_rot;     // stage rotation (R23): outputs go to group rotr_S(g, out_rot)
+    uint32_t out_S;       //   of the next layout (0: no move; needs M >= 4)
     const void* pin;      // states at stage s0-1 (packed AoS, shard-local)
     void* pout;           // states at stage s0+k-1
     const uint32_t* thr;  // side thresholds, level-table layout (level_offset)
@@ -249,8 +251,9 @@ __device__ __forceinline__ void stage_walk(const StageArgs& a, const StageTile& 
 #pragma unroll
         for (int e = 0; e < 4; ++e) v.v[e] = xs[tp[e]];
         const uint32_t j = l0 >> b;
-        const uint32_t gp0 = ((g.tlo | (j << lowbits) | g.thi) << b) | (l0 & mask);
+        uint32_t gp0 = ((g.tlo | (j << lowbits) | g.thi) << b) | (l0 & mask);
         if (M >= 4u) {
+            if (a.out_rot) gp0 = (rotr_group(gp0 >> b, a.out_rot, a.out_S) << b) | (gp0 & mask);
             *reinterpret_cast<Vec4<T>*>(pout + gp0) = v;
         } else {
             const uint32_t gp1 = (g.tlo | ((j + 1u) << lowbits) | g.thi) << 1;

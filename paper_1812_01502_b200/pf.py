@@ -86,6 +86,8 @@ def lib() -> ctypes.CDLL:
         L.pf_last_stages.argtypes = [vp]
         L.pf_set_airpf.argtypes = [vp, ctypes.c_int]
         L.pf_set_multinomial.argtypes = [vp, ctypes.c_int]
+        L.pf_set_rotation.argtypes = [vp, ctypes.c_int]
+        L.pf_rotation_offset.argtypes = [vp]
         _lib = L
     return _lib
 
@@ -94,7 +96,8 @@ EXPORTED = ["pf_workspace_bytes", "pf_init", "pf_step", "pf_step_dev", "pf_estim
             "pf_last_error", "pf_debug_get", "pf_debug_ptr", "pf_debug_set_state", "pf_last_step_launches",
             "pf_timing_enable", "pf_timing_read", "pf_workspace_bytes_sharded", "pf_init_sharded",
             "pf_step_local", "pf_shard_record", "pf_step_top", "pf_cross_buffer", "pf_cross_stage",
-            "pf_set_adaptive", "pf_last_stages", "pf_set_airpf", "pf_set_multinomial"]
+            "pf_set_adaptive", "pf_last_stages", "pf_set_airpf", "pf_set_multinomial", "pf_set_rotation",
+            "pf_rotation_offset"]
 PF_KERNEL_KINDS = 5
 KERNEL_NAMES = ("k_pass1", "k_cascade", "k_stages", "k_top", "k_cross")
 
@@ -172,6 +175,10 @@ def pf_set_multinomial(h, on: bool):
     _check(lib().pf_set_multinomial(h, 1 if on else 0), h)
 
 
+def pf_set_rotation(h, on: bool):
+    _check(lib().pf_set_rotation(h, 1 if on else 0), h)
+
+
 def pf_last_stages(h) -> int:
     return int(lib().pf_last_stages(h))
 
@@ -185,11 +192,12 @@ class ParticleFilter:
     """One filter on one GPU: workspace in a torch uint8 tensor, work on a torch stream."""
 
     def __init__(self, params: dict, N: int, M: int, seed: int, debug: bool = False, device: str = "cuda",
-                 stream=None, theta: float = 0.0, airpf: int = 0, multinomial: bool = False):
+                 stream=None, theta: float = 0.0, airpf: int = 0, multinomial: bool = False,
+                 rotate: bool = False):
         """theta > 0: fully adapted augmented resampling with ESS threshold theta
         (pf_set_adaptive); airpf = 1 (Alg. 7) or 2 (Alg. 6): AIRPF (pf_set_airpf);
-        multinomial: the plain BPF, Alg. 2 (pf_set_multinomial).  The handle then reserves
-        the buffers of that scheme."""
+        multinomial: the plain BPF, Alg. 2 (pf_set_multinomial); rotate (with theta): stage
+        rotation (pf_set_rotation).  The handle then reserves the buffers of that scheme."""
         import torch
 
         self.torch = torch
@@ -214,10 +222,15 @@ class ParticleFilter:
         self.h = pf_init(params, self.N, self.M, self.seed, self.flags, self.ws_ptr, nbytes, self.stream.cuda_stream)
         if theta > 0:
             pf_set_adaptive(self.h, theta)
+            if rotate:
+                pf_set_rotation(self.h, True)
         if airpf:
             pf_set_airpf(self.h, airpf)
         if multinomial:
             pf_set_multinomial(self.h, True)
+
+    def rotation_offset(self) -> int:
+        return int(lib().pf_rotation_offset(self.h))
 
     def last_stages(self) -> int:
         """S* of the last step (S for a plain step)."""

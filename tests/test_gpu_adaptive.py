@@ -37,7 +37,12 @@ def _snap(f, d):
     return out
 
 
-def _check(g, o, N, d):
+def _rotr(g, k, S):
+    k %= S
+    return ((g >> k) | (g << (S - k))) & ((1 << S) - 1) if k else g
+
+
+def _check(g, o, N, d, M=None, rotate=False):
     assert g["ss"] == o["sstar"], (g["ss"], o["sstar"], g["ess"], o["ess"])
     assert np.allclose(g["ess"], o["ess"], rtol=2e-5, atol=0), (g["ess"], o["ess"])
     pu.check_x(g["x"], o["x"])
@@ -51,7 +56,12 @@ def _check(g, o, N, d):
     else:
         flagged = np.zeros(N, bool)
         assert np.array_equal(g["A"], np.arange(N))
-    assert np.array_equal(g["xhat"].reshape(N, d), g["x"].reshape(N, d)[g["A"]], equal_nan=True)
+    xh = g["xhat"].reshape(N, d)
+    if rotate and 1 <= ss < o["S"]:  # x_hat is in the next layout: group g -> rotr_S(g, S*)
+        pos = np.arange(N)
+        dst = np.array([_rotr(int(p // M), ss, o["S"]) for p in pos]) * M + pos % M
+        xh = xh[dst]
+    assert np.array_equal(xh, g["x"].reshape(N, d)[g["A"]], equal_nan=True)
     pu.check_estimate(g["filt"], o["filter"][:d], o["filter"][d:])
     pu.check_estimate(g["pred"], o["predict"][:d], o["predict"][d:])
     return int(flagged.sum())
@@ -181,3 +191,35 @@ def test_adaptive_errors():
     g.step(np.array([0.1], np.float32))
     assert g.last_stages() == g.S
     g.close()
+
+
+@pytest.mark.parametrize("target,cfg_name,N,M", [(2, "C4", 1 << 14, 16), (7, "C4", 1 << 16, 64), (3, "C1", 1024, 16)])
+def test_rotation_two_steps(orc, target, cfg_name, N, M):
+    """Stage rotation (R23): step 1 stops at S* = target and writes the next
+    layout (k_pass1 for S* <= k1, the last k_stages pass otherwise); step 2 runs in that
+    layout with the rotated block carry and must agree with the oracle's rotated run."""
+    cfg = inputs.CONFIGS[cfg_name]
+    params = inputs.model_params(cfg)
+    d = int(params["d"])
+    S = int(np.log2(N // M))
+    xhat = inputs.particle_cloud(cfg, N, 12)
+    y1 = inputs.observation_for_step(cfg, 21, outlier_sigma=2.5)
+    y2 = inputs.observation_for_step(cfg, 22, outlier_sigma=1.0)
+    th = _theta_for(orc, params, N, M, 4, 2, xhat, y1, np.zeros(N), target)
+    assert th is not None
+    o1 = orc.step_adaptive(params, N, M, 4, 2, y1, xhat, np.zeros(N), th, rotate=True)
+    assert o1["sstar"] == target < S
+    f = pfb.ParticleFilter(params, N, M, 4, debug=True, theta=th, rotate=True)
+    f.set_state(xhat, 2)
+    f.step(y1)
+    g1 = _snap(f, d)
+    assert f.rotation_offset() == target % S
+    flagged = _check(g1, o1, N, d, M, rotate=True)
+    if flagged:
+        pytest.skip("a boundary draw in step 1: the two sides hold different particles")
+    pu.check_x(g1["xhat"], o1["xhat"])  # same particles, same (next) layout
+    o2 = orc.step_adaptive(params, N, M, 4, 3, y2, o1["xhat"].astype(np.float32), o1["lwc"], th, rotate=True)
+    f.step(y2)
+    g2 = _snap(f, d)
+    f.close()
+    _check(g2, o2, N, d, M, rotate=True)
