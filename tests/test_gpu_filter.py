@@ -106,3 +106,42 @@ def test_init_distribution():
     f.close()
     assert np.all(np.abs(m1) < 5 / np.sqrt(N))
     assert np.all(np.abs(m2 - 1.0) < 5 * np.sqrt(2.0 / N))
+
+
+def _rmse_end(params, ys, km, N, M, J, seed0, **kw):
+    errs = []
+    for j in range(J):
+        f = pfb.ParticleFilter(params, N, M, seed0 + j, **kw)
+        for y in ys:
+            f.step(y)
+        errs.append(f.estimate()[0] - km[-1, 0])
+        f.close()
+    return float(np.sqrt(np.mean(np.square(errs))))
+
+
+def test_theorem1_rate_on_gpu():
+    """Theorem 1 on the CUDA path: at fixed m the error of the filter
+    mean decays as M^-1/2 (log-log slope -0.5 +- 0.1 over M = 16 .. 4096)."""
+    cfg = inputs.CONFIGS["C1"]
+    p = inputs.model_params(cfg)
+    _, ys = inputs.simulate(cfg, T=8)
+    km, _ = kalman.kalman_filter(p["A"], p["Q"], p["H"], p["R"], p["m0"], p["P0"], ys)
+    m = 16
+    Ms = [16, 64, 256, 1024, 4096]
+    rmse = [_rmse_end(p, ys, km, m * M, M, J=160, seed0=20000 + 1000 * i) for i, M in enumerate(Ms)]
+    slope = np.polyfit(np.log(Ms), np.log(rmse), 1)[0]
+    assert -0.6 < slope < -0.4, (slope, rmse)
+
+
+@pytest.mark.parametrize("kw", [dict(airpf=1), dict(theta=0.5), dict(theta=0.5, rotate=True), dict(multinomial=True)])
+def test_variant_rates_on_gpu(kw):
+    """The next-row variants converge at the Monte Carlo rate too (fixed m, M = 64 .. 4096)."""
+    cfg = inputs.CONFIGS["C1"]
+    p = inputs.model_params(cfg)
+    _, ys = inputs.simulate(cfg, T=8)
+    km, _ = kalman.kalman_filter(p["A"], p["Q"], p["H"], p["R"], p["m0"], p["P0"], ys)
+    m = 16
+    Ms = [64, 512, 4096]
+    rmse = [_rmse_end(p, ys, km, m * M, M, J=120, seed0=40000 + 1000 * i, **kw) for i, M in enumerate(Ms)]
+    slope = np.polyfit(np.log(Ms), np.log(rmse), 1)[0]
+    assert -0.65 < slope < -0.35, (kw, slope, rmse)
