@@ -184,14 +184,28 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(cfg, kernel):
+def ncu_traffic(cfg, kernel, what=""):
+    """Per-launch ncu figure recorded by tools/ncu_traffic.py: DRAM bytes (what = "") or
+    issued warp instructions (what = ":warp_inst"); None when not captured."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             tr = json.load(f)
-        return tr[f"{cfg.name}:N={cfg.N}:M={cfg.M}"][kernel]
+        return tr[f"{cfg.name}:N={cfg.N}:M={cfg.M}{what}"][kernel]
     except (OSError, KeyError, ValueError):
         return None
+
+
+def issue_peak():
+    """Warp instructions per second the SMs can issue: 148 SMs x 4 schedulers x SM clock
+    (one warp instruction per scheduler per cycle; B200_PROFILING.md unit counts)."""
+    mhz = 1965.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", mhz))
+    except (OSError, ValueError):
+        pass
+    return 148 * 4 * mhz * 1e6
 
 
 def run_ours(args):
@@ -278,12 +292,25 @@ def run_ours(args):
         alg = algorithmic_bytes(cfg_loc, dom)
         achieved = alg / (dom_ms / dom_n / 1e3) / 1e9
         peak, peak_src = measured_peak()
+        plain = not (args.theta or args.airpf or args.multinomial)  # the ncu figures are the plain step's
         roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4), "traffic": ncu_traffic(cfg, dom),
+                    "frac": round(achieved / peak, 4), "traffic": ncu_traffic(cfg, dom) if plain else None,
                     "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
                     "kernel_share_of_step": round(dom_ms / max(sum(v[0] for v in kt.values()), 1e-9), 3),
                     "step_alg_bytes_frac": round(value / world * 8 * cfg.d / 1e9 / peak, 4)}
         kernels = {k: {"ms_per_launch": round(v[0] / max(v[1], 1), 4), "launches": v[1]} for k, v in kt.items()}
+        # per kernel: HBM fraction (algorithmic bytes) and issue fraction (ncu instruction count)
+        for k, v in kernels.items():
+            sec = v["ms_per_launch"] / 1e3
+            if sec <= 0:
+                continue
+            ab = algorithmic_bytes(cfg_loc, k)
+            if ab:
+                v["hbm_frac"] = round(ab / sec / 1e9 / peak, 4)
+            wi = ncu_traffic(cfg, k, ":warp_inst")
+            if wi is not None and plain:
+                v["issue_frac"] = round(wi / sec / issue_peak(), 4)
+        roofline["issue_frac_dominant"] = kernels.get(dom, {}).get("issue_frac")
 
         # end-to-end through the public API: pinned H2D of y_n, step, D2H of the estimate
         e2e = None
