@@ -51,18 +51,24 @@ __global__ void __launch_bounds__(kEssThreads) k_ess_chunks(const __grid_constan
 }
 
 __global__ void k_ess_final(const __grid_constant__ EssArgs a) {
-    const uint32_t s = threadIdx.x;
+    // warp s sums level s's chunk partials: lane-strided in a fixed order, then a fixed
+    // shuffle tree (deterministic)
+    const uint32_t s = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     if (s <= a.S) {
         uint32_t c0 = 0;
         for (uint32_t t = 0; t < s; ++t) c0 += (ess_level_count(a, t) + kEssChunk - 1) / kEssChunk;
         const uint32_t nc = (ess_level_count(a, s) + kEssChunk - 1) / kEssChunk;
         double s1 = 0.0, s2 = 0.0;
-        for (uint32_t c = 0; c < nc; ++c) {
+        for (uint32_t c = lane; c < nc; c += 32u) {
             s1 += a.chunks[2 * (c0 + c)];
             s2 += a.chunks[2 * (c0 + c) + 1];
         }
+        for (int o = 16; o > 0; o >>= 1) {
+            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        }
         const double units = s == 0 ? (double)a.N : (double)(a.m >> s);
-        a.out[s] = (s2 > 0.0) ? s1 * s1 / (units * s2) : 1.0;  // no weight at all: equal
+        if (lane == 0) a.out[s] = (s2 > 0.0) ? s1 * s1 / (units * s2) : 1.0;  // no weight at all: equal
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -164,7 +170,7 @@ void launch_cascade(int D, const LaunchCfg& c, const CascadeArgs& a) {
 
 void launch_ess(const LaunchCfg& chunks, const EssArgs& a) {
     k_ess_chunks<<<ess_chunks_total(a), kEssThreads, 0, chunks.stream>>>(a);
-    k_ess_final<<<1, ((a.S + 1 + 31) / 32) * 32, 0, chunks.stream>>>(a);
+    k_ess_final<<<1, 32 * (a.S + 1), 0, chunks.stream>>>(a);
 }
 
 void launch_init(int D, int kind, const LaunchCfg& c, const InitArgs& a) {
