@@ -66,3 +66,18 @@ def test_workspace_scales(pfb):
     assert 1.9 < b / a < 2.1
     dbg = pfb.pf_workspace_bytes(p, 1 << 20, 64, pfb.PF_FLAG_DEBUG)
     assert dbg > a + (1 << 20) * 14 * 4
+
+
+def test_scheme_flags_reserve_their_buffers(pfb):
+    """PF_FLAG_ADAPTIVE / _AIRPF / _MULTINOMIAL add the buffers include/pf.h states."""
+    p = inputs.model_params(inputs.CONFIGS["C4"])
+    N, M = 1 << 20, 64
+    base = pfb.pf_workspace_bytes(p, N, M)
+    ad = pfb.pf_workspace_bytes(p, N, M, pfb.PF_FLAG_ADAPTIVE)
+    air = pfb.pf_workspace_bytes(p, N, M, pfb.PF_FLAG_AIRPF)
+    mn = pfb.pf_workspace_bytes(p, N, M, pfb.PF_FLAG_MULTINOMIAL)
+    assert ad - base >= 8 * N            # two fp32 log-weight buffers
+    assert air - base >= 12 * (N // M)   # island map (int32) + island log-means (fp64)
+    assert mn - base >= 8 * N            # log-weights + tile CDFs (fp32)
+    both = pfb.pf_workspace_bytes(p, N, M, pfb.PF_FLAG_ADAPTIVE | pfb.PF_FLAG_MULTINOMIAL)
+    assert both >= max(ad, mn)
