@@ -82,7 +82,7 @@ def _theta_for(orc, params, N, M, seed, n, xhat, y, lwc, target):
 
 
 CASES = [("C1", 1024, 64, 1), ("C1", 1024, 16, 2), ("C4", 1 << 16, 64, 3), ("C4", 1 << 14, 16, 5),
-         ("C3", 1 << 16, 32, 2), ("C2", 1 << 16, 256, 1)]
+         ("C3", 1 << 16, 32, 2), ("C2", 1 << 16, 256, 1), ("C3", 1 << 14, 2, 3), ("C3", 1 << 15, 8192, 2)]
 
 
 @pytest.mark.parametrize("cfg_name,N,M,n", CASES)
