@@ -48,6 +48,8 @@ def parse():
                     help="AIRPF (Alg. 4) with Alg. 7 (1) or Alg. 6 (2) instead of augmented resampling")
     ap.add_argument("--rotate", action="store_true",
                     help="with --theta: stage rotation (PAPER.md:1309)")
+    ap.add_argument("--exchange", default="pull", choices=["pull", "pairwise"],
+                    help="N > 1: cross stages as one all-to-all pull (default) or L pairwise rounds")
     ap.add_argument("--multinomial", action="store_true",
                     help="the plain BPF (Alg. 2, multinomial resampling) instead of augmented resampling")
     return ap.parse_args()
@@ -248,7 +250,7 @@ def run_ours(args):
             tr = pfd.TorchTransport()
 
             def step(k, yd=None):
-                pfd.sharded_step(f, tr, None, y_dev[k % T] if yd is None else yd)
+                pfd.sharded_step(f, tr, None, y_dev[k % T] if yd is None else yd, exchange=args.exchange)
 
             def estimate():
                 return f.estimate(pf.PF_PHI_X, pf.PF_EST_FILTER)
@@ -342,7 +344,7 @@ def run_ours(args):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": dict(config_dict(cfg, world, "single" if world == 1 else f"groups sharded over {world} GPUs"),
+                "config": dict(config_dict(cfg, world, "single" if world == 1 else f"groups sharded over {world} GPUs, {args.exchange} exchange"),
                                **({"theta": args.theta, "stage_rotation": bool(args.rotate),
                                    "stages_run_mean": float(np.mean(stages)),
                                    "stages_run_hist": np.bincount(stages, minlength=cfg.S + 1).tolist()}

@@ -205,6 +205,27 @@ int pf_cross_buffer(pf_handle* h, const void** dev_states, size_t* bytes);
  * states.  Asynchronous. */
 int pf_cross_stage(pf_handle* h, int t, const void* dev_partner_states);
 
+/* Pull exchange: the L cross stages in one all-to-all instead of L pairwise rounds.
+ * Every output composes its L cross-stage draws (counter-based; the thresholds are known
+ * after pf_step_top) into the (owner rank, local position) of its stage-S_loc source.
+ * Sequence on every rank, after pf_step_top:
+ *   pf_cross_pull_plan(h, counts)        counts[r] = how many of my outputs read rank r
+ *                                        (HOST, G uint64; synchronises)
+ *   <exchange counts: all-to-all>        -> how many of my states each rank requests
+ *   pf_cross_pull_pack(h, offsets, &req) offsets = exclusive prefix of counts (HOST);
+ *                                        req = DEVICE uint32 local positions grouped by owner
+ *   <all-to-all of req with splits counts / received counts>
+ *   pf_cross_pull_serve(h, req_in, n, &states)  gathers the n requested stage-S_loc states
+ *                                        (DEVICE, n x d fp32, request order); n <= N
+ *   <all-to-all of states back>          -> N/G states grouped by owner, in my request order
+ *   pf_cross_pull_finish(h, states_in)   scatters them to their outputs: x_hat of the shard
+ * Gives bitwise the x_hat of the pairwise rounds (pf_cross_stage).  Errors: PF_EINVAL,
+ * PF_ESTATE (not sharded / before pf_step_top), PF_ECUDA. */
+int pf_cross_pull_plan(pf_handle* h, uint64_t* host_counts);
+int pf_cross_pull_pack(pf_handle* h, const uint64_t* host_offsets, const uint32_t** dev_requests);
+int pf_cross_pull_serve(pf_handle* h, const uint32_t* dev_requests_in, uint64_t n, const void** dev_states);
+int pf_cross_pull_finish(pf_handle* h, const void* dev_states_in);
+
 /* --- debug / test exports (parity harness) ------------------------------------ */
 #define PF_DBG_X 1         /* x_n before resampling, N x d fp32 (needs PF_FLAG_DEBUG) */
 #define PF_DBG_LOGW 2      /* log g_n(x_n^i), N fp32 (needs PF_FLAG_DEBUG) */

@@ -201,6 +201,7 @@ struct Layout {
     size_t isl_A, isl_choice, isl_logW;                                  // PF_FLAG_AIRPF
     size_t mn_cdf, mn_cdf32, mn_trec, mn_off;                            // PF_FLAG_MULTINOMIAL
     size_t shard_rec, recs, top_logV, top_thr, top_scratch;
+    size_t pull_src, pull_rank, pull_counts, pull_fill, pull_off, pull_req, pull_outpos, pull_serve;  // world > 1
     size_t dbg_x, dbg_lw, dbg_anc, dbg_A;
     size_t total;
 };
@@ -231,6 +232,15 @@ Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags, uint32
     L.top_logV = take((size_t)world * 8);
     L.top_thr = take((size_t)world * 4);
     L.top_scratch = take((size_t)2 * world * PS * 8);
+    const bool sh = world > 1;
+    L.pull_src = take(sh ? N * 4 : 0);
+    L.pull_rank = take(sh ? N * 4 : 0);
+    L.pull_counts = take(sh ? (size_t)world * 8 : 0);
+    L.pull_fill = take(sh ? (size_t)world * 4 : 0);
+    L.pull_off = take(sh ? (size_t)world * 8 : 0);
+    L.pull_req = take(sh ? N * 4 : 0);
+    L.pull_outpos = take(sh ? N * 4 : 0);
+    L.pull_serve = take(sh ? xb * world : 0);  // worst case: every rank reads only this shard
     const bool ad = flags & PF_FLAG_ADAPTIVE;
     const bool mn = flags & PF_FLAG_MULTINOMIAL;
     L.lw0 = take((ad || mn) ? N * 4 : 0);
@@ -1008,6 +1018,83 @@ int pf_cross_stage(pf_handle* h, int t, const void* dev_partner_states) {
     h->mark(PF_KERNEL_CROSS, false);
     h->cur ^= 1;
     return check_cuda(h, "pf_cross_stage");
+}
+
+// ---- pull exchange of the cross stages (include/pf.h) --------------------
+static PullArgs pull_args(pf_handle* h) {
+    PullArgs a;
+    a.key = make_key(h->seed);
+    a.n = h->step_n;
+    a.S_loc = h->S;
+    a.L = h->L;
+    a.rank = h->rank;
+    a.b = h->b;
+    a.M = h->M;
+    a.Nloc = h->N;
+    a.top_thr = h->at<uint32_t>(h->lay.top_thr);
+    a.G = h->world;
+    a.src_local = h->at<uint32_t>(h->lay.pull_src);
+    a.src_rank = h->at<uint32_t>(h->lay.pull_rank);
+    a.counts = h->at<unsigned long long>(h->lay.pull_counts);
+    a.fill = h->at<uint32_t>(h->lay.pull_fill);
+    a.offsets = h->at<unsigned long long>(h->lay.pull_off);
+    a.req = h->at<uint32_t>(h->lay.pull_req);
+    a.outpos = h->at<uint32_t>(h->lay.pull_outpos);
+    a.dbg_anc = (h->flags & PF_FLAG_DEBUG) ? h->at<int32_t>(h->lay.dbg_anc) : nullptr;
+    return a;
+}
+
+int pf_cross_pull_plan(pf_handle* h, uint64_t* host_counts) {
+    if (!h || !host_counts) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
+    if (!h->top_done) return fail(h, PF_ESTATE, "pf_step_top must run first");
+    const PullArgs a = pull_args(h);
+    cudaMemsetAsync(a.counts, 0, (size_t)h->world * 8, h->stream);
+    cudaMemsetAsync(a.fill, 0, (size_t)h->world * 4, h->stream);
+    h->mark(PF_KERNEL_CROSS, true);
+    launch_pull_compose(h->stream, a, (h->flags & PF_FLAG_DEBUG) != 0);
+    h->mark(PF_KERNEL_CROSS, false);
+    cudaError_t e = cudaMemcpyAsync(host_counts, a.counts, (size_t)h->world * 8, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_cross_pull_plan: ") + cudaGetErrorString(e));
+    return check_cuda(h, "pf_cross_pull_plan");
+}
+
+int pf_cross_pull_pack(pf_handle* h, const uint64_t* host_offsets, const uint32_t** dev_requests) {
+    if (!h || !host_offsets || !dev_requests) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
+    const PullArgs a = pull_args(h);
+    const cudaError_t e = cudaMemcpyAsync(const_cast<unsigned long long*>(a.offsets), host_offsets,
+                                          (size_t)h->world * 8, cudaMemcpyHostToDevice, h->stream);
+    if (e != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_cross_pull_pack: ") + cudaGetErrorString(e));
+    h->mark(PF_KERNEL_CROSS, true);
+    launch_pull_pack(h->stream, a);
+    h->mark(PF_KERNEL_CROSS, false);
+    *dev_requests = a.req;
+    return check_cuda(h, "pf_cross_pull_pack");
+}
+
+int pf_cross_pull_serve(pf_handle* h, const uint32_t* dev_requests_in, uint64_t n, const void** dev_states) {
+    if (!h || (n && !dev_requests_in) || !dev_states) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
+    if (n > h->N * (uint64_t)h->world) return fail(h, PF_EINVAL, "too many requests");
+    float* out = h->at<float>(h->lay.pull_serve);
+    h->mark(PF_KERNEL_CROSS, true);
+    if (n) launch_pull_move(h->stream, h->plan.D, true, h->X(h->cur), dev_requests_in, out, n);
+    h->mark(PF_KERNEL_CROSS, false);
+    *dev_states = out;
+    return check_cuda(h, "pf_cross_pull_serve");
+}
+
+int pf_cross_pull_finish(pf_handle* h, const void* dev_states_in) {
+    if (!h || !dev_states_in) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
+    h->mark(PF_KERNEL_CROSS, true);
+    launch_pull_move(h->stream, h->plan.D, false, static_cast<const float*>(dev_states_in),
+                     h->at<uint32_t>(h->lay.pull_outpos), h->X(h->cur ^ 1), h->N);
+    h->mark(PF_KERNEL_CROSS, false);
+    h->cur ^= 1;
+    return check_cuda(h, "pf_cross_pull_finish");
 }
 
 int pf_step(pf_handle* h, const float* y_host) {

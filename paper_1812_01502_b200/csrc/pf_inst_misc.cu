@@ -1,4 +1,6 @@
 // Instantiations of k_init, k_cascade and the debug kernels.
+#include <algorithm>
+
 #include "pf_launch.h"
 
 namespace pfk {
@@ -157,6 +159,103 @@ __global__ void k_block_gather(const float* in, float* out, const int32_t* A, ui
 void launch_block_gather(cudaStream_t st, const float* in, float* out, const int32_t* A, uint64_t N, uint32_t b,
                          uint32_t D) {
     k_block_gather<<<1184, 256, 0, st>>>(in, out, A, N, b, D);
+}
+
+// ---- pull exchange (PullArgs in pf_kernels.cuh) ---------------------------------------
+__global__ void __launch_bounds__(256) k_pull_compose(const __grid_constant__ PullArgs a) {
+    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < a.Nloc;
+         l += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t c = a.rank, lc = (uint32_t)l;
+        for (uint32_t t = a.L; t >= 1u; --t) {  // the stage S_loc + t draw at the current position
+            const uint64_t gpos = (uint64_t)c * a.Nloc + lc;
+            const uint4 blk = rng_block(a.key, (uint32_t)(gpos >> 2), a.n, kDomainResample, a.S_loc + t);
+            const uint32_t r = word_of(blk, (int)(gpos & 3u));
+            const uint32_t P = __ldg(a.top_thr + (a.G - (a.G >> (t - 1))) + (c >> t));
+            const uint32_t bit = 1u << (t - 1);
+            c = ((r >> a.b) < P) ? (c & ~bit) : (c | bit);
+            lc = ((lc >> a.b) << a.b) | (r & (a.M - 1u));
+        }
+        a.src_local[l] = lc;
+        a.src_rank[l] = c;
+        atomicAdd(a.counts + c, 1ull);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_pull_pack(const __grid_constant__ PullArgs a) {
+    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < a.Nloc;
+         l += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = a.src_rank[l];
+        const uint64_t k = a.offsets[c] + atomicAdd(a.fill + c, 1u);
+        a.req[k] = a.src_local[l];
+        a.outpos[k] = (uint32_t)l;
+    }
+}
+
+// stage tables of the cross stages for the debug interface (every local position's draw)
+__global__ void k_pull_debug_tables(const __grid_constant__ PullArgs a) {
+    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < a.Nloc;
+         l += (uint64_t)gridDim.x * blockDim.x)
+        for (uint32_t t = 1; t <= a.L; ++t) {
+            const uint64_t gpos = (uint64_t)a.rank * a.Nloc + l;
+            const uint4 blk = rng_block(a.key, (uint32_t)(gpos >> 2), a.n, kDomainResample, a.S_loc + t);
+            const uint32_t r = word_of(blk, (int)(gpos & 3u));
+            const uint32_t P = __ldg(a.top_thr + (a.G - (a.G >> (t - 1))) + (a.rank >> t));
+            const uint32_t bit = 1u << (t - 1);
+            const uint32_t c = ((r >> a.b) < P) ? (a.rank & ~bit) : (a.rank | bit);
+            const uint64_t src = (uint64_t)c * a.Nloc + ((((uint32_t)l >> a.b) << a.b) | (r & (a.M - 1u)));
+            a.dbg_anc[(uint64_t)(a.S_loc + t - 1) * a.Nloc + l] = (int32_t)src;
+        }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_pull_gather(const float* __restrict__ x, const uint32_t* __restrict__ idx,
+                                                     float* __restrict__ out, uint64_t n) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = idx[k];
+#pragma unroll
+        for (int c = 0; c < D; ++c) out[k * D + c] = __ldg(x + i * D + c);
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_pull_scatter(const float* __restrict__ in, const uint32_t* __restrict__ pos,
+                                                      float* __restrict__ x, uint64_t n) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = pos[k];
+#pragma unroll
+        for (int c = 0; c < D; ++c) x[i * D + c] = in[k * D + c];
+    }
+}
+
+void launch_pull_compose(cudaStream_t st, const PullArgs& a, bool debug) {
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((a.Nloc + 255) / 256, 148ull * 8);
+    k_pull_compose<<<grid, 256, 0, st>>>(a);
+    if (debug) k_pull_debug_tables<<<grid, 256, 0, st>>>(a);
+}
+
+void launch_pull_pack(cudaStream_t st, const PullArgs& a) {
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((a.Nloc + 255) / 256, 148ull * 8);
+    k_pull_pack<<<grid, 256, 0, st>>>(a);
+}
+
+void launch_pull_move(cudaStream_t st, int D, bool gather, const float* src, const uint32_t* idx, float* dst,
+                      uint64_t n) {
+    const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148ull * 8));
+    if (gather) {
+        switch (D) {
+            case 1: k_pull_gather<1><<<grid, 256, 0, st>>>(src, idx, dst, n); break;
+            case 2: k_pull_gather<2><<<grid, 256, 0, st>>>(src, idx, dst, n); break;
+            case 4: k_pull_gather<4><<<grid, 256, 0, st>>>(src, idx, dst, n); break;
+            default: k_pull_gather<8><<<grid, 256, 0, st>>>(src, idx, dst, n); break;
+        }
+    } else {
+        switch (D) {
+            case 1: k_pull_scatter<1><<<grid, 256, 0, st>>>(src, idx, dst, n); break;
+            case 2: k_pull_scatter<2><<<grid, 256, 0, st>>>(src, idx, dst, n); break;
+            case 4: k_pull_scatter<4><<<grid, 256, 0, st>>>(src, idx, dst, n); break;
+            default: k_pull_scatter<8><<<grid, 256, 0, st>>>(src, idx, dst, n); break;
+        }
+    }
 }
 
 void launch_cascade(int D, const LaunchCfg& c, const CascadeArgs& a) {

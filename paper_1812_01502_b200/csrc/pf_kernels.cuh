@@ -419,6 +419,29 @@ __global__ void __launch_bounds__(256) k_cross(const __grid_constant__ CrossArgs
 }
 
 // -------------------------------------------------------------------------------------
+// Pull exchange of the cross stages (alternative to L rounds of k_cross):
+// every output of this shard composes its L cross-stage draws locally (they are
+// counter-based, and every rank holds the top thresholds after k_top), giving the
+// (rank, local position) of its stage-S_loc source; the requests are grouped by owner
+// rank, exchanged in one all-to-all, served by a gather on the owner, and the states come
+// back in a second all-to-all.  Same draws and the same x_hat as the pairwise rounds.
+struct PullArgs {
+    Key key;
+    uint32_t n, S_loc, L, rank, b, M;
+    uint64_t Nloc;
+    const uint32_t* top_thr;  // G - 1 top thresholds (top level t at G - (G >> (t-1)))
+    uint32_t G;
+    uint32_t* src_local;      // Nloc: local position of the source on its owner
+    uint32_t* src_rank;       // Nloc: owner rank
+    unsigned long long* counts;  // G: requests per owner rank
+    uint32_t* fill;           // G: slots used (pack)
+    const unsigned long long* offsets;  // G: start of each owner's requests (pack)
+    uint32_t* req;            // Nloc: requests grouped by owner rank
+    uint32_t* outpos;         // Nloc: the output each request fills
+    int32_t* dbg_anc;         // stage tables (debug) or nullptr
+};
+
+// -------------------------------------------------------------------------------------
 // Debug helpers (not on the timed path).
 template <int UNUSED>
 __global__ void k_debug_compose(const int32_t* __restrict__ anc, uint64_t N, uint32_t S, int32_t* __restrict__ A) {

@@ -44,6 +44,10 @@ inline void launch_stages(int D, int tb, bool dbg, int qpt, const LaunchCfg& c, 
 void launch_cascade(int D, const LaunchCfg& c, const CascadeArgs& a);
 void launch_ess(const LaunchCfg& chunks, const EssArgs& a);
 void launch_island(cudaStream_t st, const IslandArgs& a);
+void launch_pull_compose(cudaStream_t st, const PullArgs& a, bool debug);
+void launch_pull_pack(cudaStream_t st, const PullArgs& a);
+void launch_pull_move(cudaStream_t st, int D, bool gather, const float* src, const uint32_t* idx, float* dst,
+                      uint64_t n);
 void launch_multinomial(int D, cudaStream_t st, const MultinomialArgs& a, const float* lw);
 void launch_block_gather(cudaStream_t st, const float* in, float* out, const int32_t* A, uint64_t N, uint32_t b,
                          uint32_t D);

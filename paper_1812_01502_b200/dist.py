@@ -87,6 +87,16 @@ class TorchTransport:
         return recv
 
 
+    def all_to_all(self, send, send_splits, recv_splits):
+        """One all-to-all of a 1-D tensor: send_splits[r] elements to rank r (in rank order),
+        recv_splits[r] elements from rank r.  NCCL over NVLink on GPUs, gloo on CPU."""
+        import torch
+        out = torch.empty(int(sum(recv_splits)), dtype=send.dtype, device=send.device)
+        self.dist.all_to_all_single(out, send.contiguous(), output_split_sizes=[int(v) for v in recv_splits],
+                                    input_split_sizes=[int(v) for v in send_splits], group=self.group)
+        return out
+
+
 # ----------------------------------------------------------------------------- backend
 class LibBackend:
     """One shard on the current GPU through the C-ABI (libpf.so)."""
@@ -143,6 +153,30 @@ class LibBackend:
         self._keep_p = partner_buf
         self.pf._check(self.pf.lib().pf_cross_stage(self.h, t, partner_buf.data_ptr()), self.h)
 
+    # pull exchange (include/pf.h pf_cross_pull_*)
+    def pull_plan(self) -> np.ndarray:
+        counts = np.zeros(self.world, np.uint64)
+        self.pf._check(self.pf.lib().pf_cross_pull_plan(self.h, counts.ctypes.data), self.h)
+        return counts.astype(np.int64)
+
+    def pull_pack(self, offsets: np.ndarray):
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        p = ctypes.c_void_p()
+        self.pf._check(self.pf.lib().pf_cross_pull_pack(self.h, off.ctypes.data, ctypes.byref(p)), self.h)
+        nloc = self.N // self.world
+        return self._view(int(p.value), 4 * nloc, self.torch.int32)
+
+    def pull_serve(self, req_in):
+        n = int(req_in.numel())
+        p = ctypes.c_void_p()
+        ptr = req_in.data_ptr() if n else None
+        self.pf._check(self.pf.lib().pf_cross_pull_serve(self.h, ptr, n, ctypes.byref(p)), self.h)
+        return self._view(int(p.value), 4 * self.d * n, self.torch.uint8)
+
+    def pull_finish(self, states_in):
+        self._keep_s = states_in
+        self.pf._check(self.pf.lib().pf_cross_pull_finish(self.h, states_in.data_ptr()), self.h)
+
     def step_local_dev(self, y_dev):
         self.pf._check(self.pf.lib().pf_step_local(self.h, None, y_dev.data_ptr()), self.h)
         p = ctypes.c_void_p()
@@ -185,11 +219,16 @@ class LibBackend:
 
 
 # ----------------------------------------------------------------------------- steps
-def sharded_step(backend, transport, y, y_dev=None) -> None:
+def sharded_step(backend, transport, y, y_dev=None, exchange: str = "pairwise") -> None:
     """One collective time step on this rank (every rank calls it with the same y; with
-    y_dev the observation is read from device memory)."""
+    y_dev the observation is read from device memory).  exchange: "pairwise" (L rounds of
+    whole-buffer swaps with the butterfly partner) or "pull" (one all-to-all of exactly
+    the states each rank's outputs read)."""
     rec = backend.step_local(y) if y_dev is None else backend.step_local_dev(y_dev)
     backend.step_top(transport.allgather(rec))
+    if exchange == "pull":
+        pull_exchange(backend, transport)
+        return
     world = transport.world
     L = world.bit_length() - 1
     for t in range(1, L + 1):
@@ -198,7 +237,51 @@ def sharded_step(backend, transport, y, y_dev=None) -> None:
         backend.cross_stage(t, recv)
 
 
-def loopback_step(backends: Sequence, y) -> None:
+def pull_exchange(backend, transport) -> None:
+    """The L cross stages as one pull (include/pf.h pf_cross_pull_*): composed sources,
+    requests to their owners (all-to-all), owners gather, states back (all-to-all)."""
+    import torch
+    counts = backend.pull_plan()                         # my outputs per owner rank
+    cnt = torch.tensor(counts, dtype=torch.int64, device=transport_device(transport))
+    asked = transport.all_to_all(cnt, [1] * transport.world, [1] * transport.world).cpu().numpy()
+    offsets = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
+    req = backend.pull_pack(offsets)
+    req_in = transport.all_to_all(req, counts, asked)    # positions others read from me
+    served = backend.pull_serve(req_in)
+    sb = 4 * backend.d                                   # state bytes
+    states = transport.all_to_all(served, asked * sb, counts * sb)
+    backend.pull_finish(states)
+
+
+def transport_device(transport):
+    return "cuda" if getattr(transport, "nccl", False) else "cpu"
+
+
+def loopback_pull(backends: Sequence) -> None:
+    """pull_exchange for G shards on one GPU (the all-to-alls are slices and copies)."""
+    import torch
+    G = len(backends)
+    counts = [b.pull_plan() for b in backends]           # counts[q][r]: rank q's outputs read r
+    reqs = []
+    for q, b in enumerate(backends):
+        off = np.concatenate([[0], np.cumsum(counts[q])[:-1]]).astype(np.int64)
+        reqs.append((b.pull_pack(off), off))
+    served = []
+    for r, b in enumerate(backends):                     # requests to r, in requester order
+        parts = [reqs[q][0][int(reqs[q][1][r]): int(reqs[q][1][r] + counts[q][r])] for q in range(G)]
+        req_in = torch.cat(parts) if parts else torch.empty(0, dtype=torch.int32, device="cuda")
+        served.append((b.pull_serve(req_in.contiguous()).clone(), [int(counts[q][r]) for q in range(G)]))
+    sb = 4 * backends[0].d
+    for q, b in enumerate(backends):                     # states back, grouped by owner
+        parts = []
+        for r in range(G):
+            buf, per_q = served[r]
+            start = sum(per_q[:q]) * sb
+            parts.append(buf[start: start + per_q[q] * sb])
+        b.pull_finish(torch.cat(parts).contiguous())
+
+
+def loopback_step(backends: Sequence, y, exchange: str = "pairwise") -> None:
     """The same collective sequence for G shards held by one process on one GPU (the
     exchange is a pointer hand-over; every kernel is stream-ordered, none waits on
     another shard's kernel)."""
@@ -207,6 +290,9 @@ def loopback_step(backends: Sequence, y) -> None:
     allr = torch.stack([r for r in recs])
     for b in backends:
         b.step_top(allr)
+    if exchange == "pull":
+        loopback_pull(backends)
+        return
     world = len(backends)
     L = world.bit_length() - 1
     for t in range(1, L + 1):

@@ -87,6 +87,10 @@ def lib() -> ctypes.CDLL:
         L.pf_set_airpf.argtypes = [vp, ctypes.c_int]
         L.pf_set_multinomial.argtypes = [vp, ctypes.c_int]
         L.pf_set_rotation.argtypes = [vp, ctypes.c_int]
+        L.pf_cross_pull_plan.argtypes = [vp, vp]
+        L.pf_cross_pull_pack.argtypes = [vp, vp, ctypes.POINTER(vp)]
+        L.pf_cross_pull_serve.argtypes = [vp, vp, u64, ctypes.POINTER(vp)]
+        L.pf_cross_pull_finish.argtypes = [vp, vp]
         L.pf_rotation_offset.argtypes = [vp]
         _lib = L
     return _lib
@@ -97,7 +101,8 @@ EXPORTED = ["pf_workspace_bytes", "pf_init", "pf_step", "pf_step_dev", "pf_estim
             "pf_timing_enable", "pf_timing_read", "pf_workspace_bytes_sharded", "pf_init_sharded",
             "pf_step_local", "pf_shard_record", "pf_step_top", "pf_cross_buffer", "pf_cross_stage",
             "pf_set_adaptive", "pf_last_stages", "pf_set_airpf", "pf_set_multinomial", "pf_set_rotation",
-            "pf_rotation_offset"]
+            "pf_rotation_offset", "pf_cross_pull_plan", "pf_cross_pull_pack", "pf_cross_pull_serve",
+            "pf_cross_pull_finish"]
 PF_KERNEL_KINDS = 5
 KERNEL_NAMES = ("k_pass1", "k_cascade", "k_stages", "k_top", "k_cross")
 

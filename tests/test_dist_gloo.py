@@ -2,7 +2,8 @@
 world_size = 2 over gloo on CPU.  The per-shard compute is a CPU stand-in built from the
 oracle (test infrastructure), so this checks the collective sequence itself: records
 gathered in rank order, butterfly partners, every cross-stage source lies in the own or
-the partner shard, the exchanged buffers, and the final shards = the oracle's x_hat."""
+the partner shard, the exchanged buffers, and the final shards = the oracle's x_hat; and
+the pull exchange (composed sources, one all-to-all of requests, one of states)."""
 import os
 import socket
 
@@ -87,6 +88,33 @@ class OracleShard:
             out[l] = self.buf[src - self.pos0] if owner == self.rank else pbuf[src - peer * self.nloc]
         self.buf = out
 
+    # pull exchange (dist.pull_exchange)
+    def pull_plan(self):
+        pos = np.arange(self.pos0, self.pos0 + self.nloc)
+        for s in range(self.S, self.Sloc, -1):
+            pos = self.r["a"][s - 1][pos]
+        self.src_owner = pos // self.nloc
+        self.src_local = pos % self.nloc
+        return np.bincount(self.src_owner, minlength=self.world).astype(np.int64)
+
+    def pull_pack(self, offsets):
+        order = np.argsort(self.src_owner, kind="stable")  # grouped by owner, output order within
+        self.outpos = order
+        starts = np.concatenate([[0], np.cumsum(np.bincount(self.src_owner, minlength=self.world))[:-1]])
+        assert np.array_equal(starts, offsets)
+        return torch.from_numpy(self.src_local[order].astype(np.int32))
+
+    def pull_serve(self, req_in):
+        idx = req_in.numpy().astype(np.int64)
+        assert np.all((idx >= 0) & (idx < self.nloc))
+        return torch.from_numpy(self.buf[idx].view(np.uint8).reshape(-1).copy())
+
+    def pull_finish(self, states):
+        st = states.numpy().view(np.float32).reshape(self.nloc, self.d)
+        out = np.empty_like(self.buf)
+        out[self.outpos] = st
+        self.buf = out
+
     def finish(self):
         full = self.r["xhat"].astype(np.float32)
         assert np.array_equal(self.buf, full[self.pos0: self.pos0 + self.nloc])
@@ -94,7 +122,7 @@ class OracleShard:
         self.n += 1
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, exchange="pairwise"):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -106,7 +134,7 @@ def _worker(rank, world, port, q):
         tr = pfd.TorchTransport()
         _, ys = inputs.simulate(cfg, T=3)
         for y in ys:
-            pfd.sharded_step(be, tr, y)
+            pfd.sharded_step(be, tr, y, exchange=exchange)
             be.finish()
         dist.barrier()
         dist.destroy_process_group()
@@ -123,12 +151,12 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_gloo_sharded_sequence(world):
+@pytest.mark.parametrize("world,exchange", [(2, "pairwise"), (4, "pairwise"), (2, "pull"), (4, "pull")])
+def test_gloo_sharded_sequence(world, exchange):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, exchange)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)

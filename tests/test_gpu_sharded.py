@@ -16,9 +16,10 @@ from paper_1812_01502_b200 import dist as pfd  # noqa: E402
 from paper_1812_01502_b200 import pf as pfb  # noqa: E402
 
 
+@pytest.mark.parametrize("exchange", ["pairwise", "pull"])
 @pytest.mark.parametrize("name,N,M,G", [("C4", 1 << 16, 64, 2), ("C4", 1 << 16, 64, 4), ("C3", 1 << 15, 32, 4),
                                         ("C2", 1 << 15, 256, 2), ("C3", 1 << 12, 2, 8), ("C1", 1024, 64, 8)])
-def test_loopback_matches_single_gpu(name, N, M, G):
+def test_loopback_matches_single_gpu(name, N, M, G, exchange):
     cfg = inputs.CONFIGS[name]
     p = inputs.model_params(cfg)
     _, ys = inputs.simulate(cfg, T=3)
@@ -27,7 +28,7 @@ def test_loopback_matches_single_gpu(name, N, M, G):
     shards = [pfd.LibBackend(p, N, M, 21, r, G, debug=True) for r in range(G)]
     for n, y in enumerate(ys):
         single.step(y)
-        pfd.loopback_step(shards, y)
+        pfd.loopback_step(shards, y, exchange=exchange)
         for phi in (pfb.PF_PHI_X, pfb.PF_PHI_X2):
             for kind in (pfb.PF_EST_FILTER, pfb.PF_EST_PREDICT):
                 e1 = single.estimate(phi, kind)
