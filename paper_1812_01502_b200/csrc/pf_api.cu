@@ -1047,6 +1047,7 @@ static PullArgs pull_args(pf_handle* h) {
 int pf_cross_pull_plan(pf_handle* h, uint64_t* host_counts) {
     if (!h || !host_counts) return fail(h, PF_EINVAL, "NULL argument");
     if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
+    if (h->world > 64) return fail(h, PF_EINVAL, "the pull exchange supports up to 64 ranks");
     if (!h->top_done) return fail(h, PF_ESTATE, "pf_step_top must run first");
     const PullArgs a = pull_args(h);
     cudaMemsetAsync(a.counts, 0, (size_t)h->world * 8, h->stream);

@@ -162,7 +162,14 @@ void launch_block_gather(cudaStream_t st, const float* in, float* out, const int
 }
 
 // ---- pull exchange (PullArgs in pf_kernels.cuh) ---------------------------------------
+// Requests per owner: a shared-memory histogram per CTA, one global atomic per bin per CTA
+// (G <= 64 bins).
+constexpr uint32_t kPullMaxG = 64;
+
 __global__ void __launch_bounds__(256) k_pull_compose(const __grid_constant__ PullArgs a) {
+    __shared__ unsigned int hist[kPullMaxG];
+    for (uint32_t t = threadIdx.x; t < a.G; t += blockDim.x) hist[t] = 0u;
+    __syncthreads();
     for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < a.Nloc;
          l += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t c = a.rank, lc = (uint32_t)l;
@@ -177,17 +184,48 @@ __global__ void __launch_bounds__(256) k_pull_compose(const __grid_constant__ Pu
         }
         a.src_local[l] = lc;
         a.src_rank[l] = c;
-        atomicAdd(a.counts + c, 1ull);
+        atomicAdd(hist + c, 1u);
     }
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < a.G; t += blockDim.x)
+        if (hist[t]) atomicAdd(a.counts + t, (unsigned long long)hist[t]);
 }
 
+// Slots: per 256 outputs, warp ballots per owner give each request its rank inside the
+// warp, a small scan over the warps its rank inside the CTA, and one global atomic per
+// owner reserves the CTA's range (outputs keep their order inside a CTA chunk).
 __global__ void __launch_bounds__(256) k_pull_pack(const __grid_constant__ PullArgs a) {
-    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < a.Nloc;
-         l += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t c = a.src_rank[l];
-        const uint64_t k = a.offsets[c] + atomicAdd(a.fill + c, 1u);
-        a.req[k] = a.src_local[l];
-        a.outpos[k] = (uint32_t)l;
+    __shared__ unsigned int wcnt[8][kPullMaxG];
+    __shared__ unsigned int wbase[8][kPullMaxG];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < a.Nloc; base += stride) {
+        const uint64_t l = base + threadIdx.x;
+        const bool valid = l < a.Nloc;
+        const uint32_t c = valid ? a.src_rank[l] : 0xffffffffu;
+        uint32_t myrank = 0u;
+        for (uint32_t bn = 0; bn < a.G; ++bn) {
+            const unsigned int m = __ballot_sync(0xffffffffu, c == bn);
+            if (c == bn) myrank = __popc(m & ((1u << lane) - 1u));
+            if (lane == 0) wcnt[warp][bn] = __popc(m);
+        }
+        __syncthreads();
+        for (uint32_t bn = threadIdx.x; bn < a.G; bn += blockDim.x) {
+            unsigned int tot = 0u;
+            for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) tot += wcnt[w][bn];
+            unsigned int off = tot ? atomicAdd(a.fill + bn, tot) : 0u;
+            for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
+                wbase[w][bn] = off;
+                off += wcnt[w][bn];
+            }
+        }
+        __syncthreads();
+        if (valid) {
+            const uint64_t k = a.offsets[c] + wbase[warp][c] + myrank;
+            a.req[k] = a.src_local[l];
+            a.outpos[l] = (uint32_t)k;  // where output l's state will arrive
+        }
+        __syncthreads();
     }
 }
 
@@ -212,18 +250,31 @@ __global__ void __launch_bounds__(256) k_pull_gather(const float* __restrict__ x
                                                      float* __restrict__ out, uint64_t n) {
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t i = idx[k];
+        if constexpr (D % 4 == 0) {
 #pragma unroll
-        for (int c = 0; c < D; ++c) out[k * D + c] = __ldg(x + i * D + c);
+            for (int c = 0; c < D / 4; ++c)
+                reinterpret_cast<float4*>(out)[k * (D / 4) + c] = __ldg(reinterpret_cast<const float4*>(x) + i * (D / 4) + c);
+        } else {
+#pragma unroll
+            for (int c = 0; c < D; ++c) out[k * D + c] = __ldg(x + i * D + c);
+        }
     }
 }
 
+// output l's state from the received buffer (x[l] = in[slot[l]]: the writes stream)
 template <int D>
-__global__ void __launch_bounds__(256) k_pull_scatter(const float* __restrict__ in, const uint32_t* __restrict__ pos,
+__global__ void __launch_bounds__(256) k_pull_scatter(const float* __restrict__ in, const uint32_t* __restrict__ slot,
                                                       float* __restrict__ x, uint64_t n) {
-    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = pos[k];
+    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < n; l += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = slot[l];
+        if constexpr (D % 4 == 0) {
 #pragma unroll
-        for (int c = 0; c < D; ++c) x[i * D + c] = in[k * D + c];
+            for (int c = 0; c < D / 4; ++c)
+                reinterpret_cast<float4*>(x)[l * (D / 4) + c] = __ldg(reinterpret_cast<const float4*>(in) + k * (D / 4) + c);
+        } else {
+#pragma unroll
+            for (int c = 0; c < D; ++c) x[l * D + c] = __ldg(in + k * D + c);
+        }
     }
 }
 

@@ -437,7 +437,7 @@ struct PullArgs {
     uint32_t* fill;           // G: slots used (pack)
     const unsigned long long* offsets;  // G: start of each owner's requests (pack)
     uint32_t* req;            // Nloc: requests grouped by owner rank
-    uint32_t* outpos;         // Nloc: the output each request fills
+    uint32_t* outpos;         // Nloc: request slot of output l (where its state arrives)
     int32_t* dbg_anc;         // stage tables (debug) or nullptr
 };
 
