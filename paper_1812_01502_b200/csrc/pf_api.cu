@@ -1,9 +1,13 @@
 // pf_api.cu -- C-ABI (include/pf.h) and host orchestration of one BPF step.
 //
-// Launch sequence of pf_step (DESIGN.md §4):
-//   k_pass1 (NT tiles) -> k_cascade (ceil(NT/2048) CTAs) -> k_stages x (#passes)
+// Launch sequence of pf_step (DESIGN.md §5):
+//   k_pass1 (NT tiles) -> k_cascade (one wave of CTAs) -> k_stages x (#passes)
 // Every pass moves the particle states through shared-memory tiles (coalesced reads and
-// writes; no random HBM access anywhere on the step).
+// writes; no random HBM access anywhere on the step).  The next rows reuse the same
+// kernels: run_step_adaptive (weigh -> cascade -> ESS -> resample up to S*),
+// run_step_airpf (AIRPF pass -> cascade -> island stages), run_step_multinomial (weigh ->
+// cascade -> global CDF search and gather); the sharded step is pf_step_local /
+// pf_step_top followed by the pull exchange (pf_cross_pull_*) or pf_cross_stage rounds.
 #include <cuda_runtime.h>
 
 #include <cmath>

@@ -10,7 +10,10 @@
 //   k_stages    (pf_stages.cuh) stages s0..s0+k-1 for a tile of 2^k groups spaced
 //               2^{s0-1} apart (exactly the groups the butterfly pairs at those stages),
 //               moving the particle states once per pass
-//   k_top / k_cross   the cross-shard stages of a sharded run
+//   k_top / k_cross   the cross-shard stages of a sharded run (pairwise rounds); the pull
+//               exchange kernels k_pull_* live in pf_inst_misc.cu
+//   next rows   k_ess_* (fully adapted scheme), k_island_* (AIRPF), MultinomialArgs
+//               (Alg. 2, pf_multinomial.cu); k_pass1's weigh / resample / AIRPF modes
 //
 // Draw contract: every resampling word is word (i & 3) of Philox block
 // (i >> 2, n, RESAMPLE<<24 | s, 0); stage 1 u = (r>>8) 2^-24 with a = #{k < 2M-1 :
