@@ -1263,6 +1263,7 @@ int pf_debug_set_state(pf_handle* h, const float* host_xhat, uint32_t n) {
     h->n = n;
     h->carry_mode = 0;  // the given state is unweighted
     h->isl_valid = false;  // and holds x_hat itself
+    h->rho = 0;            // in the natural group layout
     return PF_OK;
 }
 
