@@ -1,5 +1,8 @@
 // Philox4x32-10 throughput on B200: (A) __umulhi + mul, (B) 64-bit multiply (IMAD.WIDE),
 // (C) B with the key schedule precomputed in kernel parameters (constant bank operands).
+// Measured on B200 (round 1): A 4.72e11, B 4.73e11, C 4.94e11 Philox blocks/s for the whole
+// GPU = ~75 cycles per warp-block per SM sub-partition (20 IMAD.WIDE on the FMA-heavy pipe
+// at 4 cycles each).  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o philox_bench philox_bench.cu
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
