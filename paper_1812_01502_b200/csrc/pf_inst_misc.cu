@@ -106,27 +106,43 @@ __device__ __forceinline__ uint32_t island_takes(const IslandArgs& a, uint32_t c
     return take;
 }
 
+// Thread per pair of partner quads (stages s >= 3: quads c4 and c4 ^ 2^{s-3}, the same
+// lane e holding partners) or per quad (s <= 2: the partner lies in the same quad): every
+// Philox block is computed once and Alg. 7's rule sees both sides' draws.
 __global__ void __launch_bounds__(256) k_island_draw(const __grid_constant__ IslandArgs a) {
     const uint32_t nq = (a.m + 3u) >> 2;
+    const uint32_t np = nq >= 2u ? nq >> 1 : 1u;  // work items per stage (upper bound)
     const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (t >= (uint64_t)nq * a.S) return;
-    const uint32_t s = (uint32_t)(t / nq) + 1u, c4 = (uint32_t)(t % nq);
-    uint32_t take = island_takes(a, c4, s);
-    if (a.modified) {  // Alg. 7: a pair that swapped blocks keeps its own
-        const uint32_t bit = 1u << (s - 1);
-        const uint32_t p4 = (bit >= 4u) ? (c4 ^ (bit >> 2)) : c4;
-        const uint32_t ptake = (p4 == c4) ? take : island_takes(a, p4, s);
-        uint32_t keep = 0u;
+    const uint32_t s = (uint32_t)(t / nq) + 1u, w = (uint32_t)(t % nq);
+    const uint32_t bit = 1u << (s - 1);
+    if (bit < 4u) {  // partners inside the quad
+        const uint32_t c4 = w;
+        uint32_t take = island_takes(a, c4, s);
+        if (a.modified) {
+            uint32_t keep = 0u;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const uint32_t i = 4u * c4 + (uint32_t)e;
-            const uint32_t h = i ^ bit;
-            const uint32_t eh = h & 3u;
-            if (((take >> e) & 1u) && ((ptake >> eh) & 1u)) keep |= 1u << e;
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t eh = (uint32_t)e ^ bit;
+                if (((take >> e) & 1u) && ((take >> eh) & 1u)) keep |= 1u << e;
+            }
+            take &= ~keep;
         }
-        take &= ~keep;
+        a.choice[(uint64_t)(s - 1) * nq + c4] = (uint8_t)take;
+        return;
     }
-    a.choice[(uint64_t)(s - 1) * nq + c4] = (uint8_t)take;
+    if (w >= np) return;
+    const uint32_t qb = bit >> 2;  // quad-index bit of the partner
+    const uint32_t lo4 = ((w & ~(qb - 1u)) << 1) | (w & (qb - 1u));  // insert a 0 at bit log2(qb)
+    const uint32_t hi4 = lo4 | qb;
+    uint32_t tl = island_takes(a, lo4, s), th = island_takes(a, hi4, s);
+    if (a.modified) {  // lane e of the low quad and lane e of the high quad are partners
+        const uint32_t keep = tl & th;
+        tl &= ~keep;
+        th &= ~keep;
+    }
+    a.choice[(uint64_t)(s - 1) * nq + lo4] = (uint8_t)tl;
+    a.choice[(uint64_t)(s - 1) * nq + hi4] = (uint8_t)th;
 }
 
 __global__ void __launch_bounds__(256) k_island_compose(const __grid_constant__ IslandArgs a) {
