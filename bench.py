@@ -48,8 +48,9 @@ def parse():
                     help="AIRPF (Alg. 4) with Alg. 7 (1) or Alg. 6 (2) instead of augmented resampling")
     ap.add_argument("--rotate", action="store_true",
                     help="with --theta: stage rotation (PAPER.md:1309)")
-    ap.add_argument("--exchange", default="pull", choices=["pull", "pairwise"],
-                    help="N > 1: cross stages as one all-to-all pull (default) or L pairwise rounds")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "pull", "pairwise"],
+                    help="N > 1: cross stages as one peer-memory gather over NVLink (default; the pull "
+                         "exchange if a rank cannot map its peers), one all-to-all pull, or L pairwise rounds")
     ap.add_argument("--multinomial", action="store_true",
                     help="the plain BPF (Alg. 2, multinomial resampling) instead of augmented resampling")
     return ap.parse_args()
@@ -248,6 +249,15 @@ def run_ours(args):
             # strong scaling: the global N of the configuration is split over the ranks
             f = pfd.LibBackend(params, cfg.N, cfg.M, args.seed, rank, world, stream=stream)
             tr = pfd.TorchTransport()
+            if args.exchange == "peer":
+                try:
+                    pfd.peer_connect(f, tr)
+                    ok = True
+                except pf.PFError as e:
+                    print(f"[bench] rank {rank}: peer mapping failed ({e}); pull exchange", file=sys.stderr)
+                    ok = False
+                if not all(tr.allgather_object(ok)):
+                    args.exchange = "pull"
 
             def step(k, yd=None):
                 pfd.sharded_step(f, tr, None, y_dev[k % T] if yd is None else yd, exchange=args.exchange)

@@ -226,6 +226,34 @@ int pf_cross_pull_pack(pf_handle* h, const uint64_t* host_offsets, const uint32_
 int pf_cross_pull_serve(pf_handle* h, const uint32_t* dev_requests_in, uint64_t n, const void** dev_states);
 int pf_cross_pull_finish(pf_handle* h, const void* dev_states_in);
 
+/* Peer-memory exchange: the L cross stages as ONE kernel that composes every output's
+ * (owner rank, local position) as the pull exchange does and reads that state straight
+ * from the owner's workspace over NVLink (P2P loads through CUDA IPC mappings) into this
+ * shard's x_hat.  No request/reply round, no host synchronisation.
+ *   pf_peer_export(h, handle, &offset)  handle: HOST, PF_IPC_HANDLE_BYTES bytes (the CUDA
+ *                                       IPC handle of the allocation that holds this
+ *                                       workspace); offset: the workspace's offset in it
+ *   <all-gather of (handle, offset)>    (once, at set-up)
+ *   pf_peer_open(h, handles, offsets)   HOST, world x PF_IPC_HANDLE_BYTES / world uint64
+ *                                       in rank order; maps every other rank's workspace
+ *                                       (closed by pf_destroy)
+ *   pf_peer_set(h, workspaces)          instead of export/open when every rank's workspace
+ *                                       is already addressable here (shards on one GPU):
+ *                                       HOST, world uint64 DEVICE addresses, [rank] = own
+ *   per step, after pf_step_top:  pf_cross_peer(h)  <device barrier>
+ * Ordering is the caller's: every rank's stage-S_loc states must be complete before any
+ * rank reads them (the all-gather of the shard records that precedes pf_step_top gives
+ * this when it is stream-ordered, as NCCL's is), and no rank may start its next step
+ * before every rank has read them (the barrier: e.g. a 1-element NCCL all-reduce
+ * enqueued on the handle's stream).
+ * Gives bitwise the x_hat of the pull exchange and of the pairwise rounds.
+ * Errors: PF_EINVAL, PF_ESTATE (not sharded, before pf_step_top, no mapping), PF_ECUDA. */
+#define PF_IPC_HANDLE_BYTES 64
+int pf_peer_export(pf_handle* h, void* ipc_handle, uint64_t* offset);
+int pf_peer_open(pf_handle* h, const void* ipc_handles, const uint64_t* offsets);
+int pf_peer_set(pf_handle* h, const uint64_t* dev_workspaces);
+int pf_cross_peer(pf_handle* h);
+
 /* --- debug / test exports (parity harness) ------------------------------------ */
 #define PF_DBG_X 1         /* x_n before resampling, N x d fp32 (needs PF_FLAG_DEBUG) */
 #define PF_DBG_LOGW 2      /* log g_n(x_n^i), N fp32 (needs PF_FLAG_DEBUG) */

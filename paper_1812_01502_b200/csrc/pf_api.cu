@@ -310,6 +310,9 @@ struct pf_handle {
     uint32_t carry_mask = 0xffffffffu;
     uint32_t rho = 0;        // current rotation offset (bookkeeping for pf_last_stages users)
     bool anc_ready = false;  // dbg_A holds the ancestors of the last (multinomial) step
+    // peer-memory exchange (pf_peer_open / pf_peer_set / pf_cross_peer)
+    std::vector<unsigned char*> peer_ws;    // every rank's workspace, mapped here
+    std::vector<void*> peer_ipc;            // IPC mappings to close (allocation bases)
     // kernel timing
     bool timing;
     struct Rec {
@@ -344,6 +347,7 @@ struct pf_handle {
     }
     ~pf_handle() {
         for (cudaEvent_t e : pool) cudaEventDestroy(e);
+        for (void* p : peer_ipc) cudaIpcCloseMemHandle(p);
     }
     float* X(int i) { return reinterpret_cast<float*>(ws + (i ? lay.X1 : lay.X0)); }
     template <typename T>
@@ -1100,6 +1104,89 @@ int pf_cross_pull_finish(pf_handle* h, const void* dev_states_in) {
     h->mark(PF_KERNEL_CROSS, false);
     h->cur ^= 1;
     return check_cuda(h, "pf_cross_pull_finish");
+}
+
+// ---- peer-memory exchange of the cross stages (include/pf.h) ------------
+static_assert(sizeof(cudaIpcMemHandle_t) == PF_IPC_HANDLE_BYTES, "IPC handle size");
+typedef int (*MemGetAddressRangeFn)(unsigned long long*, size_t*, unsigned long long);
+
+int pf_peer_export(pf_handle* h, void* ipc_handle, uint64_t* offset) {
+    if (!h || !ipc_handle || !offset) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !fn || q != cudaDriverEntryPointSuccess)
+        return fail(h, PF_ECUDA, "pf_peer_export: cuMemGetAddressRange unavailable");
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (reinterpret_cast<MemGetAddressRangeFn>(fn)(&base, &size, reinterpret_cast<unsigned long long>(h->ws)) != 0)
+        return fail(h, PF_ECUDA, "pf_peer_export: the workspace is not a device allocation");
+    cudaIpcMemHandle_t hd;
+    e = cudaIpcGetMemHandle(&hd, reinterpret_cast<void*>(base));
+    if (e != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_peer_export: ") + cudaGetErrorString(e));
+    std::memcpy(ipc_handle, &hd, sizeof(hd));
+    *offset = reinterpret_cast<unsigned long long>(h->ws) - base;
+    return PF_OK;
+}
+
+int pf_peer_open(pf_handle* h, const void* ipc_handles, const uint64_t* offsets) {
+    if (!h || !ipc_handles || !offsets) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
+    if (h->world > kPeerMaxG) return fail(h, PF_EINVAL, "the peer exchange supports up to 64 ranks");
+    for (void* p : h->peer_ipc) cudaIpcCloseMemHandle(p);
+    h->peer_ipc.clear();
+    h->peer_ws.assign(h->world, nullptr);
+    for (uint32_t r = 0; r < h->world; ++r) {
+        if (r == h->rank) {
+            h->peer_ws[r] = h->ws;
+            continue;
+        }
+        cudaIpcMemHandle_t hd;
+        std::memcpy(&hd, static_cast<const unsigned char*>(ipc_handles) + (size_t)r * PF_IPC_HANDLE_BYTES, sizeof(hd));
+        void* p = nullptr;
+        const cudaError_t e = cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            h->peer_ws.clear();
+            return fail(h, PF_ECUDA, std::string("pf_peer_open: rank ") + std::to_string(r) + ": " + cudaGetErrorString(e));
+        }
+        h->peer_ipc.push_back(p);
+        h->peer_ws[r] = static_cast<unsigned char*>(p) + offsets[r];
+    }
+    return PF_OK;
+}
+
+int pf_peer_set(pf_handle* h, const uint64_t* dev_workspaces) {
+    if (!h || !dev_workspaces) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
+    if (h->world > kPeerMaxG) return fail(h, PF_EINVAL, "the peer exchange supports up to 64 ranks");
+    if (reinterpret_cast<unsigned char*>(dev_workspaces[h->rank]) != h->ws)
+        return fail(h, PF_EINVAL, "dev_workspaces[rank] must be this handle's workspace");
+    for (uint32_t r = 0; r < h->world; ++r)
+        if (!dev_workspaces[r] || (dev_workspaces[r] & 255u)) return fail(h, PF_EINVAL, "NULL or misaligned workspace");
+    for (void* p : h->peer_ipc) cudaIpcCloseMemHandle(p);
+    h->peer_ipc.clear();
+    h->peer_ws.assign(h->world, nullptr);
+    for (uint32_t r = 0; r < h->world; ++r) h->peer_ws[r] = reinterpret_cast<unsigned char*>(dev_workspaces[r]);
+    return PF_OK;
+}
+
+int pf_cross_peer(pf_handle* h) {
+    if (!h) return fail(h, PF_EINVAL, "NULL handle");
+    if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
+    if (!h->top_done) return fail(h, PF_ESTATE, "pf_step_top must run first");
+    if (h->peer_ws.size() != h->world) return fail(h, PF_ESTATE, "no peer mapping: pf_peer_open or pf_peer_set first");
+    const PullArgs a = pull_args(h);
+    PeerArgs p;
+    const size_t xoff = h->cur ? h->lay.X1 : h->lay.X0;  // same layout on every rank
+    for (uint32_t r = 0; r < kPeerMaxG; ++r)
+        p.x[r] = r < h->world ? reinterpret_cast<const float*>(h->peer_ws[r] + xoff) : nullptr;
+    p.out = h->X(h->cur ^ 1);
+    h->mark(PF_KERNEL_CROSS, true);
+    launch_peer_gather(h->stream, h->plan.D, a, p, (h->flags & PF_FLAG_DEBUG) != 0);
+    h->mark(PF_KERNEL_CROSS, false);
+    h->cur ^= 1;
+    return check_cuda(h, "pf_cross_peer");
 }
 
 int pf_step(pf_handle* h, const float* y_host) {

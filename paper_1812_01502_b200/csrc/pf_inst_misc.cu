@@ -182,22 +182,30 @@ void launch_block_gather(cudaStream_t st, const float* in, float* out, const int
 // (G <= 64 bins).
 constexpr uint32_t kPullMaxG = 64;
 
+// Stage-S_loc source (owner rank c, local position lc) of output l: the L cross-stage
+// draws composed from the last stage back (counter-based, thresholds from pf_step_top).
+__device__ __forceinline__ void compose_cross(const PullArgs& a, uint64_t l, uint32_t& c, uint32_t& lc) {
+    c = a.rank;
+    lc = (uint32_t)l;
+    for (uint32_t t = a.L; t >= 1u; --t) {  // the stage S_loc + t draw at the current position
+        const uint64_t gpos = (uint64_t)c * a.Nloc + lc;
+        const uint4 blk = rng_block(a.key, (uint32_t)(gpos >> 2), a.n, kDomainResample, a.S_loc + t);
+        const uint32_t r = word_of(blk, (int)(gpos & 3u));
+        const uint32_t P = __ldg(a.top_thr + (a.G - (a.G >> (t - 1))) + (c >> t));
+        const uint32_t bit = 1u << (t - 1);
+        c = ((r >> a.b) < P) ? (c & ~bit) : (c | bit);
+        lc = ((lc >> a.b) << a.b) | (r & (a.M - 1u));
+    }
+}
+
 __global__ void __launch_bounds__(256) k_pull_compose(const __grid_constant__ PullArgs a) {
     __shared__ unsigned int hist[kPullMaxG];
     for (uint32_t t = threadIdx.x; t < a.G; t += blockDim.x) hist[t] = 0u;
     __syncthreads();
     for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < a.Nloc;
          l += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t c = a.rank, lc = (uint32_t)l;
-        for (uint32_t t = a.L; t >= 1u; --t) {  // the stage S_loc + t draw at the current position
-            const uint64_t gpos = (uint64_t)c * a.Nloc + lc;
-            const uint4 blk = rng_block(a.key, (uint32_t)(gpos >> 2), a.n, kDomainResample, a.S_loc + t);
-            const uint32_t r = word_of(blk, (int)(gpos & 3u));
-            const uint32_t P = __ldg(a.top_thr + (a.G - (a.G >> (t - 1))) + (c >> t));
-            const uint32_t bit = 1u << (t - 1);
-            c = ((r >> a.b) < P) ? (c & ~bit) : (c | bit);
-            lc = ((lc >> a.b) << a.b) | (r & (a.M - 1u));
-        }
+        uint32_t c, lc;
+        compose_cross(a, l, c, lc);
         a.src_local[l] = lc;
         a.src_rank[l] = c;
         atomicAdd(hist + c, 1u);
@@ -292,6 +300,67 @@ __global__ void __launch_bounds__(256) k_pull_scatter(const float* __restrict__ 
             for (int c = 0; c < D; ++c) x[l * D + c] = __ldg(in + k * D + c);
         }
     }
+}
+
+// Peer-memory exchange: output l composes its source and reads the state straight from
+// the owner's buffer (a peer pointer over NVLink, or a local one) — the compose and the
+// transfer in one pass, no request/reply round.  Four outputs per thread: their loads
+// are issued together so that four remote reads are in flight per thread.
+template <int D>
+__global__ void __launch_bounds__(256) k_peer_gather(const __grid_constant__ PullArgs a,
+                                                     const __grid_constant__ PeerArgs p) {
+    constexpr int U = 4;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t l0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l0 < a.Nloc; l0 += stride * U) {
+        const float* src[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t l = l0 + (uint64_t)u * stride;
+            uint32_t c = 0u, lc = 0u;
+            if (l < a.Nloc) compose_cross(a, l, c, lc);
+            src[u] = p.x[c] + (uint64_t)lc * D;
+        }
+        if constexpr (D % 4 == 0) {
+            float4 v[U][D / 4];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (l0 + (uint64_t)u * stride < a.Nloc)
+#pragma unroll
+                    for (int q = 0; q < D / 4; ++q) v[u][q] = __ldg(reinterpret_cast<const float4*>(src[u]) + q);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t l = l0 + (uint64_t)u * stride;
+                if (l < a.Nloc)
+#pragma unroll
+                    for (int q = 0; q < D / 4; ++q) reinterpret_cast<float4*>(p.out)[l * (D / 4) + q] = v[u][q];
+            }
+        } else {
+            float v[U][D];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (l0 + (uint64_t)u * stride < a.Nloc)
+#pragma unroll
+                    for (int q = 0; q < D; ++q) v[u][q] = __ldg(src[u] + q);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t l = l0 + (uint64_t)u * stride;
+                if (l < a.Nloc)
+#pragma unroll
+                    for (int q = 0; q < D; ++q) p.out[l * D + q] = v[u][q];
+            }
+        }
+    }
+}
+
+void launch_peer_gather(cudaStream_t st, int D, const PullArgs& a, const PeerArgs& p, bool debug) {
+    const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((a.Nloc + 1023) / 1024, 148ull * 8));
+    switch (D) {
+        case 1: k_peer_gather<1><<<grid, 256, 0, st>>>(a, p); break;
+        case 2: k_peer_gather<2><<<grid, 256, 0, st>>>(a, p); break;
+        case 4: k_peer_gather<4><<<grid, 256, 0, st>>>(a, p); break;
+        default: k_peer_gather<8><<<grid, 256, 0, st>>>(a, p); break;
+    }
+    if (debug) k_pull_debug_tables<<<grid, 256, 0, st>>>(a);
 }
 
 void launch_pull_compose(cudaStream_t st, const PullArgs& a, bool debug) {

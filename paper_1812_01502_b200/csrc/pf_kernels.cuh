@@ -444,6 +444,14 @@ struct PullArgs {
     int32_t* dbg_anc;         // stage tables (debug) or nullptr
 };
 
+// Peer-memory exchange (pf_cross_peer): every rank's stage-S_loc state buffer, mapped into
+// this process (CUDA IPC over NVLink, or local pointers for shards on one GPU).
+constexpr uint32_t kPeerMaxG = 64;
+struct PeerArgs {
+    const float* x[kPeerMaxG];  // x[r] = rank r's X(cur), Nloc x d fp32
+    float* out;                 // this shard's x_hat (X(cur ^ 1))
+};
+
 // -------------------------------------------------------------------------------------
 // Debug helpers (not on the timed path).
 template <int UNUSED>

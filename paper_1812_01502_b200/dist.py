@@ -87,6 +87,26 @@ class TorchTransport:
         return recv
 
 
+    def allgather_object(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def device_barrier(self, stream=None):
+        """Every rank's work enqueued so far on `stream` is complete before anything enqueued
+        after it runs: a 1-element NCCL all-reduce on the stream (no host synchronisation);
+        with gloo a stream synchronisation and a host barrier."""
+        import torch
+        if self.nccl:
+            if getattr(self, "_bar", None) is None:
+                self._bar = torch.zeros(1, dtype=torch.float32, device="cuda")
+            with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
+                self.dist.all_reduce(self._bar, group=self.group)
+        else:
+            if stream is not None:
+                stream.synchronize()
+            self.dist.barrier(group=self.group)
+
     def all_to_all(self, send, send_splits, recv_splits):
         """One all-to-all of a 1-D tensor: send_splits[r] elements to rank r (in rank order),
         recv_splits[r] elements from rank r.  NCCL over NVLink on GPUs, gloo on CPU."""
@@ -177,6 +197,25 @@ class LibBackend:
         self._keep_s = states_in
         self.pf._check(self.pf.lib().pf_cross_pull_finish(self.h, states_in.data_ptr()), self.h)
 
+    # peer-memory exchange (include/pf.h pf_peer_* / pf_cross_peer)
+    def peer_export(self):
+        hd = np.zeros(self.pf.PF_IPC_HANDLE_BYTES, np.uint8)
+        off = np.zeros(1, np.uint64)
+        self.pf._check(self.pf.lib().pf_peer_export(self.h, hd.ctypes.data, off.ctypes.data), self.h)
+        return hd.tobytes(), int(off[0])
+
+    def peer_open(self, handles, offsets):
+        hd = np.frombuffer(b"".join(handles), np.uint8).copy()
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        self.pf._check(self.pf.lib().pf_peer_open(self.h, hd.ctypes.data, off.ctypes.data), self.h)
+
+    def peer_set(self, workspaces):
+        ws = np.ascontiguousarray(workspaces, dtype=np.uint64)
+        self.pf._check(self.pf.lib().pf_peer_set(self.h, ws.ctypes.data), self.h)
+
+    def cross_peer(self):
+        self.pf._check(self.pf.lib().pf_cross_peer(self.h), self.h)
+
     def step_local_dev(self, y_dev):
         self.pf._check(self.pf.lib().pf_step_local(self.h, None, y_dev.data_ptr()), self.h)
         p = ctypes.c_void_p()
@@ -223,9 +262,13 @@ def sharded_step(backend, transport, y, y_dev=None, exchange: str = "pairwise") 
     """One collective time step on this rank (every rank calls it with the same y; with
     y_dev the observation is read from device memory).  exchange: "pairwise" (L rounds of
     whole-buffer swaps with the butterfly partner) or "pull" (one all-to-all of exactly
-    the states each rank's outputs read)."""
+    the states each rank's outputs read) or "peer" (one kernel reads them straight from
+    the owners' memory over NVLink; peer_connect first)."""
     rec = backend.step_local(y) if y_dev is None else backend.step_local_dev(y_dev)
     backend.step_top(transport.allgather(rec))
+    if exchange == "peer":
+        peer_exchange(backend, transport)
+        return
     if exchange == "pull":
         pull_exchange(backend, transport)
         return
@@ -251,6 +294,34 @@ def pull_exchange(backend, transport) -> None:
     sb = 4 * backend.d                                   # state bytes
     states = transport.all_to_all(served, asked * sb, counts * sb)
     backend.pull_finish(states)
+
+
+def peer_connect(backend, transport) -> None:
+    """Set-up of the peer-memory exchange: all-gather every rank's (IPC handle, offset) and
+    map the other ranks' workspaces (include/pf.h pf_peer_export / pf_peer_open)."""
+    got = transport.allgather_object(backend.peer_export())
+    backend.peer_open([g[0] for g in got], [g[1] for g in got])
+
+
+def peer_exchange(backend, transport) -> None:
+    """The L cross stages as one peer-memory gather (pf_cross_peer).  Every rank's
+    stage-S_loc states are complete before any rank reads them: the record all-gather
+    that precedes pf_step_top completes only after every rank's local passes.  A device
+    barrier after the gather keeps every rank's next step from overwriting them early."""
+    backend.cross_peer()
+    transport.device_barrier(getattr(backend, "stream", None))
+
+
+def loopback_peer(backends: Sequence) -> None:
+    """peer_exchange for G shards on one GPU: every shard maps the others' workspaces by
+    address; the G gathers are independent stream-ordered kernels."""
+    ws = [b.ws_ptr for b in backends]
+    for b in backends:
+        if getattr(b, "_peer_ws", None) != ws:
+            b.peer_set(ws)
+            b._peer_ws = ws
+    for b in backends:
+        b.cross_peer()
 
 
 def transport_device(transport):
@@ -292,6 +363,9 @@ def loopback_step(backends: Sequence, y, exchange: str = "pairwise") -> None:
         b.step_top(allr)
     if exchange == "pull":
         loopback_pull(backends)
+        return
+    if exchange == "peer":
+        loopback_peer(backends)
         return
     world = len(backends)
     L = world.bit_length() - 1

@@ -92,6 +92,10 @@ def lib() -> ctypes.CDLL:
         L.pf_cross_pull_serve.argtypes = [vp, vp, u64, ctypes.POINTER(vp)]
         L.pf_cross_pull_finish.argtypes = [vp, vp]
         L.pf_rotation_offset.argtypes = [vp]
+        L.pf_peer_export.argtypes = [vp, vp, vp]
+        L.pf_peer_open.argtypes = [vp, vp, vp]
+        L.pf_peer_set.argtypes = [vp, vp]
+        L.pf_cross_peer.argtypes = [vp]
         _lib = L
     return _lib
 
@@ -102,7 +106,8 @@ EXPORTED = ["pf_workspace_bytes", "pf_init", "pf_step", "pf_step_dev", "pf_estim
             "pf_step_local", "pf_shard_record", "pf_step_top", "pf_cross_buffer", "pf_cross_stage",
             "pf_set_adaptive", "pf_last_stages", "pf_set_airpf", "pf_set_multinomial", "pf_set_rotation",
             "pf_rotation_offset", "pf_cross_pull_plan", "pf_cross_pull_pack", "pf_cross_pull_serve",
-            "pf_cross_pull_finish"]
+            "pf_cross_pull_finish", "pf_peer_export", "pf_peer_open", "pf_peer_set", "pf_cross_peer"]
+PF_IPC_HANDLE_BYTES = 64
 PF_KERNEL_KINDS = 5
 KERNEL_NAMES = ("k_pass1", "k_cascade", "k_stages", "k_top", "k_cross")
 

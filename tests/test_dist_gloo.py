@@ -3,9 +3,13 @@ world_size = 2 over gloo on CPU.  The per-shard compute is a CPU stand-in built 
 oracle (test infrastructure), so this checks the collective sequence itself: records
 gathered in rank order, butterfly partners, every cross-stage source lies in the own or
 the partner shard, the exchanged buffers, and the final shards = the oracle's x_hat; and
-the pull exchange (composed sources, one all-to-all of requests, one of states)."""
+the pull exchange (composed sources, one all-to-all of requests, one of states); and the
+peer exchange (handles all-gathered in rank order, every rank reads the owners' state
+buffers in place -- stood in for by shared memory-mapped files -- and the barrier keeps
+a fast rank from overwriting its buffer before the others have read it)."""
 import os
 import socket
+import time
 
 import numpy as np
 import pytest
@@ -36,7 +40,7 @@ def test_partners_and_schedule():
 class OracleShard:
     """CPU stand-in for LibBackend: one shard's view of the oracle's full step."""
 
-    def __init__(self, params, N, M, seed, rank, world):
+    def __init__(self, params, N, M, seed, rank, world, peer_dir=None):
         from oracle import oracle as orc
         self.orc = orc
         self.params, self.N, self.M, self.seed = params, N, M, seed
@@ -50,6 +54,10 @@ class OracleShard:
         self.pos0 = rank * self.nloc
         self.xhat = orc.init(params, N, seed).astype(np.float32)
         self.n = 0
+        self.peer_dir = peer_dir
+        if peer_dir:  # this shard's "workspace": the state buffer other ranks read in place
+            self.mine = np.lib.format.open_memmap(os.path.join(peer_dir, f"ws{rank}.npy"), mode="w+",
+                                                  dtype=np.float32, shape=(self.nloc, self.d))
 
     def _states_at(self, s):
         """Full-problem states at stage s positions: x[a_1(...a_s(i))]."""
@@ -62,6 +70,9 @@ class OracleShard:
         self.r = self.orc.step(self.params, self.N, self.M, self.seed, self.n, y, self.xhat)
         self.stage = self.Sloc
         self.buf = self._states_at(self.Sloc)[self.pos0: self.pos0 + self.nloc].copy()
+        if self.peer_dir:
+            self.mine[:] = self.buf
+            self.mine.flush()
         lv = self.r["logV"][self.orc.level_offset(self.m, self.Sloc) + self.rank]
         return torch.tensor([lv] + [0.0] * (2 + 4 * self.d), dtype=torch.float64)
 
@@ -115,6 +126,23 @@ class OracleShard:
         out[self.outpos] = st
         self.buf = out
 
+    # peer exchange (dist.peer_connect / dist.peer_exchange)
+    def peer_export(self):
+        name = f"ws{self.rank}.npy".encode()
+        return name.ljust(64, b"\0"), 0
+
+    def peer_open(self, handles, offsets):
+        assert len(handles) == self.world and all(o == 0 for o in offsets)
+        names = [h.rstrip(b"\0").decode() for h in handles]
+        assert names == [f"ws{q}.npy" for q in range(self.world)], "handles not gathered in rank order"
+        self.peers = [np.load(os.path.join(self.peer_dir, nm), mmap_mode="r") for nm in names]
+
+    def cross_peer(self):
+        if self.rank:  # rank 0 runs ahead: without the barrier it overwrites its buffer early
+            time.sleep(0.3)
+        self.pull_plan()
+        self.buf = np.stack([np.array(self.peers[o][l]) for o, l in zip(self.src_owner, self.src_local)])
+
     def finish(self):
         full = self.r["xhat"].astype(np.float32)
         assert np.array_equal(self.buf, full[self.pos0: self.pos0 + self.nloc])
@@ -122,7 +150,7 @@ class OracleShard:
         self.n += 1
 
 
-def _worker(rank, world, port, q, exchange="pairwise"):
+def _worker(rank, world, port, q, exchange="pairwise", peer_dir=None):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -130,8 +158,11 @@ def _worker(rank, world, port, q, exchange="pairwise"):
         cfg = inputs.CONFIGS["C1"]
         params = inputs.model_params(cfg)
         N, M = 256, 16
-        be = OracleShard(params, N, M, 5, rank, world)
+        be = OracleShard(params, N, M, 5, rank, world, peer_dir=peer_dir)
         tr = pfd.TorchTransport()
+        if exchange == "peer":
+            dist.barrier()  # every rank's buffer file exists
+            pfd.peer_connect(be, tr)
         _, ys = inputs.simulate(cfg, T=3)
         for y in ys:
             pfd.sharded_step(be, tr, y, exchange=exchange)
@@ -151,12 +182,14 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world,exchange", [(2, "pairwise"), (4, "pairwise"), (2, "pull"), (4, "pull")])
-def test_gloo_sharded_sequence(world, exchange):
+@pytest.mark.parametrize("world,exchange", [(2, "pairwise"), (4, "pairwise"), (2, "pull"), (4, "pull"),
+                                            (2, "peer"), (4, "peer")])
+def test_gloo_sharded_sequence(world, exchange, tmp_path):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, exchange)) for r in range(world)]
+    peer_dir = str(tmp_path) if exchange == "peer" else None
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, exchange, peer_dir)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)

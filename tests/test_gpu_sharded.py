@@ -16,7 +16,7 @@ from paper_1812_01502_b200 import dist as pfd  # noqa: E402
 from paper_1812_01502_b200 import pf as pfb  # noqa: E402
 
 
-@pytest.mark.parametrize("exchange", ["pairwise", "pull"])
+@pytest.mark.parametrize("exchange", ["pairwise", "pull", "peer"])
 @pytest.mark.parametrize("name,N,M,G", [("C4", 1 << 16, 64, 2), ("C4", 1 << 16, 64, 4), ("C3", 1 << 15, 32, 4),
                                         ("C2", 1 << 15, 256, 2), ("C3", 1 << 12, 2, 8), ("C1", 1024, 64, 8)])
 def test_loopback_matches_single_gpu(name, N, M, G, exchange):

@@ -1,5 +1,5 @@
 """Projection of the sharded step on one GPU: G shards of a configuration run back to back
-through the loopback transport (python tools/loopback_bench.py C4 8 [pull|pairwise] [steps]).
+through the loopback transport (python tools/loopback_bench.py C4 8 [pull|pairwise|peer] [steps]).
 Reports the device time per step summed over the shards, per kernel kind, and the bytes the
 exchange would move between GPUs; a projection only (no NVLink, shards serialised)."""
 import os
