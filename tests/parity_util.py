@@ -19,14 +19,16 @@ BOUNDARY = 1e-6
 def check_x(x_gpu, x_orc):
     x_gpu = np.asarray(x_gpu, np.float64).reshape(x_orc.shape)
     same_nonfinite = (~np.isfinite(x_orc)) & ((x_gpu == x_orc) | (np.isnan(x_gpu) & np.isnan(x_orc)))
-    err = np.where(same_nonfinite, 0.0, np.abs(x_gpu - x_orc) / (1.0 + np.abs(x_orc)))
+    with np.errstate(invalid="ignore"):  # inf - inf where both sides agree (masked out)
+        err = np.where(same_nonfinite, 0.0, np.abs(x_gpu - x_orc) / (1.0 + np.abs(x_orc)))
     assert np.all(err <= 1e-5), f"x mismatch: max rel err {err.max():.3g}"
 
 
 def check_lw(lw_gpu, lw_orc):
     lw_gpu = np.asarray(lw_gpu, np.float64)
     both_inf = np.isneginf(lw_gpu) & np.isneginf(lw_orc)
-    err = np.where(both_inf, 0.0, np.abs(lw_gpu - lw_orc) / (1.0 + np.abs(lw_orc)))
+    with np.errstate(invalid="ignore"):  # -inf - -inf where both sides agree (masked out)
+        err = np.where(both_inf, 0.0, np.abs(lw_gpu - lw_orc) / (1.0 + np.abs(lw_orc)))
     assert np.all(err <= 1e-5), f"log-weight mismatch: max rel err {np.nanmax(err):.3g}"
 
 

@@ -44,3 +44,28 @@ def test_loopback_matches_single_gpu(name, N, M, G, exchange):
     single.close()
     for b in shards:
         b.close()
+
+
+def test_peer_exchange_errors():
+    cfg = inputs.CONFIGS["C1"]
+    p = inputs.model_params(cfg)
+    N, M, G = 1024, 16, 2
+    shards = [pfd.LibBackend(p, N, M, 3, r, G) for r in range(G)]
+    _, ys = inputs.simulate(cfg, T=1)
+    recs = [b.step_local(ys[0]) for b in shards]
+    allr = torch.stack(recs)
+    for b in shards:
+        b.step_top(allr)
+    with pytest.raises(pfb.PFError):  # no mapping yet
+        shards[0].cross_peer()
+    with pytest.raises(pfb.PFError):  # [rank] must be the own workspace
+        shards[0].peer_set([shards[1].ws_ptr, shards[1].ws_ptr])
+    with pytest.raises(pfb.PFError):  # NULL peer
+        shards[0].peer_set([shards[0].ws_ptr, 0])
+    pfd.loopback_peer(shards)  # now mapped: runs
+    single = pfb.ParticleFilter(p, N, M, 3)
+    with pytest.raises(pfb.PFError):  # not a sharded handle
+        pfb._check(pfb.lib().pf_cross_peer(single.h), single.h)
+    single.close()
+    for b in shards:
+        b.close()
