@@ -913,6 +913,8 @@ static int init_core(const pf_model* model, uint64_t N, uint32_t M, uint64_t see
     h->last_launches = 0;
     h->timing = false;
     cudaMemsetAsync(h->at<uint32_t>(L.ticket), 0, 16, h->stream);
+    if (flags & (PF_FLAG_ADAPTIVE | PF_FLAG_MULTINOMIAL))
+        cudaMemsetAsync(h->at<uint32_t>(L.ess_lmax), 0, 16, h->stream);  // running max, reset after each use
     {
         InitArgs ia;
         ia.mp = h->mp;

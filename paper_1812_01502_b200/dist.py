@@ -122,7 +122,9 @@ class LibBackend:
     """One shard on the current GPU through the C-ABI (libpf.so)."""
 
     def __init__(self, params: dict, N: int, M: int, seed: int, rank: int, world: int, debug: bool = False,
-                 stream=None):
+                 stream=None, poison: Optional[int] = None):
+        """poison (a byte, checking aid): as pf.ParticleFilter -- fill the workspace before
+        pf_init_sharded and keep a guard band behind it (guard_intact())."""
         import torch
 
         from . import pf
@@ -139,9 +141,14 @@ class LibBackend:
         nbytes = int(L.pf_workspace_bytes_sharded(ctypes.byref(m), self.N, self.M, self.flags, self.world))
         if nbytes == 0:
             raise pf.PFError(pf.PF_EINVAL, "invalid sharded topology")
-        self.ws = torch.empty(nbytes + 256, dtype=torch.uint8, device="cuda")
+        self._guard = pf.GUARD_BYTES if poison is not None else 0
+        self.ws = torch.empty(nbytes + 256 + self._guard, dtype=torch.uint8, device="cuda")
+        if poison is not None:
+            self.ws.fill_(int(poison) & 0xFF)
+            self._poison = int(poison) & 0xFF
         base = self.ws.data_ptr()
         self.ws_ptr = base + ((-base) % 256)
+        self.ws_bytes = nbytes
         h = ctypes.c_void_p()
         pf._check(L.pf_init_sharded(ctypes.byref(m), self.N, self.M, seed, self.flags, self.rank, self.world,
                                     self.ws_ptr, nbytes, self.stream.cuda_stream, ctypes.byref(h)))
@@ -250,6 +257,13 @@ class LibBackend:
             raise ValueError(what)
         self.stream.synchronize()
         return t.cpu().numpy()
+
+    def guard_intact(self) -> bool:
+        if not self._guard:
+            return True
+        self.stream.synchronize()
+        off = self.ws_ptr - self.ws.data_ptr() + self.ws_bytes
+        return bool((self.ws[off: off + self._guard] == self._poison).all().item())
 
     def close(self):
         if getattr(self, "h", None) is not None:

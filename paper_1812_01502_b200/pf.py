@@ -108,6 +108,7 @@ EXPORTED = ["pf_workspace_bytes", "pf_init", "pf_step", "pf_step_dev", "pf_estim
             "pf_rotation_offset", "pf_cross_pull_plan", "pf_cross_pull_pack", "pf_cross_pull_serve",
             "pf_cross_pull_finish", "pf_peer_export", "pf_peer_open", "pf_peer_set", "pf_cross_peer"]
 PF_IPC_HANDLE_BYTES = 64
+GUARD_BYTES = 1 << 16  # guard band behind a poisoned workspace (ParticleFilter(poison=...))
 PF_KERNEL_KINDS = 5
 KERNEL_NAMES = ("k_pass1", "k_cascade", "k_stages", "k_top", "k_cross")
 
@@ -203,11 +204,13 @@ class ParticleFilter:
 
     def __init__(self, params: dict, N: int, M: int, seed: int, debug: bool = False, device: str = "cuda",
                  stream=None, theta: float = 0.0, airpf: int = 0, multinomial: bool = False,
-                 rotate: bool = False):
+                 rotate: bool = False, poison: Optional[int] = None):
         """theta > 0: fully adapted augmented resampling with ESS threshold theta
         (pf_set_adaptive); airpf = 1 (Alg. 7) or 2 (Alg. 6): AIRPF (pf_set_airpf);
         multinomial: the plain BPF, Alg. 2 (pf_set_multinomial); rotate (with theta): stage
-        rotation (pf_set_rotation).  The handle then reserves the buffers of that scheme."""
+        rotation (pf_set_rotation).  The handle then reserves the buffers of that scheme.
+        poison (a byte, checking aid): fill the workspace with it before pf_init and keep
+        a guard band behind it (guard_intact()) -- results must not depend on the byte."""
         import torch
 
         self.torch = torch
@@ -224,7 +227,11 @@ class ParticleFilter:
         nbytes = pf_workspace_bytes(params, self.N, self.M, self.flags)
         if nbytes == 0:
             raise PFError(PF_EINVAL, "invalid model/topology (pf_workspace_bytes returned 0)")
-        self.ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        self._guard = GUARD_BYTES if poison is not None else 0
+        self.ws = torch.empty(nbytes + 256 + self._guard, dtype=torch.uint8, device=self.device)
+        if poison is not None:
+            self.ws.fill_(int(poison) & 0xFF)
+            self._poison = int(poison) & 0xFF
         base = self.ws.data_ptr()
         self._off = (-base) % 256
         self.ws_ptr = base + self._off
@@ -238,6 +245,14 @@ class ParticleFilter:
             pf_set_airpf(self.h, airpf)
         if multinomial:
             pf_set_multinomial(self.h, True)
+
+    def guard_intact(self) -> bool:
+        """With poison: the guard band behind the workspace still holds the poison byte."""
+        if not self._guard:
+            return True
+        self.stream.synchronize()
+        tail = self.ws[self._off + self.ws_bytes: self._off + self.ws_bytes + self._guard]
+        return bool((tail == self._poison).all().item())
 
     def rotation_offset(self) -> int:
         return int(lib().pf_rotation_offset(self.h))
