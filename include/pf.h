@@ -70,6 +70,10 @@ typedef struct pf_handle pf_handle;
                                    one GPU): 8 N bytes + O(N/1024) */
 #define PF_FLAG_AIRPF 4u /* reserve the island buffers of AIRPF (pf_set_airpf; one GPU, M >= 4):
                             13 N/M + S N/(4M) bytes */
+#define PF_FLAG_GUARD 16u /* checking aid: a PF_GUARD_BYTES gap after every workspace region
+                            (fill the workspace before pf_init; pf_guard_check counts the gap
+                            bytes a step overwrote) */
+#define PF_GUARD_BYTES 4096
 
 /* Bytes of device workspace pf_init needs for this problem (0 if invalid). */
 size_t pf_workspace_bytes(const pf_model* model, uint64_t N, uint32_t M, uint32_t flags);
@@ -253,6 +257,12 @@ int pf_peer_export(pf_handle* h, void* ipc_handle, uint64_t* offset);
 int pf_peer_open(pf_handle* h, const void* ipc_handles, const uint64_t* offsets);
 int pf_peer_set(pf_handle* h, const uint64_t* dev_workspaces);
 int pf_cross_peer(pf_handle* h);
+
+/* PF_FLAG_GUARD handles: count the bytes of the inter-region gaps that differ from
+ * `fill` (the byte the caller filled the workspace with before pf_init).  A nonzero
+ * count means some kernel wrote outside its region.  Synchronises.  Errors: PF_EINVAL,
+ * PF_ESTATE (no PF_FLAG_GUARD), PF_ECUDA. */
+int pf_guard_check(pf_handle* h, unsigned char fill, uint64_t* bad_bytes);
 
 /* --- debug / test exports (parity harness) ------------------------------------ */
 #define PF_DBG_X 1         /* x_n before resampling, N x d fp32 (needs PF_FLAG_DEBUG) */

@@ -207,15 +207,22 @@ struct Layout {
     size_t shard_rec, recs, top_logV, top_thr, top_scratch;
     size_t pull_src, pull_rank, pull_counts, pull_fill, pull_off, pull_req, pull_outpos, pull_serve;  // world > 1
     size_t dbg_x, dbg_lw, dbg_anc, dbg_A;
+    size_t guard_count;                // PF_FLAG_GUARD
+    std::vector<size_t> gaps;          // PF_FLAG_GUARD: offsets of the PF_GUARD_BYTES gaps
     size_t total;
 };
 
 Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags, uint32_t world, int Sglobal) {
     Layout L;
     size_t off = 0;
+    const bool guard = flags & PF_FLAG_GUARD;
     auto take = [&](size_t bytes) {
         const size_t o = off;
         off = align256(off + bytes);
+        if (guard) {  // a gap behind every region (PF_GUARD_BYTES is a multiple of 256)
+            L.gaps.push_back(off);
+            off += PF_GUARD_BYTES;
+        }
         return o;
     };
     const uint64_t m = N / M;
@@ -269,6 +276,7 @@ Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags, uint32
     L.dbg_anc = take(dbg ? (size_t)N * Sglobal * 4 : 0);
     (void)S;
     L.dbg_A = take(dbg ? N * 4 : 0);
+    L.guard_count = take(guard ? 16 : 0);
     L.total = off;
     return L;
 }
@@ -1189,6 +1197,20 @@ int pf_cross_peer(pf_handle* h) {
     h->mark(PF_KERNEL_CROSS, false);
     h->cur ^= 1;
     return check_cuda(h, "pf_cross_peer");
+}
+
+int pf_guard_check(pf_handle* h, unsigned char fill, uint64_t* bad_bytes) {
+    if (!h || !bad_bytes) return fail(h, PF_EINVAL, "NULL argument");
+    if (!(h->flags & PF_FLAG_GUARD)) return fail(h, PF_ESTATE, "handle not created with PF_FLAG_GUARD");
+    unsigned long long* cnt = h->at<unsigned long long>(h->lay.guard_count);
+    cudaMemsetAsync(cnt, 0, 8, h->stream);
+    for (size_t g : h->lay.gaps) launch_guard_check(h->stream, h->ws + g, PF_GUARD_BYTES, fill, cnt);
+    unsigned long long bad = 0;
+    cudaError_t e = cudaMemcpyAsync(&bad, cnt, 8, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_guard_check: ") + cudaGetErrorString(e));
+    *bad_bytes = bad;
+    return check_cuda(h, "pf_guard_check");
 }
 
 int pf_step(pf_handle* h, const float* y_host) {

@@ -363,6 +363,20 @@ void launch_peer_gather(cudaStream_t st, int D, const PullArgs& a, const PeerArg
     if (debug) k_pull_debug_tables<<<grid, 256, 0, st>>>(a);
 }
 
+// PF_FLAG_GUARD: count the gap bytes that differ from the fill byte
+__global__ void __launch_bounds__(256) k_guard_check(const unsigned char* __restrict__ p, size_t n, unsigned char fill,
+                                                     unsigned long long* bad) {
+    unsigned int c = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        c += p[i] != fill;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31u) == 0u && c) atomicAdd(bad, (unsigned long long)c);
+}
+
+void launch_guard_check(cudaStream_t st, const unsigned char* p, size_t n, unsigned char fill, unsigned long long* bad) {
+    k_guard_check<<<(uint32_t)((n + 255) / 256), 256, 0, st>>>(p, n, fill, bad);
+}
+
 void launch_pull_compose(cudaStream_t st, const PullArgs& a, bool debug) {
     const uint32_t grid = (uint32_t)std::min<uint64_t>((a.Nloc + 255) / 256, 148ull * 8);
     k_pull_compose<<<grid, 256, 0, st>>>(a);

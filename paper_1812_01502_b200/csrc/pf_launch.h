@@ -46,6 +46,7 @@ void launch_ess(const LaunchCfg& chunks, const EssArgs& a);
 void launch_island(cudaStream_t st, const IslandArgs& a);
 void launch_pull_compose(cudaStream_t st, const PullArgs& a, bool debug);
 void launch_pull_pack(cudaStream_t st, const PullArgs& a);
+void launch_guard_check(cudaStream_t st, const unsigned char* p, size_t n, unsigned char fill, unsigned long long* bad);
 void launch_peer_gather(cudaStream_t st, int D, const PullArgs& a, const PeerArgs& p, bool debug);
 void launch_pull_move(cudaStream_t st, int D, bool gather, const float* src, const uint32_t* idx, float* dst,
                       uint64_t n);

@@ -134,7 +134,7 @@ class LibBackend:
         self.params = params
         self.N, self.M, self.rank, self.world = int(N), int(M), int(rank), int(world)
         self.d = int(params["d"])
-        self.flags = pf.PF_FLAG_DEBUG if debug else 0
+        self.flags = (pf.PF_FLAG_DEBUG if debug else 0) | (pf.PF_FLAG_GUARD if poison is not None else 0)
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         L = pf.lib()
         m, keep = pf.make_model(params)
@@ -261,9 +261,10 @@ class LibBackend:
     def guard_intact(self) -> bool:
         if not self._guard:
             return True
-        self.stream.synchronize()
+        bad = np.zeros(1, np.uint64)
+        self.pf._check(self.pf.lib().pf_guard_check(self.h, self._poison, bad.ctypes.data), self.h)
         off = self.ws_ptr - self.ws.data_ptr() + self.ws_bytes
-        return bool((self.ws[off: off + self._guard] == self._poison).all().item())
+        return int(bad[0]) == 0 and bool((self.ws[off: off + self._guard] == self._poison).all().item())
 
     def close(self):
         if getattr(self, "h", None) is not None:

@@ -24,6 +24,7 @@ PF_FLAG_DEBUG = 1
 PF_FLAG_ADAPTIVE = 2
 PF_FLAG_AIRPF = 4
 PF_FLAG_MULTINOMIAL = 8
+PF_FLAG_GUARD = 16
 PF_PHI_X, PF_PHI_X2 = 1, 2
 PF_EST_FILTER, PF_EST_PREDICT = 1, 2
 PF_DBG_X, PF_DBG_LOGW, PF_DBG_ANC_STAGE, PF_DBG_ANC_FINAL, PF_DBG_XHAT, PF_DBG_LOGV, PF_DBG_THRESH = 1, 2, 3, 4, 5, 6, 7
@@ -96,6 +97,7 @@ def lib() -> ctypes.CDLL:
         L.pf_peer_open.argtypes = [vp, vp, vp]
         L.pf_peer_set.argtypes = [vp, vp]
         L.pf_cross_peer.argtypes = [vp]
+        L.pf_guard_check.argtypes = [vp, ctypes.c_ubyte, vp]
         _lib = L
     return _lib
 
@@ -106,7 +108,8 @@ EXPORTED = ["pf_workspace_bytes", "pf_init", "pf_step", "pf_step_dev", "pf_estim
             "pf_step_local", "pf_shard_record", "pf_step_top", "pf_cross_buffer", "pf_cross_stage",
             "pf_set_adaptive", "pf_last_stages", "pf_set_airpf", "pf_set_multinomial", "pf_set_rotation",
             "pf_rotation_offset", "pf_cross_pull_plan", "pf_cross_pull_pack", "pf_cross_pull_serve",
-            "pf_cross_pull_finish", "pf_peer_export", "pf_peer_open", "pf_peer_set", "pf_cross_peer"]
+            "pf_cross_pull_finish", "pf_peer_export", "pf_peer_open", "pf_peer_set", "pf_cross_peer",
+            "pf_guard_check"]
 PF_IPC_HANDLE_BYTES = 64
 GUARD_BYTES = 1 << 16  # guard band behind a poisoned workspace (ParticleFilter(poison=...))
 PF_KERNEL_KINDS = 5
@@ -209,8 +212,9 @@ class ParticleFilter:
         (pf_set_adaptive); airpf = 1 (Alg. 7) or 2 (Alg. 6): AIRPF (pf_set_airpf);
         multinomial: the plain BPF, Alg. 2 (pf_set_multinomial); rotate (with theta): stage
         rotation (pf_set_rotation).  The handle then reserves the buffers of that scheme.
-        poison (a byte, checking aid): fill the workspace with it before pf_init and keep
-        a guard band behind it (guard_intact()) -- results must not depend on the byte."""
+        poison (a byte, checking aid): fill the workspace with it before pf_init, with a
+        gap after every region (PF_FLAG_GUARD) and a band behind it (guard_intact()) --
+        results must not depend on the byte."""
         import torch
 
         self.torch = torch
@@ -221,7 +225,8 @@ class ParticleFilter:
         self.m = self.N // self.M
         self.S = int(round(np.log2(self.m)))
         self.flags = ((PF_FLAG_DEBUG if debug else 0) | (PF_FLAG_ADAPTIVE if theta > 0 else 0) |
-                      (PF_FLAG_AIRPF if airpf else 0) | (PF_FLAG_MULTINOMIAL if multinomial else 0))
+                      (PF_FLAG_AIRPF if airpf else 0) | (PF_FLAG_MULTINOMIAL if multinomial else 0) |
+                      (PF_FLAG_GUARD if poison is not None else 0))
         self.device = torch.device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         nbytes = pf_workspace_bytes(params, self.N, self.M, self.flags)
@@ -247,12 +252,14 @@ class ParticleFilter:
             pf_set_multinomial(self.h, True)
 
     def guard_intact(self) -> bool:
-        """With poison: the guard band behind the workspace still holds the poison byte."""
+        """With poison: the gaps between the workspace regions (PF_FLAG_GUARD, pf_guard_check)
+        and the band behind the workspace still hold the poison byte."""
         if not self._guard:
             return True
-        self.stream.synchronize()
+        bad = np.zeros(1, np.uint64)
+        _check(lib().pf_guard_check(self.h, self._poison, bad.ctypes.data), self.h)
         tail = self.ws[self._off + self.ws_bytes: self._off + self.ws_bytes + self._guard]
-        return bool((tail == self._poison).all().item())
+        return int(bad[0]) == 0 and bool((tail == self._poison).all().item())
 
     def rotation_offset(self) -> int:
         return int(lib().pf_rotation_offset(self.h))

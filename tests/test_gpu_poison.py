@@ -1,8 +1,9 @@
 """Memory-safety checks without compute-sanitizer (closed on this GPU pool): every step
 variant runs on workspaces pre-filled with different bytes (0x00, 0xFF = NaN patterns,
 0x7F) and must give BITWISE the same estimates and particles -- a read of a workspace byte
-the step never wrote would make the result depend on the fill -- and must leave a 64 KiB
-guard band behind the workspace untouched (no write past its end).  Sizes span several
+the step never wrote would make the result depend on the fill -- and must leave untouched
+the 4 KiB gaps PF_FLAG_GUARD puts after every workspace region (pf_guard_check: no kernel
+writes outside its buffer) and a 64 KiB band behind the workspace.  Sizes span several
 tiles, the smallest and largest M of the configs, and d = 1, 4, 8."""
 import numpy as np
 import pytest
@@ -93,3 +94,22 @@ def test_sharded_fill_independent_and_guard(exchange, name, N, M):
             continue
         for a, b in zip(ref, out):
             assert np.array_equal(a, b), f"sharded result depends on the workspace fill ({fill:#x})"
+
+
+def test_guard_check_detects_a_stray_write():
+    cfg = inputs.CONFIGS["C1"]
+    p = inputs.model_params(cfg)
+    f = pfb.ParticleFilter(p, 1024, 64, 8, poison=0x5A)
+    f.step(np.array([0.3], np.float32))
+    assert f.guard_intact()
+    xb = 1024 * 1 * 4  # X0 is the first region (N x d fp32); its gap follows it
+    f.ws[f._off + xb + 17] = 0x00
+    assert not f.guard_intact()
+    bad = np.zeros(1, np.uint64)
+    pfb._check(pfb.lib().pf_guard_check(f.h, 0x5A, bad.ctypes.data), f.h)
+    assert int(bad[0]) == 1
+    f.close()
+    g = pfb.ParticleFilter(p, 1024, 64, 8)
+    with pytest.raises(pfb.PFError):  # no PF_FLAG_GUARD
+        pfb._check(pfb.lib().pf_guard_check(g.h, 0, bad.ctypes.data), g.h)
+    g.close()
