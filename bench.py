@@ -304,7 +304,8 @@ def run_ours(args):
         alg = algorithmic_bytes(cfg_loc, dom)
         achieved = alg / (dom_ms / dom_n / 1e3) / 1e9
         peak, peak_src = measured_peak()
-        plain = not (args.theta or args.airpf or args.multinomial)  # the ncu figures are the plain step's
+        # the ncu figures are the plain one-GPU step's (per launch at the full N)
+        plain = not (args.theta or args.airpf or args.multinomial) and world == 1
         roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(cfg, dom) if plain else None,
                     "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
