@@ -164,12 +164,17 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- ours
-def algorithmic_bytes(cfg, kernel: str) -> float:
+NVLINK_PEER_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction per GPU (900 nominal)
+
+
+def algorithmic_bytes(cfg, kernel: str, exchange: str = "pairwise") -> float:
     """Algorithmic HBM bytes per launch: the bytes the kernel must move
     once, with no sector amplification and no re-reads.  cfg: this rank's shard."""
     N, d = cfg.N, cfg.d
     if kernel in ("k_pass1", "k_stages"):
         return N * 8 * d   # read the tile's states once, write them once
+    if kernel == "k_cross" and exchange == "peer":
+        return N * 8 * d   # every output's state read once (mostly from peers) and written once
     if kernel == "k_cross":
         return N * 8 * d + N * 4 * d  # own read + write, partner half on average
     if kernel in ("k_cascade", "k_top"):
@@ -301,7 +306,8 @@ def run_ours(args):
         dom = max(kt, key=lambda k: kt[k][0])
         dom_ms, dom_n = kt[dom]
         cfg_loc = cfg.with_sizes(cfg.M, cfg.m // world)
-        alg = algorithmic_bytes(cfg_loc, dom)
+        exch = args.exchange if world > 1 else ""
+        alg = algorithmic_bytes(cfg_loc, dom, exch)
         achieved = alg / (dom_ms / dom_n / 1e3) / 1e9
         peak, peak_src = measured_peak()
         # the ncu figures are the plain one-GPU step's (per launch at the full N)
@@ -311,13 +317,25 @@ def run_ours(args):
                     "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
                     "kernel_share_of_step": round(dom_ms / max(sum(v[0] for v in kt.values()), 1e-9), 3),
                     "step_alg_bytes_frac": round(value / world * 8 * cfg.d / 1e9 / peak, 4)}
+        # peer exchange: bytes that must cross NVLink per launch = the states read from the
+        # other ranks, (1 - 1/G) of the shard's outputs on average
+        nvl_bytes = cfg_loc.N * 4 * cfg.d * (1 - 1 / world) if exch == "peer" else 0.0
+        if dom == "k_cross" and nvl_bytes:
+            nv = nvl_bytes / (dom_ms / dom_n / 1e3) / 1e9
+            roofline.update({"bound": "nvlink", "achieved": round(nv, 1), "peak": NVLINK_PEER_GBS,
+                             "frac": round(nv / NVLINK_PEER_GBS, 4), "traffic": None,
+                             "algorithmic_bytes_per_launch": nvl_bytes,
+                             "peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)"})
         kernels = {k: {"ms_per_launch": round(v[0] / max(v[1], 1), 4), "launches": v[1]} for k, v in kt.items()}
+        if nvl_bytes and "k_cross" in kernels and kernels["k_cross"]["ms_per_launch"] > 0:
+            kernels["k_cross"]["nvlink_frac"] = round(
+                nvl_bytes / (kernels["k_cross"]["ms_per_launch"] / 1e3) / 1e9 / NVLINK_PEER_GBS, 4)
         # per kernel: HBM fraction (algorithmic bytes) and issue fraction (ncu instruction count)
         for k, v in kernels.items():
             sec = v["ms_per_launch"] / 1e3
             if sec <= 0:
                 continue
-            ab = algorithmic_bytes(cfg_loc, k)
+            ab = algorithmic_bytes(cfg_loc, k, exch)
             if ab:
                 v["hbm_frac"] = round(ab / sec / 1e9 / peak, 4)
             wi = ncu_traffic(cfg, k, ":warp_inst")
