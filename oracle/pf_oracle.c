@@ -137,27 +137,32 @@ void orc_init(const orc_model* mdl, uint64_t N, uint64_t seed, double* x0)
 }
 
 /* Alg. 1 l.302-303: zeta_n^i ~ f(zhat_{n-1}^i, .).
- * LG: x = A xhat + LQ z;  SV: x = phi xhat + sigma z.  z from the MUTATE field at n. */
+ * LG: x = A xhat + LQ z;  SV: x = phi xhat + sigma z.  z from the MUTATE field at n.
+ * mutate_one: particle i (global index, the noise counter) from its xhat row. */
+static void mutate_one(const orc_model* mdl, uint64_t seed, uint32_t n, uint64_t i, const double* xh, double* x)
+{
+    int d = mdl->d;
+    double z[8];
+    for (int k = 0; k < d; ++k)
+        z[k] = orc_normal(seed, ORC_DOMAIN_MUTATE, n, i * (uint64_t)d + (uint64_t)k);
+    for (int k = 0; k < d; ++k) {
+        double v;
+        if (mdl->kind == 2) {
+            v = (double)mdl->sv_phi * xh[0] + (double)mdl->sv_sigma * z[0];
+        } else {
+            v = 0.0;
+            for (int j = 0; j < d; ++j) v += (double)mdl->A[k * d + j] * xh[j];
+            for (int j = 0; j < d; ++j) v += (double)mdl->LQ[k * d + j] * z[j];
+        }
+        x[k] = v;
+    }
+}
+
 void orc_mutate(const orc_model* mdl, uint64_t N, uint64_t seed, uint32_t n,
                 const double* xhat, double* x)
 {
     int d = mdl->d;
-    for (uint64_t i = 0; i < N; ++i) {
-        double z[8];
-        for (int k = 0; k < d; ++k)
-            z[k] = orc_normal(seed, ORC_DOMAIN_MUTATE, n, i * (uint64_t)d + (uint64_t)k);
-        for (int k = 0; k < d; ++k) {
-            double v;
-            if (mdl->kind == 2) {
-                v = (double)mdl->sv_phi * xhat[i] + (double)mdl->sv_sigma * z[0];
-            } else {
-                v = 0.0;
-                for (int j = 0; j < d; ++j) v += (double)mdl->A[k * d + j] * xhat[i * d + j];
-                for (int j = 0; j < d; ++j) v += (double)mdl->LQ[k * d + j] * z[j];
-            }
-            x[i * d + k] = v;
-        }
-    }
+    for (uint64_t i = 0; i < N; ++i) mutate_one(mdl, seed, n, i, xhat + i * d, x + i * d);
 }
 
 /* g_n(x) = g(x, y_n), in the log domain with normalising constants
@@ -165,31 +170,35 @@ void orc_mutate(const orc_model* mdl, uint64_t N, uint64_t seed, uint32_t n,
  * LG: log g = -1/2 (y - Hx)^T Rinv (y - Hx).
  * SV: y | x ~ N(0, beta^2 e^x)  =>  log g = -x/2 - y^2 e^{-x} / (2 beta^2).
  * A non-finite result (non-finite x) is -inf. */
+static double logweight_one(const orc_model* mdl, const float* y, const double* x)
+{
+    int d = mdl->d, dy = mdl->dy;
+    double v;
+    if (mdl->kind == 2) {
+        double xv = x[0];
+        double yv = (double)y[0];
+        double beta = (double)mdl->sv_beta;
+        v = -0.5 * xv - yv * yv * exp(-xv) / (2.0 * beta * beta);
+    } else {
+        double r[8];
+        for (int k = 0; k < dy; ++k) {
+            double hx = 0.0;
+            for (int j = 0; j < d; ++j) hx += (double)mdl->H[k * d + j] * x[j];
+            r[k] = (double)y[k] - hx;
+        }
+        double q = 0.0;
+        for (int k = 0; k < dy; ++k)
+            for (int j = 0; j < dy; ++j) q += r[k] * (double)mdl->Rinv[k * dy + j] * r[j];
+        v = -0.5 * q;
+    }
+    return isfinite(v) ? v : -INFINITY;
+}
+
 void orc_logweight(const orc_model* mdl, uint64_t N, const float* y, const double* x,
                    double* lw)
 {
-    int d = mdl->d, dy = mdl->dy;
-    for (uint64_t i = 0; i < N; ++i) {
-        double v;
-        if (mdl->kind == 2) {
-            double xv = x[i];
-            double yv = (double)y[0];
-            double beta = (double)mdl->sv_beta;
-            v = -0.5 * xv - yv * yv * exp(-xv) / (2.0 * beta * beta);
-        } else {
-            double r[8];
-            for (int k = 0; k < dy; ++k) {
-                double hx = 0.0;
-                for (int j = 0; j < d; ++j) hx += (double)mdl->H[k * d + j] * x[i * d + j];
-                r[k] = (double)y[k] - hx;
-            }
-            double q = 0.0;
-            for (int k = 0; k < dy; ++k)
-                for (int j = 0; j < dy; ++j) q += r[k] * (double)mdl->Rinv[k * dy + j] * r[j];
-            v = -0.5 * q;
-        }
-        lw[i] = isfinite(v) ? v : -INFINITY;
-    }
+    int d = mdl->d;
+    for (uint64_t i = 0; i < N; ++i) lw[i] = logweight_one(mdl, y, x + i * d);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -499,6 +508,62 @@ int orc_step(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t seed, uint32
         orc_estimates(d, N, lw, x, Aloc, filt, pred, resamp);
     }
     free(xprev); free(Aloc);
+    return rc;
+}
+
+/* The same step at full size (C4: N = 2^28), checked on sampled outputs: lw for all N
+ * particles (kept), the estimates accumulated in the same pass, then the draws only along
+ * the ancestral paths of the sampled outputs (orc_augmented_resample_sampled) and their
+ * resampled states.  The estimates are Sum g phi / Sum g with the weights shifted by the
+ * running maximum of lw (rescaled whenever it grows): the same quantity as orc_estimates'
+ * shift by the final maximum, in one pass.  Outputs: logV (m - 1), A_out / pdelta as in
+ * orc_augmented_resample_sampled (pdelta nsamp x S), xhat_out (nsamp x d), filt / pred
+ * (2d each, phi = x then x^2). */
+int orc_step_sampled(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t seed, uint32_t n,
+                     const float* y, const float* xin, uint64_t nsamp, const int64_t* outputs,
+                     double* logV, int64_t* A_out, float* pdelta, double* xhat_out, double* filt, double* pred)
+{
+    int d = mdl->d;
+    if (M == 0 || N % M != 0 || ilog2_exact(N / M) < 1) return ORC_EINVAL;
+    double* lw = (double*)malloc(sizeof(double) * N);
+    if (!lw) return ORC_ENOMEM;
+    double L = -INFINITY, sw = 0.0;
+    double s1[8] = {0}, s2[8] = {0}, p1[8] = {0}, p2[8] = {0};
+    for (uint64_t i = 0; i < N; ++i) {
+        double xh[8], x[8];
+        for (int k = 0; k < d; ++k) xh[k] = (double)xin[i * d + k];
+        if (n == 0) memcpy(x, xh, sizeof(double) * d);
+        else mutate_one(mdl, seed, n, i, xh, x);
+        lw[i] = logweight_one(mdl, y, x);
+        if (lw[i] > L) {  /* new running maximum: rescale what was accumulated */
+            double f = (L == -INFINITY) ? 0.0 : exp(L - lw[i]);
+            sw *= f;
+            for (int k = 0; k < d; ++k) { s1[k] *= f; s2[k] *= f; }
+            L = lw[i];
+        }
+        double w = (lw[i] == -INFINITY) ? 0.0 : exp(lw[i] - L);
+        sw += w;
+        for (int k = 0; k < d; ++k) {
+            s1[k] += w * x[k];
+            s2[k] += w * x[k] * x[k];
+            p1[k] += x[k];
+            p2[k] += x[k] * x[k];
+        }
+    }
+    for (int k = 0; k < d; ++k) {
+        filt[k] = s1[k] / sw; filt[d + k] = s2[k] / sw;
+        pred[k] = p1[k] / (double)N; pred[d + k] = p2[k] / (double)N;
+    }
+    int rc = orc_augmented_resample_sampled(N, M, seed, n, lw, nsamp, outputs, NULL, NULL, pdelta, logV, A_out);
+    if (rc == ORC_OK)
+        for (uint64_t k = 0; k < nsamp; ++k) {
+            uint64_t j = (uint64_t)A_out[k];
+            double xh[8];
+            for (int c = 0; c < d; ++c) xh[c] = (double)xin[j * d + c];
+            if (n == 0) memcpy(xhat_out + k * d, xh, sizeof(double) * d);
+            else mutate_one(mdl, seed, n, j, xh, xhat_out + k * d);
+        }
+    free(lw);
     return rc;
 }
 

@@ -163,11 +163,13 @@ def particle_cloud(cfg: Config, N: int, seed: int, scale: float = 1.0) -> np.nda
     plus a handful of exact duplicates, as resampled clouds have."""
     rng = np.random.Generator(np.random.PCG64(seed))
     p = model_params(cfg)
-    if cfg.kind == PF_SV:
-        x = float(p["s0"]) * scale * rng.standard_normal((N, 1))
+    d = 1 if cfg.kind == PF_SV else cfg.d
+    sd = float(p["s0"]) * scale if cfg.kind == PF_SV else scale
+    if N * d > (1 << 26):  # full-size clouds (C4: 2^30 values): drawn in fp32, scaled in place
+        x = rng.standard_normal((N, d), dtype=np.float32)
+        x *= np.float32(sd)
     else:
-        x = scale * rng.standard_normal((N, cfg.d))
-    x = x.astype(np.float32)
+        x = (sd * rng.standard_normal((N, d))).astype(np.float32)
     if N >= 8:  # duplicates: copy a random 1/8 of the entries from random sources
         k = N // 8
         dst = rng.integers(0, N, size=k)

@@ -1,0 +1,58 @@
+"""GPU <-> oracle parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (non-debug handle, the plan of the full problem), on sampled outputs the oracle
+evaluates one by one (oracle/pf_oracle.c orc_step_sampled):
+
+* C4: N = 2^28, M = 64, S = 22, d = 4, one teacher-forced step with mutation (n = 1);
+* C5 extremes: N = 2^26 with M = 2 (S = 25) and M = 8192 (S = 13).
+
+Compared: every V level (the whole m - 1 table), the filter and predictive estimates
+(tolerance of tests/parity_util.py), and for 4096 sampled outputs (random plus tile and
+shard edges) the resampled state x_hat[i] = x_n[A(i)], except outputs whose ancestral path
+holds a draw within 1e-6 of a decision boundary (reading R5; counted and bounded)."""
+import numpy as np
+import pytest
+
+from paper_1812_01502_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+from paper_1812_01502_b200 import pf as pfb  # noqa: E402
+
+from . import parity_util as pu  # noqa: E402
+
+
+def _samples(N, k, seed):
+    rng = np.random.default_rng(seed)
+    edges = [0, 1, N - 1, N // 2 - 1, N // 2, 1023, 1024, 4095, 4096, N - 1024]
+    return np.unique(np.concatenate([rng.integers(0, N, size=k - len(edges)), edges])).astype(np.int64)
+
+
+@pytest.mark.parametrize("name,N,M,n", [("C4", 1 << 28, 64, 1), ("C5", 1 << 26, 2, 1), ("C5", 1 << 26, 8192, 1)])
+def test_full_size_sampled_parity(orc, name, N, M, n):
+    cfg = inputs.CONFIGS[name]
+    p = inputs.model_params(cfg)
+    d = int(p["d"])
+    xhat = inputs.particle_cloud(cfg, N, 29)
+    y = inputs.observation_for_step(cfg, 31, outlier_sigma=1.0)
+    outs = _samples(N, 4096, 3)
+    o = orc.step_sampled(p, N, M, 41, n, y, xhat, outs)
+
+    f = pfb.ParticleFilter(p, N, M, 41)
+    f.set_state(xhat, n)
+    del xhat
+    f.step(y)
+    pu.check_logV(f.debug_get(pfb.PF_DBG_LOGV), o["logV"])
+    filt = f.estimate(pfb.PF_PHI_X, pfb.PF_EST_FILTER)
+    pred = f.estimate(pfb.PF_PHI_X, pfb.PF_EST_PREDICT)
+    pu.check_estimate(filt, o["filter"][:d], o["filter"][d:])
+    pu.check_estimate(pred, o["predict"][:d], o["predict"][d:])
+    xg = f.debug_tensor(pfb.PF_DBG_XHAT).view(N, -1)[torch.from_numpy(outs).to("cuda"), :d].cpu().numpy()
+    f.close()
+
+    flagged = (o["pdelta"] < pu.BOUNDARY).any(axis=1)
+    assert flagged.mean() < 0.05, f"{flagged.sum()} of {len(outs)} sampled paths flagged"  # M = 8192: ~3%
+    pu.check_x(xg[~flagged], o["xhat"][~flagged])
