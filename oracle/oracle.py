@@ -55,7 +55,10 @@ def lib():
         _lib.orc_augmented_resample_sampled.argtypes = [u64, u64, u64, u32, vp, u64, vp, vp, vp, vp, vp, vp]
         _lib.orc_estimates.argtypes = [ctypes.c_int, u64, vp, vp, vp, vp, vp, vp]
         _lib.orc_step.argtypes = [vp, u64, u64, u64, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
-        _lib.orc_step_sampled.argtypes = [vp, u64, u64, u64, u32, vp, vp, u64, vp, vp, vp, vp, vp, vp, vp]
+        _lib.orc_step_sampled.argtypes = [vp, u64, u64, u64, u32, vp, vp, ctypes.c_double, u64, vp, vp, vp, vp, vp,
+                                          vp, vp, vp, vp]
+        _lib.orc_step_airpf_sampled.argtypes = [vp, u64, u64, u64, u32, vp, vp, ctypes.c_int, u64, vp, vp, vp, vp,
+                                                vp, vp, vp]
         _lib.orc_augmented_resample_partial.argtypes = [u64, u64, u64, u32, vp, ctypes.c_int, vp, vp, vp, vp]
         _lib.orc_ess_levels.argtypes = [u64, u64, vp, vp, vp]
         _lib.orc_stages_to_run.argtypes = [ctypes.c_int, vp, ctypes.c_double]
@@ -208,11 +211,11 @@ def step(params: dict, N: int, M: int, seed: int, n: int, y: np.ndarray, xin: np
 
 
 def step_sampled(params: dict, N: int, M: int, seed: int, n: int, y: np.ndarray, xin: np.ndarray,
-                 outputs: np.ndarray) -> dict:
+                 outputs: np.ndarray, theta: float = 0.0) -> dict:
     """One step at full size, evaluated on sampled outputs (orc_step_sampled): all V
     levels, the estimates, and for each sampled output its composed ancestor A, the
     boundary distances of the draws on its path (pdelta, samples x S, stage s at s-1)
-    and its resampled state xhat."""
+    and its resampled state xhat.  theta > 0: the fully adapted step (ess, sstar)."""
     mdl = make_model(params)
     d = mdl.d
     m = N // M
@@ -221,14 +224,38 @@ def step_sampled(params: dict, N: int, M: int, seed: int, n: int, y: np.ndarray,
     yy = np.ascontiguousarray(y, dtype=np.float32)
     outs = np.ascontiguousarray(outputs, dtype=np.int64)
     k = len(outs)
-    out = dict(logV=np.zeros(m - 1), A=np.zeros(k, np.int64), pdelta=np.zeros((k, S), np.float32),
-               xhat=np.zeros((k, d)), filter=np.zeros(2 * d), predict=np.zeros(2 * d))
-    rc = lib().orc_step_sampled(ctypes.byref(mdl), N, M, seed, n, _ptr(yy), _ptr(xin), k, _ptr(outs),
-                                _ptr(out["logV"]), _ptr(out["A"]), _ptr(out["pdelta"]), _ptr(out["xhat"]),
-                                _ptr(out["filter"]), _ptr(out["predict"]))
+    out = dict(logV=np.zeros(m - 1), ess=np.zeros(S + 1), A=np.zeros(k, np.int64),
+               pdelta=np.zeros((k, S), np.float32), xhat=np.zeros((k, d)), filter=np.zeros(2 * d),
+               predict=np.zeros(2 * d))
+    ss = ctypes.c_int(0)
+    rc = lib().orc_step_sampled(ctypes.byref(mdl), N, M, seed, n, _ptr(yy), _ptr(xin), float(theta), k, _ptr(outs),
+                                _ptr(out["logV"]), _ptr(out["ess"]), ctypes.byref(ss), _ptr(out["A"]),
+                                _ptr(out["pdelta"]), _ptr(out["xhat"]), _ptr(out["filter"]), _ptr(out["predict"]))
     if rc != 0:
         raise ValueError(f"orc_step_sampled rc={rc}")
-    out["S"], out["m"] = S, m
+    out["S"], out["m"], out["sstar"] = S, m, int(ss.value)
+    return out
+
+
+def step_airpf_sampled(params: dict, N: int, M: int, seed: int, n: int, y: np.ndarray, xin: np.ndarray,
+                       outputs: np.ndarray, modified: bool = True) -> dict:
+    """One AIRPF step at full size on sampled outputs (orc_step_airpf_sampled): island
+    log-means logW, island map Aisl, estimates, and per sampled output its resampled state
+    xhat and the smallest boundary distance on its path (sdelta)."""
+    mdl = make_model(params)
+    d = mdl.d
+    m = N // M
+    xin = np.ascontiguousarray(xin, dtype=np.float32).reshape(N, d)
+    yy = np.ascontiguousarray(y, dtype=np.float32)
+    outs = np.ascontiguousarray(outputs, dtype=np.int64)
+    k = len(outs)
+    out = dict(logW=np.zeros(m), Aisl=np.zeros(m, np.int64), sdelta=np.zeros(k, np.float32), xhat=np.zeros((k, d)),
+               filter=np.zeros(2 * d), predict=np.zeros(2 * d))
+    rc = lib().orc_step_airpf_sampled(ctypes.byref(mdl), N, M, seed, n, _ptr(yy), _ptr(xin), 1 if modified else 0, k,
+                                      _ptr(outs), _ptr(out["logW"]), _ptr(out["Aisl"]), _ptr(out["sdelta"]),
+                                      _ptr(out["xhat"]), _ptr(out["filter"]), _ptr(out["predict"]))
+    if rc != 0:
+        raise ValueError(f"orc_step_airpf_sampled rc={rc}")
     return out
 
 

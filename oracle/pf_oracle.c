@@ -388,28 +388,13 @@ static int augmented_resample_upto(uint64_t N, uint64_t M, uint64_t seed, uint32
     return ORC_OK;
 }
 
-/* Same draws, evaluated only along the ancestral paths of `nsamp` sampled outputs
- * (for full-size configurations where S x N tables do not fit).  The V tables are
- * computed in full, exactly as above.  For each sample k and stage s:
- *   path[k*S + (s-1)]  = the stage-s position on the path (path[k*S+S-1] = output),
- *   anc[k*S + (s-1)]   = a_s(path position),  pdelta likewise;  A_out[k] = A(output). */
-int orc_augmented_resample_sampled(uint64_t N, uint64_t M, uint64_t seed, uint32_t n,
-                                   const double* lw, uint64_t nsamp, const int64_t* outputs,
-                                   int64_t* path, int64_t* anc, float* pdelta, double* logV,
-                                   int64_t* A_out)
+/* V table of Alg. 3 (levels 1..S, layout of orc_augmented_resample) from the weights. */
+static int v_table(uint64_t N, uint64_t M, const double* lw, double* lv)
 {
-    if (M == 0 || N % M != 0) return ORC_EINVAL;
-    uint64_t m = N / M;
+    uint64_t m = N / M, twoM = 2 * M;
     int S = ilog2_exact(m);
-    int b = ilog2_exact(M);
-    if (S < 1 || b < 0) return ORC_EINVAL;
-    uint64_t twoM = 2 * M;
-    double* lv = (double*)malloc(sizeof(double) * (m - 1));
     double* C = (double*)malloc(sizeof(double) * twoM);
-    if (!lv || !C) {
-        free(lv); free(C);
-        return ORC_ENOMEM;
-    }
+    if (!C) return ORC_ENOMEM;
     for (uint64_t p = 0; p < m / 2; ++p) {
         double mx = pair_cdf(lw, 2 * p * M, twoM, C);
         lv[level_offset(m, 1) + p] = (mx == -INFINITY) ? -INFINITY : mx + log(C[twoM - 1]) - log((double)twoM);
@@ -419,9 +404,29 @@ int orc_augmented_resample_sampled(uint64_t N, uint64_t M, uint64_t seed, uint32
         double* cur = lv + level_offset(m, s);
         for (uint64_t bk = 0; bk < (m >> s); ++bk) cur[bk] = log_pair_mean(prev[2 * bk], prev[2 * bk + 1]);
     }
+    free(C);
+    return ORC_OK;
+}
+
+/* The draws of stages S_exec..1 along the ancestral path of each sampled output (the same
+ * draws as orc_augmented_resample).  path/anc/pdelta: k*S + (s-1); stages above S_exec
+ * are not drawn (pdelta = +inf, path = anc = -1). */
+static int sampled_draws(uint64_t N, uint64_t M, uint64_t seed, uint32_t n, const double* lw, const double* lv,
+                         uint64_t nsamp, const int64_t* outputs, int S_exec, int64_t* path, int64_t* anc,
+                         float* pdelta, int64_t* A_out)
+{
+    uint64_t m = N / M, twoM = 2 * M;
+    int S = ilog2_exact(m), b = ilog2_exact(M);
+    double* C = (double*)malloc(sizeof(double) * twoM);
+    if (!C) return ORC_ENOMEM;
     for (uint64_t k = 0; k < nsamp; ++k) {
         uint64_t j = (uint64_t)outputs[k];
-        for (int s = S; s >= 1; --s) {
+        for (int s = S; s > S_exec; --s) {
+            if (path) path[k * S + (uint64_t)(s - 1)] = -1;
+            if (anc) anc[k * S + (uint64_t)(s - 1)] = -1;
+            if (pdelta) pdelta[k * S + (uint64_t)(s - 1)] = INFINITY;
+        }
+        for (int s = S_exec; s >= 1; --s) {
             int64_t aj;
             double dl;
             if (s >= 2) {
@@ -438,9 +443,32 @@ int orc_augmented_resample_sampled(uint64_t N, uint64_t M, uint64_t seed, uint32
         }
         if (A_out) A_out[k] = (int64_t)j;
     }
-    if (logV) memcpy(logV, lv, sizeof(double) * (m - 1));
-    free(lv); free(C);
+    free(C);
     return ORC_OK;
+}
+
+/* Same draws, evaluated only along the ancestral paths of `nsamp` sampled outputs
+ * (for full-size configurations where S x N tables do not fit).  The V tables are
+ * computed in full, exactly as above.  For each sample k and stage s:
+ *   path[k*S + (s-1)]  = the stage-s position on the path (path[k*S+S-1] = output),
+ *   anc[k*S + (s-1)]   = a_s(path position),  pdelta likewise;  A_out[k] = A(output). */
+int orc_augmented_resample_sampled(uint64_t N, uint64_t M, uint64_t seed, uint32_t n,
+                                   const double* lw, uint64_t nsamp, const int64_t* outputs,
+                                   int64_t* path, int64_t* anc, float* pdelta, double* logV,
+                                   int64_t* A_out)
+{
+    if (M == 0 || N % M != 0) return ORC_EINVAL;
+    uint64_t m = N / M;
+    int S = ilog2_exact(m);
+    int b = ilog2_exact(M);
+    if (S < 1 || b < 0) return ORC_EINVAL;
+    double* lv = (double*)malloc(sizeof(double) * (m - 1));
+    if (!lv) return ORC_ENOMEM;
+    int rc = v_table(N, M, lw, lv);
+    if (rc == ORC_OK) rc = sampled_draws(N, M, seed, n, lw, lv, nsamp, outputs, S, path, anc, pdelta, A_out);
+    if (rc == ORC_OK && logV) memcpy(logV, lv, sizeof(double) * (m - 1));
+    free(lv);
+    return rc;
 }
 
 /* ------------------------------------------------------------------------- */
@@ -508,62 +536,6 @@ int orc_step(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t seed, uint32
         orc_estimates(d, N, lw, x, Aloc, filt, pred, resamp);
     }
     free(xprev); free(Aloc);
-    return rc;
-}
-
-/* The same step at full size (C4: N = 2^28), checked on sampled outputs: lw for all N
- * particles (kept), the estimates accumulated in the same pass, then the draws only along
- * the ancestral paths of the sampled outputs (orc_augmented_resample_sampled) and their
- * resampled states.  The estimates are Sum g phi / Sum g with the weights shifted by the
- * running maximum of lw (rescaled whenever it grows): the same quantity as orc_estimates'
- * shift by the final maximum, in one pass.  Outputs: logV (m - 1), A_out / pdelta as in
- * orc_augmented_resample_sampled (pdelta nsamp x S), xhat_out (nsamp x d), filt / pred
- * (2d each, phi = x then x^2). */
-int orc_step_sampled(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t seed, uint32_t n,
-                     const float* y, const float* xin, uint64_t nsamp, const int64_t* outputs,
-                     double* logV, int64_t* A_out, float* pdelta, double* xhat_out, double* filt, double* pred)
-{
-    int d = mdl->d;
-    if (M == 0 || N % M != 0 || ilog2_exact(N / M) < 1) return ORC_EINVAL;
-    double* lw = (double*)malloc(sizeof(double) * N);
-    if (!lw) return ORC_ENOMEM;
-    double L = -INFINITY, sw = 0.0;
-    double s1[8] = {0}, s2[8] = {0}, p1[8] = {0}, p2[8] = {0};
-    for (uint64_t i = 0; i < N; ++i) {
-        double xh[8], x[8];
-        for (int k = 0; k < d; ++k) xh[k] = (double)xin[i * d + k];
-        if (n == 0) memcpy(x, xh, sizeof(double) * d);
-        else mutate_one(mdl, seed, n, i, xh, x);
-        lw[i] = logweight_one(mdl, y, x);
-        if (lw[i] > L) {  /* new running maximum: rescale what was accumulated */
-            double f = (L == -INFINITY) ? 0.0 : exp(L - lw[i]);
-            sw *= f;
-            for (int k = 0; k < d; ++k) { s1[k] *= f; s2[k] *= f; }
-            L = lw[i];
-        }
-        double w = (lw[i] == -INFINITY) ? 0.0 : exp(lw[i] - L);
-        sw += w;
-        for (int k = 0; k < d; ++k) {
-            s1[k] += w * x[k];
-            s2[k] += w * x[k] * x[k];
-            p1[k] += x[k];
-            p2[k] += x[k] * x[k];
-        }
-    }
-    for (int k = 0; k < d; ++k) {
-        filt[k] = s1[k] / sw; filt[d + k] = s2[k] / sw;
-        pred[k] = p1[k] / (double)N; pred[d + k] = p2[k] / (double)N;
-    }
-    int rc = orc_augmented_resample_sampled(N, M, seed, n, lw, nsamp, outputs, NULL, NULL, pdelta, logV, A_out);
-    if (rc == ORC_OK)
-        for (uint64_t k = 0; k < nsamp; ++k) {
-            uint64_t j = (uint64_t)A_out[k];
-            double xh[8];
-            for (int c = 0; c < d; ++c) xh[c] = (double)xin[j * d + c];
-            if (n == 0) memcpy(xhat_out + k * d, xh, sizeof(double) * d);
-            else mutate_one(mdl, seed, n, j, xh, xhat_out + k * d);
-        }
-    free(lw);
     return rc;
 }
 
@@ -920,4 +892,125 @@ int orc_step_multinomial(const orc_model* mdl, uint64_t N, uint64_t seed, uint32
     for (uint64_t i = 0; i < N; ++i)
         for (int k = 0; k < d; ++k) xhat_out[i * d + k] = x[(uint64_t)a[i] * d + k];
     return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Full-size checks on sampled outputs (C4: N = 2^28).  lw_pass: x_n (mutated from xin
+ * when n >= 1) and lw for all N particles (lw kept, x not), with the estimates accumulated
+ * in the same pass: Sum g phi / Sum g with the weights shifted by the running maximum of
+ * lw (rescaled whenever it grows) -- the same quantity as orc_estimates' shift by the final
+ * maximum, in one pass.  filt / pred: 2d each (phi = x, then x^2). */
+static void lw_pass(const orc_model* mdl, uint64_t N, uint64_t seed, uint32_t n, const float* y, const float* xin,
+                    double* lw, double* filt, double* pred)
+{
+    int d = mdl->d;
+    double L = -INFINITY, sw = 0.0;
+    double s1[8] = {0}, s2[8] = {0}, p1[8] = {0}, p2[8] = {0};
+    for (uint64_t i = 0; i < N; ++i) {
+        double xh[8], x[8];
+        for (int k = 0; k < d; ++k) xh[k] = (double)xin[i * d + k];
+        if (n == 0) memcpy(x, xh, sizeof(double) * d);
+        else mutate_one(mdl, seed, n, i, xh, x);
+        lw[i] = logweight_one(mdl, y, x);
+        if (lw[i] > L) {  /* new running maximum: rescale what was accumulated */
+            double f = (L == -INFINITY) ? 0.0 : exp(L - lw[i]);
+            sw *= f;
+            for (int k = 0; k < d; ++k) { s1[k] *= f; s2[k] *= f; }
+            L = lw[i];
+        }
+        double w = (lw[i] == -INFINITY) ? 0.0 : exp(lw[i] - L);
+        sw += w;
+        for (int k = 0; k < d; ++k) {
+            s1[k] += w * x[k];
+            s2[k] += w * x[k] * x[k];
+            p1[k] += x[k];
+            p2[k] += x[k] * x[k];
+        }
+    }
+    for (int k = 0; k < d; ++k) {
+        filt[k] = s1[k] / sw; filt[d + k] = s2[k] / sw;
+        pred[k] = p1[k] / (double)N; pred[d + k] = p2[k] / (double)N;
+    }
+}
+
+/* x_n of particle j (recomputed from its xin row). */
+static void x_of(const orc_model* mdl, uint64_t seed, uint32_t n, const float* xin, uint64_t j, double* x)
+{
+    int d = mdl->d;
+    double xh[8];
+    for (int c = 0; c < d; ++c) xh[c] = (double)xin[j * d + c];
+    if (n == 0) memcpy(x, xh, sizeof(double) * d);
+    else mutate_one(mdl, seed, n, j, xh, x);
+}
+
+/* One step (plain, or fully adapted with theta > 0) at full size, on sampled outputs:
+ * the whole V table (logV, m - 1), the estimates, with theta > 0 the ESS levels (ess,
+ * S + 1) and S* (*sstar; the stop rule of orc_stages_to_run), and for each sampled output
+ * its composed ancestor A (stages S*..1), the boundary distances on its path (pdelta,
+ * nsamp x S, +inf above S*) and its resampled state (xhat_out, nsamp x d). */
+int orc_step_sampled(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t seed, uint32_t n,
+                     const float* y, const float* xin, double theta, uint64_t nsamp, const int64_t* outputs,
+                     double* logV, double* ess, int* sstar, int64_t* A_out, float* pdelta, double* xhat_out,
+                     double* filt, double* pred)
+{
+    if (M == 0 || N % M != 0 || ilog2_exact(N / M) < 1) return ORC_EINVAL;
+    int S = ilog2_exact(N / M);
+    double* lw = (double*)malloc(sizeof(double) * N);
+    if (!lw) return ORC_ENOMEM;
+    lw_pass(mdl, N, seed, n, y, xin, lw, filt, pred);
+    int rc = v_table(N, M, lw, logV);
+    int se = S;
+    if (rc == ORC_OK && theta > 0.0) {
+        orc_ess_levels(N, M, lw, logV, ess);
+        se = orc_stages_to_run(S, ess, theta);
+    }
+    if (sstar) *sstar = se;
+    if (rc == ORC_OK) rc = sampled_draws(N, M, seed, n, lw, logV, nsamp, outputs, se, NULL, NULL, pdelta, A_out);
+    if (rc == ORC_OK)
+        for (uint64_t k = 0; k < nsamp; ++k) x_of(mdl, seed, n, xin, (uint64_t)A_out[k], xhat_out + k * mdl->d);
+    free(lw);
+    return rc;
+}
+
+/* One AIRPF step (orc_step_airpf) at full size, on sampled outputs: the island
+ * log-means (logW, m), the island map (Aisl, m), the estimates, and for each sampled
+ * output i = b M + j its resampled state x[a_w(Aisl(b) M + j)] (xhat_out) with the
+ * smallest boundary distance on its path (sdelta): the within-island draw it takes and,
+ * at every island stage, the draws of both islands of the pair (Alg. 7 couples them). */
+int orc_step_airpf_sampled(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t seed, uint32_t n,
+                           const float* y, const float* xin, int modified, uint64_t nsamp, const int64_t* outputs,
+                           double* logW, int64_t* Aisl, float* sdelta, double* xhat_out, double* filt, double* pred)
+{
+    if (M == 0 || N % M != 0 || ilog2_exact(N / M) < 1) return ORC_EINVAL;
+    uint64_t m = N / M;
+    int S = ilog2_exact(m);
+    double* lw = (double*)malloc(sizeof(double) * N);
+    int64_t* a_w = (int64_t*)malloc(sizeof(int64_t) * N);
+    float* wdelta = (float*)malloc(sizeof(float) * N);
+    int32_t* src = (int32_t*)malloc(sizeof(int32_t) * m * (uint64_t)S);
+    float* idelta = (float*)malloc(sizeof(float) * m * (uint64_t)S);
+    int rc = (lw && a_w && wdelta && src && idelta) ? ORC_OK : ORC_ENOMEM;
+    if (rc == ORC_OK) {
+        lw_pass(mdl, N, seed, n, y, xin, lw, filt, pred);
+        rc = orc_within_island(N, M, seed, n, lw, a_w, wdelta, logW);
+    }
+    if (rc == ORC_OK) rc = orc_island_resample(m, seed, n, logW, modified, src, idelta, NULL, Aisl);
+    if (rc == ORC_OK)
+        for (uint64_t k = 0; k < nsamp; ++k) {
+            uint64_t i = (uint64_t)outputs[k], c = i / M, j = i % M;
+            float dmin = INFINITY;
+            for (int s = S; s >= 1; --s) {
+                uint64_t h = c ^ (1ull << (s - 1));
+                float a = idelta[(uint64_t)(s - 1) * m + c], b = idelta[(uint64_t)(s - 1) * m + h];
+                if (a < dmin) dmin = a;
+                if (b < dmin) dmin = b;
+                c = (uint64_t)src[(uint64_t)(s - 1) * m + c];
+            }
+            uint64_t q = c * M + j;  /* c = Aisl(i / M) */
+            if (wdelta[q] < dmin) dmin = wdelta[q];
+            sdelta[k] = dmin;
+            x_of(mdl, seed, n, xin, (uint64_t)a_w[q], xhat_out + k * mdl->d);
+        }
+    free(lw); free(a_w); free(wdelta); free(src); free(idelta);
+    return rc;
 }

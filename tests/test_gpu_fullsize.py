@@ -8,7 +8,9 @@ evaluates one by one (oracle/pf_oracle.c orc_step_sampled):
 Compared: every V level (the whole m - 1 table), the filter and predictive estimates
 (tolerance of tests/parity_util.py), and for 4096 sampled outputs (random plus tile and
 shard edges) the resampled state x_hat[i] = x_n[A(i)], except outputs whose ancestral path
-holds a draw within 1e-6 of a decision boundary (reading R5; counted and bounded)."""
+holds a draw within 1e-6 of a decision boundary (reading R5; counted and bounded).
+The fully adapted step (N1) and AIRPF (N2, Alg. 7 and 6) run the same check at C4's full
+size (orc_step_sampled with theta, orc_step_airpf_sampled)."""
 import numpy as np
 import pytest
 
@@ -56,3 +58,59 @@ def test_full_size_sampled_parity(orc, name, N, M, n):
     flagged = (o["pdelta"] < pu.BOUNDARY).any(axis=1)
     assert flagged.mean() < 0.05, f"{flagged.sum()} of {len(outs)} sampled paths flagged"  # M = 8192: ~3%
     pu.check_x(xg[~flagged], o["xhat"][~flagged])
+
+
+def test_full_size_adaptive_sampled(orc):
+    """Fully adapted step (N1) at C4's full size: ESS levels, S*, V table, estimates and
+    sampled x_hat after S* stages."""
+    cfg = inputs.CONFIGS["C4"]
+    p = inputs.model_params(cfg)
+    N, M, n, theta = cfg.N, cfg.M, 1, 0.5
+    xhat = inputs.particle_cloud(cfg, N, 37)
+    y = inputs.observation_for_step(cfg, 38, outlier_sigma=1.5)
+    outs = _samples(N, 4096, 4)
+    o = orc.step_sampled(p, N, M, 43, n, y, xhat, outs, theta=theta)
+    if np.any(np.abs(o["ess"] - theta) < 1e-4 * theta):  # S* would be a rounding decision
+        pytest.skip(f"theta within 1e-4 of an ESS level: {o['ess']}")
+    f = pfb.ParticleFilter(p, N, M, 43, theta=theta)
+    f.set_state(xhat, n)
+    del xhat
+    f.step(y)
+    assert f.last_stages() == o["sstar"], (f.last_stages(), o["sstar"], o["ess"])
+    assert np.allclose(f.debug_get(pfb.PF_DBG_ESS), o["ess"], rtol=2e-5, atol=0)
+    pu.check_logV(f.debug_get(pfb.PF_DBG_LOGV), o["logV"])
+    pu.check_estimate(f.estimate(pfb.PF_PHI_X, pfb.PF_EST_FILTER), o["filter"][:4], o["filter"][4:])
+    pu.check_estimate(f.estimate(pfb.PF_PHI_X, pfb.PF_EST_PREDICT), o["predict"][:4], o["predict"][4:])
+    xg = f.debug_tensor(pfb.PF_DBG_XHAT)[torch.from_numpy(outs).to("cuda")].cpu().numpy()
+    f.close()
+    flagged = (o["pdelta"] < pu.BOUNDARY).any(axis=1)
+    assert flagged.mean() < 0.01
+    pu.check_x(xg[~flagged], o["xhat"][~flagged])
+
+
+@pytest.mark.parametrize("modified", [True, False])
+def test_full_size_airpf_sampled(orc, modified):
+    """AIRPF (N2) at C4's full size: island log-means, island map and x_hat on sampled
+    outputs (path free of boundary draws), estimates."""
+    cfg = inputs.CONFIGS["C4"]
+    p = inputs.model_params(cfg)
+    N, M, n = cfg.N, cfg.M, 1
+    xhat = inputs.particle_cloud(cfg, N, 47)
+    y = inputs.observation_for_step(cfg, 48, outlier_sigma=1.0)
+    outs = _samples(N, 4096, 5)
+    o = orc.step_airpf_sampled(p, N, M, 53, n, y, xhat, outs, modified=modified)
+    f = pfb.ParticleFilter(p, N, M, 53, airpf=1 if modified else 2)
+    f.set_state(xhat, n)
+    del xhat
+    f.step(y)
+    pu.check_logV(f.debug_get(pfb.PF_DBG_ISLAND_LOGW), o["logW"])
+    pu.check_estimate(f.estimate(pfb.PF_PHI_X, pfb.PF_EST_FILTER), o["filter"][:4], o["filter"][4:])
+    pu.check_estimate(f.estimate(pfb.PF_PHI_X, pfb.PF_EST_PREDICT), o["predict"][:4], o["predict"][4:])
+    A = f.debug_get(pfb.PF_DBG_ISLAND_A).astype(np.int64)
+    xg = f.debug_tensor(pfb.PF_DBG_XHAT)[torch.from_numpy(outs).to("cuda")].cpu().numpy()
+    f.close()
+    ok = o["sdelta"] >= pu.BOUNDARY
+    assert ok.mean() > 0.95
+    blk = outs // M
+    assert np.array_equal(A[blk[ok]], o["Aisl"][blk[ok]])
+    pu.check_x(xg[ok], o["xhat"][ok])

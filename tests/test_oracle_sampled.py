@@ -32,3 +32,44 @@ def test_sampled_equals_full_step(orc, name, N, M, n):
     sub = np.array([N - 1, 0, N // 2, 3])
     s2 = orc.step_sampled(p, N, M, 11, n, y, x, sub)
     assert np.array_equal(s2["A"], full["A"][sub]) and np.array_equal(s2["xhat"], full["xhat"][sub])
+
+
+@pytest.mark.parametrize("name,N,M,n,theta", [("C4", 1 << 12, 16, 3, 0.3), ("C1", 1024, 64, 1, 0.9),
+                                              ("C3", 1 << 11, 2, 2, 0.05), ("C4", 1 << 12, 16, 3, 1e-9)])
+def test_sampled_adaptive_equals_full_adaptive(orc, name, N, M, n, theta):
+    cfg = inputs.CONFIGS[name]
+    p = inputs.model_params(cfg)
+    x = inputs.particle_cloud(cfg, N, 8)
+    y = inputs.observation_for_step(cfg, 6 + n, outlier_sigma=2.0)
+    full = orc.step_adaptive(p, N, M, 13, n, y, x, np.zeros(N), theta)
+    smp = orc.step_sampled(p, N, M, 13, n, y, x, np.arange(N), theta=theta)
+    assert smp["sstar"] == full["sstar"]
+    assert np.array_equal(smp["ess"], full["ess"])
+    assert np.array_equal(smp["A"], full["A"])
+    assert np.array_equal(smp["xhat"], full["xhat"])
+    assert np.array_equal(smp["logV"], full["logV"])
+    assert np.all(np.isinf(smp["pdelta"][:, smp["sstar"]:]))
+
+
+@pytest.mark.parametrize("modified", [True, False])
+@pytest.mark.parametrize("name,N,M,n", [("C4", 1 << 12, 16, 3), ("C1", 1024, 64, 1), ("C3", 1 << 11, 4, 2)])
+def test_sampled_airpf_equals_full_airpf(orc, name, N, M, n, modified):
+    cfg = inputs.CONFIGS[name]
+    p = inputs.model_params(cfg)
+    x = inputs.particle_cloud(cfg, N, 9)
+    y = inputs.observation_for_step(cfg, 7 + n, outlier_sigma=1.0)
+    full = orc.step_airpf(p, N, M, 17, n, y, x, modified=modified)
+    smp = orc.step_airpf_sampled(p, N, M, 17, n, y, x, np.arange(N), modified=modified)
+    assert np.array_equal(smp["Aisl"], full["Aisl"])
+    assert np.array_equal(smp["logW"], full["logW"])
+    assert np.array_equal(smp["xhat"], full["xhat"])
+    assert np.allclose(smp["filter"], full["filter"], rtol=1e-12, atol=1e-300)
+    # sdelta = min over the within draw taken and both islands' draws at every stage
+    m, S = N // M, full["S"]
+    for i in range(0, N, max(1, N // 64)):
+        c, dm = i // M, np.inf
+        for s in range(S, 0, -1):
+            dm = min(dm, full["idelta"][s - 1][c], full["idelta"][s - 1][c ^ (1 << (s - 1))])
+            c = full["src"][s - 1][c]
+        dm = min(dm, full["wdelta"][c * M + i % M])
+        assert smp["sdelta"][i] == np.float32(dm)
