@@ -57,6 +57,8 @@ def lib():
         _lib.orc_step.argtypes = [vp, u64, u64, u64, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         _lib.orc_step_sampled.argtypes = [vp, u64, u64, u64, u32, vp, vp, ctypes.c_double, u64, vp, vp, vp, vp, vp,
                                           vp, vp, vp, vp]
+        _lib.orc_step_multinomial_sampled.argtypes = [vp, u64, u64, u32, vp, vp, u64, vp, ctypes.c_double, vp, vp, vp,
+                                                      vp, vp, vp, vp]
         _lib.orc_step_airpf_sampled.argtypes = [vp, u64, u64, u64, u32, vp, vp, ctypes.c_int, u64, vp, vp, vp, vp,
                                                 vp, vp, vp]
         _lib.orc_augmented_resample_partial.argtypes = [u64, u64, u64, u32, vp, ctypes.c_int, vp, vp, vp, vp]
@@ -441,6 +443,28 @@ def step_multinomial(params: dict, N: int, seed: int, n: int, y: np.ndarray, xin
                                     _ptr(out["filter"]), _ptr(out["predict"]))
     if rc != 0:
         raise ValueError(f"orc_step_multinomial rc={rc}")
+    return out
+
+
+def step_multinomial_sampled(params: dict, N: int, seed: int, n: int, y: np.ndarray, xin: np.ndarray,
+                             outputs: np.ndarray, eps: float = 1e-6) -> dict:
+    """Alg. 2 step at full size on sampled outputs (orc_step_multinomial_sampled): a, the
+    boundary distance sdelta, the states of particles a + (-2..2) (xnb), the window
+    [klo, khi] of the draws for u -+ eps, estimates."""
+    mdl = make_model(params)
+    d = mdl.d
+    xin = np.ascontiguousarray(xin, dtype=np.float32).reshape(N, d)
+    yy = np.ascontiguousarray(y, dtype=np.float32)
+    outs = np.ascontiguousarray(outputs, dtype=np.int64)
+    k = len(outs)
+    out = dict(a=np.zeros(k, np.int64), klo=np.zeros(k, np.int64), khi=np.zeros(k, np.int64),
+               sdelta=np.zeros(k, np.float32), xnb=np.zeros((k, 5, d)), filter=np.zeros(2 * d), predict=np.zeros(2 * d))
+    rc = lib().orc_step_multinomial_sampled(ctypes.byref(mdl), N, seed, n, _ptr(yy), _ptr(xin), k, _ptr(outs),
+                                            float(eps), _ptr(out["a"]), _ptr(out["klo"]), _ptr(out["khi"]),
+                                            _ptr(out["sdelta"]), _ptr(out["xnb"]), _ptr(out["filter"]),
+                                            _ptr(out["predict"]))
+    if rc != 0:
+        raise ValueError(f"orc_step_multinomial_sampled rc={rc}")
     return out
 
 

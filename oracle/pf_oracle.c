@@ -1014,3 +1014,68 @@ int orc_step_airpf_sampled(const orc_model* mdl, uint64_t N, uint64_t M, uint64_
     free(lw); free(a_w); free(wdelta); free(src); free(idelta);
     return rc;
 }
+
+/* Multinomial step (orc_step_multinomial, Alg. 2) at full size on sampled outputs: the
+ * estimates, and per sampled output i its ancestor a(i) (the literal CDF search of
+ * orc_multinomial on the fp64 CDF of all N weights), the distance of its uniform to the
+ * nearest boundary C_k / C_{N-1} (sdelta) and the states of the particles a(i) + k,
+ * k = -2..2 (xnb, nsamp x 5 x d; NaN outside [0, N)), and the index window [klo, khi] of
+ * the draws for the uniforms u - eps and u + eps (every ancestor a draw within eps of u in
+ * uniform units could select). */
+static uint64_t cdf_search(const double* C, uint64_t N, double t)
+{
+    uint64_t lo = 0, hi = N - 1;
+    while (lo < hi) {
+        uint64_t mid = lo + (hi - lo) / 2;
+        if (C[mid] <= t) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+int orc_step_multinomial_sampled(const orc_model* mdl, uint64_t N, uint64_t seed, uint32_t n, const float* y,
+                                 const float* xin, uint64_t nsamp, const int64_t* outputs, double eps,
+                                 int64_t* a_out, int64_t* klo, int64_t* khi, float* sdelta, double* xnb,
+                                 double* filt, double* pred)
+{
+    int d = mdl->d;
+    if (N == 0) return ORC_EINVAL;
+    double* lw = (double*)malloc(sizeof(double) * N);
+    double* C = (double*)malloc(sizeof(double) * N);
+    if (!lw || !C) {
+        free(lw); free(C);
+        return ORC_ENOMEM;
+    }
+    lw_pass(mdl, N, seed, n, y, xin, lw, filt, pred);
+    double L = -INFINITY;
+    for (uint64_t j = 0; j < N; ++j)
+        if (lw[j] > L) L = lw[j];
+    double acc = 0.0;
+    for (uint64_t j = 0; j < N; ++j) {
+        acc += (L == -INFINITY) ? 1.0 : exp(lw[j] - L);
+        C[j] = acc;
+    }
+    const double total = C[N - 1];
+    for (uint64_t k = 0; k < nsamp; ++k) {
+        uint64_t i = (uint64_t)outputs[k];
+        double u = u01(rng_word(seed, (uint32_t)(i >> 2), n, ORC_DOMAIN_MULTI, 0u, (int)(i & 3u)));
+        uint64_t lo = cdf_search(C, N, u * total);
+        a_out[k] = (int64_t)lo;
+        klo[k] = (int64_t)cdf_search(C, N, (u - eps) * total);
+        khi[k] = (int64_t)cdf_search(C, N, (u + eps) * total);
+        double d1 = (lo < N - 1) ? fabs(u - C[lo] / total) : INFINITY;
+        double d0 = (lo > 0) ? fabs(u - C[lo - 1] / total) : INFINITY;
+        sdelta[k] = (float)(d0 < d1 ? d0 : d1);
+        for (int o = -2; o <= 2; ++o) {
+            double* dst = xnb + (k * 5 + (uint64_t)(o + 2)) * d;
+            int64_t j = (int64_t)lo + o;
+            if (j < 0 || (uint64_t)j >= N) {
+                for (int c = 0; c < d; ++c) dst[c] = NAN;
+            } else {
+                x_of(mdl, seed, n, xin, (uint64_t)j, dst);
+            }
+        }
+    }
+    free(lw); free(C);
+    return ORC_OK;
+}

@@ -114,3 +114,33 @@ def test_full_size_airpf_sampled(orc, modified):
     blk = outs // M
     assert np.array_equal(A[blk[ok]], o["Aisl"][blk[ok]])
     pu.check_x(xg[ok], o["xhat"][ok])
+
+
+def test_full_size_multinomial_sampled(orc):
+    """The plain BPF with multinomial resampling (Alg. 2) at C4's full size.  With N = 2^28
+    the CDF boundaries are ~1/N apart, closer than any fixed margin, so the check is: every
+    sampled GPU ancestor lies in the oracle's window of draws for u -+ 1e-6 (the GPU's fp32
+    tile CDFs, reading R22, round within it), most are exact, and x_hat is the ancestor's
+    state.  The handle keeps the ancestors (PF_FLAG_DEBUG; same kernels and launches)."""
+    cfg = inputs.CONFIGS["C4"]
+    p = inputs.model_params(cfg)
+    N, n = cfg.N, 1
+    xhat = inputs.particle_cloud(cfg, N, 57)
+    y = inputs.observation_for_step(cfg, 58, outlier_sigma=1.0)
+    outs = _samples(N, 4096, 6)
+    o = orc.step_multinomial_sampled(p, N, 59, n, y, xhat, outs, eps=1e-6)
+    f = pfb.ParticleFilter(p, N, cfg.M, 59, multinomial=True, debug=True)
+    f.set_state(xhat, n)
+    del xhat
+    f.step(y)
+    pu.check_estimate(f.estimate(pfb.PF_PHI_X, pfb.PF_EST_FILTER), o["filter"][:4], o["filter"][4:])
+    pu.check_estimate(f.estimate(pfb.PF_PHI_X, pfb.PF_EST_PREDICT), o["predict"][:4], o["predict"][4:])
+    idx = torch.from_numpy(outs).to("cuda")
+    ag = f.debug_tensor(pfb.PF_DBG_ANC_FINAL)[idx].cpu().numpy().astype(np.int64)
+    xg = f.debug_tensor(pfb.PF_DBG_XHAT)[idx].cpu().numpy()
+    f.close()
+    inside = (o["klo"] <= ag) & (ag <= o["khi"])
+    assert inside.all(), f"{(~inside).sum()} ancestors outside the 1e-6 window"
+    exact = ag == o["a"]
+    assert exact.mean() > 0.9, exact.mean()
+    pu.check_x(xg[exact], o["xnb"][exact, 2])

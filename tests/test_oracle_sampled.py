@@ -73,3 +73,26 @@ def test_sampled_airpf_equals_full_airpf(orc, name, N, M, n, modified):
             c = full["src"][s - 1][c]
         dm = min(dm, full["wdelta"][c * M + i % M])
         assert smp["sdelta"][i] == np.float32(dm)
+
+
+@pytest.mark.parametrize("name,N,n", [("C4", 1 << 12, 3), ("C1", 1024, 0), ("C3", 1 << 11, 2)])
+def test_sampled_multinomial_equals_full(orc, name, N, n):
+    cfg = inputs.CONFIGS[name]
+    p = inputs.model_params(cfg)
+    x = inputs.particle_cloud(cfg, N, 10)
+    y = inputs.observation_for_step(cfg, 8 + n, outlier_sigma=1.0)
+    full = orc.step_multinomial(p, N, 19, n, y, x)
+    smp = orc.step_multinomial_sampled(p, N, 19, n, y, x, np.arange(N))
+    assert np.array_equal(smp["a"], full["a"])
+    assert np.array_equal(smp["sdelta"], full["delta"])
+    assert np.array_equal(smp["xnb"][:, 2], full["xhat"])
+    for o in (-2, -1, 1, 2):
+        j = full["a"] + o
+        ok = (j >= 0) & (j < N)
+        assert np.array_equal(smp["xnb"][ok, 2 + o], full["x"][j[ok]])
+        assert np.all(np.isnan(smp["xnb"][~ok, 2 + o]))
+    assert np.allclose(smp["filter"], full["filter"], rtol=1e-12, atol=1e-300)
+    # the eps window contains the draw and shrinks to it away from boundaries
+    assert np.all((smp["klo"] <= smp["a"]) & (smp["a"] <= smp["khi"]))
+    far = smp["sdelta"] > 1e-6
+    assert np.array_equal(smp["klo"][far], smp["a"][far]) and np.array_equal(smp["khi"][far], smp["a"][far])
