@@ -145,3 +145,24 @@ def test_variant_rates_on_gpu(kw):
     rmse = [_rmse_end(p, ys, km, m * M, M, J=120, seed0=40000 + 1000 * i, **kw) for i, M in enumerate(Ms)]
     slope = np.polyfit(np.log(Ms), np.log(rmse), 1)[0]
     assert -0.65 < slope < -0.35, (kw, slope, rmse)
+
+
+def test_c4_full_size_filter_vs_kalman():
+    """The bench's workload end to end: C4 at N = 2^28 over its T = 50 observations through
+    pf_step_dev (as bench.py), filter means against the exact Kalman means at every step
+    (same error model as test_lg_large_vs_kalman)."""
+    cfg = inputs.CONFIGS["C4"]
+    p = inputs.model_params(cfg)
+    _, ys = inputs.simulate(cfg)
+    km, kc = kalman.kalman_filter(p["A"], p["Q"], p["H"], p["R"], p["m0"], p["P0"], ys)
+    f = pfb.ParticleFilter(p, cfg.N, cfg.M, 1)
+    yd = torch.tensor(np.asarray(ys, np.float32), device="cuda")
+    means = np.zeros((len(ys), cfg.d))
+    for n in range(len(ys)):
+        f.step_dev(yd[n])
+        means[n] = f.estimate(pfb.PF_PHI_X, pfb.PF_EST_FILTER)
+    f.close()
+    S = np.log2(cfg.N // cfg.M)
+    sd = np.sqrt(np.diagonal(kc, axis1=1, axis2=2))
+    err = np.abs(means - km) / (sd * np.sqrt(S / cfg.N))
+    assert np.all(err < 60), err.max()
