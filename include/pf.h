@@ -102,6 +102,14 @@ int pf_step(pf_handle* h, const float* y_host);
  * device observations are not detected. */
 int pf_step_dev(pf_handle* h, const float* y_dev);
 
+/* T consecutive steps in one call (no per-step host round trip through the binding):
+ * step k reads observation k from y_dev (DEVICE, T x dy fp32, contiguous).  est_dev
+ * (DEVICE, T x 4 x d fp64, or NULL) receives after step k the rows filter x, filter x^2,
+ * predictive x, predictive x^2 of that step.  Asynchronous on
+ * the handle's stream except where a step itself synchronises (the fully adapted
+ * scheme reads S* back).  Errors as pf_step_dev; steps before a failing one stay done. */
+int pf_run_dev(pf_handle* h, const float* y_dev, uint32_t T, double* est_dev);
+
 /* --- fully adapted augmented resampling (AIRPF2) ---
  * With theta in (0, 1], every later pf_step evaluates the ESS of the stage weights
  *   E_s = (N^-1 sum_i V_s^i)^2 / (N^-1 sum_i (V_s^i)^2),  s = 0 (V_0 = the weights), 1..S

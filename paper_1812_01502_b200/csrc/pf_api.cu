@@ -1227,6 +1227,22 @@ int pf_step_dev(pf_handle* h, const float* y_dev) {
     return dispatch_step(h, nullptr, y_dev);
 }
 
+int pf_run_dev(pf_handle* h, const float* y_dev, uint32_t T, double* est_dev) {
+    if (!h || (T && !y_dev)) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world > 1) return fail(h, PF_ESTATE, "sharded handle: use pf_step_local / pf_step_top / pf_cross_stage");
+    const int d = h->mp.d, D = h->plan.D;
+    for (uint32_t k = 0; k < T; ++k) {
+        const int rc = dispatch_step(h, nullptr, y_dev + (size_t)k * h->mp.dy);
+        if (rc != PF_OK) return rc;
+        if (est_dev) {  // rows: filter x, filter x^2, predict x, predict x^2 (d doubles each)
+            const cudaError_t e = cudaMemcpy2DAsync(est_dev + (size_t)k * 4 * d, (size_t)d * 8, h->at<double>(h->lay.est),
+                                                    (size_t)D * 8, (size_t)d * 8, 4, cudaMemcpyDeviceToDevice, h->stream);
+            if (e != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_run_dev: ") + cudaGetErrorString(e));
+        }
+    }
+    return PF_OK;
+}
+
 int pf_estimate(pf_handle* h, int phi, int kind, double* out) {
     if (!h || !out) return fail(h, PF_EINVAL, "NULL argument");
     if (!h->have_step) return fail(h, PF_ESTATE, "no completed step");

@@ -98,6 +98,7 @@ def lib() -> ctypes.CDLL:
         L.pf_peer_set.argtypes = [vp, vp]
         L.pf_cross_peer.argtypes = [vp]
         L.pf_guard_check.argtypes = [vp, ctypes.c_ubyte, vp]
+        L.pf_run_dev.argtypes = [vp, vp, ctypes.c_uint32, vp]
         _lib = L
     return _lib
 
@@ -109,7 +110,7 @@ EXPORTED = ["pf_workspace_bytes", "pf_init", "pf_step", "pf_step_dev", "pf_estim
             "pf_set_adaptive", "pf_last_stages", "pf_set_airpf", "pf_set_multinomial", "pf_set_rotation",
             "pf_rotation_offset", "pf_cross_pull_plan", "pf_cross_pull_pack", "pf_cross_pull_serve",
             "pf_cross_pull_finish", "pf_peer_export", "pf_peer_open", "pf_peer_set", "pf_cross_peer",
-            "pf_guard_check"]
+            "pf_guard_check", "pf_run_dev"]
 PF_IPC_HANDLE_BYTES = 64
 GUARD_BYTES = 1 << 16  # guard band behind a poisoned workspace (ParticleFilter(poison=...))
 PF_KERNEL_KINDS = 5
@@ -335,6 +336,18 @@ class ParticleFilter:
         out = t.cpu().numpy()
         if what == PF_DBG_THRESH:
             out = out.view(np.uint32)
+        return out
+
+    def run_dev(self, y_dev, estimates: bool = True):
+        """len(y_dev) consecutive steps (pf_run_dev); y_dev: device fp32 tensor (T, dy).
+        Returns a device fp64 tensor (T, 4, d): filter x, filter x^2, predictive x,
+        predictive x^2 after every step (or None with estimates=False)."""
+        torch = self.torch
+        y = y_dev.contiguous()
+        T = int(y.shape[0])
+        out = torch.empty((T, 4, self.d), dtype=torch.float64, device=self.device) if estimates else None
+        _check(lib().pf_run_dev(self.h, y.data_ptr(), T, out.data_ptr() if out is not None else None), self.h)
+        self._keep_y = y
         return out
 
     def set_state(self, xhat: np.ndarray, n: int):

@@ -166,3 +166,25 @@ def test_c4_full_size_filter_vs_kalman():
     sd = np.sqrt(np.diagonal(kc, axis1=1, axis2=2))
     err = np.abs(means - km) / (sd * np.sqrt(S / cfg.N))
     assert np.all(err < 60), err.max()
+
+
+@pytest.mark.parametrize("kw", [{}, {"theta": 0.5}, {"airpf": 1}, {"multinomial": True}])
+def test_run_dev_equals_steps(kw):
+    """pf_run_dev (T steps in one call) gives bitwise the per-step results."""
+    cfg = inputs.CONFIGS["C2"]
+    p = inputs.model_params(cfg)
+    N, M = 1 << 16, 256
+    _, ys = inputs.simulate(cfg, T=6)
+    yd = torch.tensor(np.asarray(ys, np.float32), device="cuda")
+    a = pfb.ParticleFilter(p, N, M, 9, **kw)
+    b = pfb.ParticleFilter(p, N, M, 9, **kw)
+    est = a.run_dev(yd).cpu().numpy()
+    for n in range(len(ys)):
+        b.step_dev(yd[n])
+        want = [b.estimate(pfb.PF_PHI_X, pfb.PF_EST_FILTER), b.estimate(pfb.PF_PHI_X2, pfb.PF_EST_FILTER),
+                b.estimate(pfb.PF_PHI_X, pfb.PF_EST_PREDICT), b.estimate(pfb.PF_PHI_X2, pfb.PF_EST_PREDICT)]
+        assert np.array_equal(est[n], np.stack(want)), n
+    assert np.array_equal(a.debug_get(pfb.PF_DBG_XHAT), b.debug_get(pfb.PF_DBG_XHAT))
+    assert a.run_dev(yd[:0], estimates=False) is None  # T = 0: nothing to do
+    a.close()
+    b.close()
