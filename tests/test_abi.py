@@ -81,3 +81,16 @@ def test_scheme_flags_reserve_their_buffers(pfb):
     assert mn - base >= 8 * N            # log-weights + tile CDFs (fp32)
     both = pfb.pf_workspace_bytes(p, N, M, pfb.PF_FLAG_ADAPTIVE | pfb.PF_FLAG_MULTINOMIAL)
     assert both >= max(ad, mn)
+
+
+def test_guard_flag_adds_gaps(pfb):
+    """PF_FLAG_GUARD: one PF_GUARD_BYTES gap after every workspace region, whatever the
+    other flags (the region count is fixed by the layout)."""
+    p = inputs.model_params(inputs.CONFIGS["C4"])
+    N, M = 1 << 20, 64
+    for flags in (0, pfb.PF_FLAG_DEBUG, pfb.PF_FLAG_ADAPTIVE | pfb.PF_FLAG_AIRPF | pfb.PF_FLAG_MULTINOMIAL):
+        plain = pfb.pf_workspace_bytes(p, N, M, flags)
+        guarded = pfb.pf_workspace_bytes(p, N, M, flags | pfb.PF_FLAG_GUARD)
+        extra = guarded - plain
+        assert extra > 0 and (extra - 256) % 4096 == 0  # gaps + the 256-byte counter region
+        assert 30 <= (extra - 256) // 4096 <= 60  # one gap per region (+ the guard counter's own)
