@@ -140,6 +140,19 @@ __device__ __forceinline__ float warp_sum_transpose(float* v, uint32_t lane) {
     return v[0];
 }
 
+// Shared-memory slot of float4 s of the state tile: a thread writes its quad's D float4s
+// (one per store instruction), so without a swizzle the 8 threads of a store phase hit
+// only 2 (D = 4) or 1 (D = 8) of the 8 16-byte bank groups.  XOR-ing the low log2(D) bits
+// with bits 3.. of the index spreads them over all 8; it stays inside the quad.  Measured
+// (profiles/r1_ab_xs_swizzle.txt): AIRPF mode -3.8% and d = 8 -11% per k_pass1 launch,
+// the fused d = 4 pass +0.3% (its extra XORs cost more than the conflicts), so it is on
+// for d = 8 and the AIRPF mode only.
+template <int D, bool ON>
+__device__ __forceinline__ uint32_t xs_swz(uint32_t s) {
+    if constexpr (ON) return s ^ ((s >> 3) & (uint32_t)(D - 1));
+    else return s;
+}
+
 template <int D, int KIND, bool DBG, int QPT, int TB, int MODE = kPass1Fused>
 __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : 1) k_pass1(const __grid_constant__ Pass1Args a) {
     constexpr int PS = 2 + 4 * D;  // partial: max, sw, s1[D], s2[D], p1[D], p2[D]
@@ -161,6 +174,7 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : 1) 
     const uint32_t base = tile * P1;  // N < 2^31
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nwarps = threads >> 5;
     constexpr bool AIR = MODE == kPass1Airpf;
+    constexpr bool SWZ = AIR || D == 8;  // swizzled state tile (xs_swz)
     const uint32_t Z = AIR ? (M >> 2) : (M >> 1);  // quads per stage-1 pool (2M positions; AIRPF: one island of M)
     const uint32_t pool_sh = AIR ? b : b + 1u;      // log2 of the pool size
     const uint32_t c0t = (a.pos0 + base) >> 2;  // Philox counter of the tile's first quad
@@ -259,7 +273,8 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : 1) 
         if (!valid) continue;
 #pragma unroll
         for (int c = 0; c < D; ++c)
-            reinterpret_cast<float4*>(xs)[q * D + c] = make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+            reinterpret_cast<float4*>(xs)[xs_swz<D, SWZ>(q * D + c)] =
+                make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
         if constexpr (DBG) {
 #pragma unroll
             for (int c = 0; c < D; ++c)
@@ -322,7 +337,10 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : 1) 
             for (int k = 0; k < D; ++k) {
                 float xv;
                 if constexpr (KEEPX) xv = xr[it][e * D + k];
-                else xv = valid ? xs[(4 * q + e) * D + k] : 0.0f;
+                else {
+                    const uint32_t fi = (4u * q + e) * D + k;
+                    xv = valid ? xs[(xs_swz<D, SWZ>(fi >> 2) << 2) | (fi & 3u)] : 0.0f;
+                }
                 acc[2 + k] = fmaf(wf, xv, acc[2 + k]);
                 acc[2 + D + k] = fmaf(wf * xv, xv, acc[2 + D + k]);
                 acc[2 + 2 * D + k] += xv;
@@ -565,13 +583,13 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : 1) 
             if constexpr (D == 1) {
                 v[e] = xs[tp[e]];
             } else if constexpr (D == 2) {
-                const float2 t = reinterpret_cast<const float2*>(xs)[tp[e]];
+                const float2 t = reinterpret_cast<const float2*>(xs)[(xs_swz<D, SWZ>(tp[e] >> 1) << 1) | (tp[e] & 1u)];
                 v[2 * e] = t.x;
                 v[2 * e + 1] = t.y;
             } else {
 #pragma unroll
                 for (int c = 0; c < D / 4; ++c) {
-                    const float4 t = reinterpret_cast<const float4*>(xs)[tp[e] * (D / 4) + c];
+                    const float4 t = reinterpret_cast<const float4*>(xs)[xs_swz<D, SWZ>(tp[e] * (D / 4) + c)];
                     v[e * D + 4 * c] = t.x;
                     v[e * D + 4 * c + 1] = t.y;
                     v[e * D + 4 * c + 2] = t.z;
