@@ -271,10 +271,12 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : 1) 
             for (int k = 0; k < 4 * D; ++k) xr[it][k] = valid ? x[k] : 0.0f;
         }
         if (!valid) continue;
-#pragma unroll
-        for (int c = 0; c < D; ++c)
-            reinterpret_cast<float4*>(xs)[xs_swz<D, SWZ>(q * D + c)] =
-                make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+        if constexpr (!(MODE == kPass1Weigh && KEEPX)) {  // the weigh pass has no walk: the tile is read
+#pragma unroll                                              // back only by a non-KEEPX estimate
+            for (int c = 0; c < D; ++c)
+                reinterpret_cast<float4*>(xs)[xs_swz<D, SWZ>(q * D + c)] =
+                    make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+        }
         if constexpr (DBG) {
 #pragma unroll
             for (int c = 0; c < D; ++c)
