@@ -1,4 +1,4 @@
-# A/B of two in-tree builds (ab/libpf_base.so vs ab/libpf_swz.so) on the same box
+# A/B of two in-tree builds on the same box: build each variant, copy its libpf.so to ab/libpf_base.so and ab/libpf_swz.so (ab/ is git-ignored), then run this
 cat > /tmp/ab_cases.txt <<'C'
 X=1 -- --config C4
 X=1 -- --config C4 --airpf 1
