@@ -76,32 +76,67 @@ def config_dict(cfg, world, parallelism):
 
 
 # ----------------------------------------------------------------------------- oracle
-def oracle_sample(cfg, n_sample, steps, warmup=0):
-    """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
-    same model and M, N = n_sample particles, `steps` mutating steps after `warmup`
-    untimed ones.  Single thread."""
+def oracle_timed(cfg, n_sample, steps, warmup=0, threads=1):
+    """Time the fp64 oracle (as it stands, never tuned) on a bounded sample of the
+    workload: same model and M, N = n_sample particles per filter, `steps` mutating steps
+    after `warmup` untimed ones.  threads > 1: that many independent filters (seeds 5..)
+    run concurrently, one per host core (the oracle is a plain C library called through
+    ctypes, which releases the GIL); throughput counts every thread's particle-steps.
+    Returns the cpu_baseline dict plus the per-step wall times."""
+    import threading
+
     from oracle import oracle as orc
     from paper_1812_01502_b200 import inputs
     params = inputs.model_params(cfg)
-    x = inputs.particle_cloud(cfg, n_sample, 5)
     _, ys = inputs.simulate(cfg, T=warmup + steps + 1)
-    for n in range(1, warmup + 1):
-        x = orc.step(params, n_sample, cfg.M, 1, n, ys[n], x, tables=False)["xhat"].astype("float32")
-    t0 = time.perf_counter()
+    xs = [inputs.particle_cloud(cfg, n_sample, 5 + t) for t in range(threads)]
+    for t in range(threads):
+        for n in range(1, warmup + 1):
+            xs[t] = orc.step(params, n_sample, cfg.M, 1 + t, n, ys[n], xs[t], tables=False)["xhat"].astype("float32")
+    step_wall = []
     for n in range(warmup + 1, warmup + steps + 1):
-        r = orc.step(params, n_sample, cfg.M, 1, n, ys[n], x, tables=False)
-        x = r["xhat"].astype("float32")
-    dt = time.perf_counter() - t0
+        def work(t, n=n):
+            xs[t] = orc.step(params, n_sample, cfg.M, 1 + t, n, ys[n], xs[t], tables=False)["xhat"].astype("float32")
+        th = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+        t0 = time.perf_counter()
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        step_wall.append(time.perf_counter() - t0)
+    dt = sum(step_wall)
     m = n_sample // cfg.M
-    return dict(value=n_sample * steps / dt, unit=UNIT, cores=1, kind="oracle",
-                sample=f"{cfg.name} model, M={cfg.M}, N={n_sample} (m={m}, S={m.bit_length() - 1}) per step, "
-                       f"{steps} steps, fp64 C oracle, 1 thread, {dt:.1f} s")
+    value = threads * n_sample * steps / dt
+    return dict(value=value, unit=UNIT, cores=threads, kind="oracle",
+                sample=f"{cfg.name} model, M={cfg.M}, N={n_sample} (m={m}, S={m.bit_length() - 1}) per filter, "
+                       f"{threads} independent filter(s) on {threads} host thread(s), {steps} steps, fp64 C oracle, "
+                       f"{dt:.1f} s"), step_wall
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(cfg):
+    """The oracle on all host cores (one independent filter per core) next to one core."""
+    n_sample = min(cfg.N, 1 << 20)
+    one, _ = oracle_timed(cfg, n_sample, 2, threads=1)
+    cores = host_cores()
+    allc, _ = oracle_timed(cfg, n_sample, 2, threads=cores) if cores > 1 else (one, None)
+    allc = dict(allc)
+    allc["single_core_value"] = one["value"]
+    allc["nproc"] = cores
+    return allc
 
 
 def run_reference(args):
-    """The reference arm: the oracle as it stands, on the host cores, rank 0 only.  Each of
-    the K timed steps is a bounded sample of the workload (same model and M; N shrunk so
-    that K steps take ~15-30 s of CPU)."""
+    """The reference arm: the oracle as it stands, on all host cores, rank 0 only.  Each
+    of the K timed steps is a bounded sample of the workload (same model and M; N shrunk so
+    that the whole run takes ~1-3 min of wall time), run as one independent filter per
+    core.  The config printed is the one timed (N, m, S of the sample)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -109,14 +144,18 @@ def run_reference(args):
     from oracle import oracle as orc
     orc.build()
     steps = max(1, args.steps)
+    cores = host_cores()
     n_sample = 1 << max(1, min(20, ((1 << 24) // steps).bit_length() - 1))
     n_sample = min(cfg.N, max(n_sample, 2 * cfg.M))
-    cb = oracle_sample(cfg, n_sample, steps, warmup=max(0, args.warmup))
+    cb, walls = oracle_timed(cfg, n_sample, steps, warmup=min(max(0, args.warmup), 1), threads=cores)
+    timed = cfg.with_sizes(cfg.M, n_sample // cfg.M)
+    conf = config_dict(timed, 1, f"fp64 CPU oracle, {cores} independent filters on {cores} host threads")
+    conf.update({"sample_of": {"workload": cfg.name, "N": cfg.N, "m": cfg.m, "S": cfg.S},
+                 "filters_per_step": cores})
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
-            "steps": steps, "warmup": args.warmup, "ms_per_step": n_sample / cb["value"] * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": config_dict(cfg, 1, "single-thread CPU oracle"),
-            "cpu_baseline": cb,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(walls) / len(walls),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": conf, "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -237,6 +276,7 @@ def run_ours(args):
     params = inputs.model_params(cfg)
     _, ys = inputs.simulate(cfg)
     T = len(ys)
+    ys32 = [np.ascontiguousarray(y, np.float32) for y in ys]
     stream = torch.cuda.Stream(dev)
     with torch.cuda.stream(stream):
         y_dev = torch.tensor(np.asarray(ys, np.float32), device=dev)
@@ -244,8 +284,11 @@ def run_ours(args):
             f = pf.ParticleFilter(params, cfg.N, cfg.M, args.seed, stream=stream, theta=args.theta,
                                   airpf=args.airpf, multinomial=args.multinomial, rotate=args.rotate)
 
-            def step(k, yd=None):
-                f.step_dev(y_dev[k % T] if yd is None else yd)
+            def step(k):
+                f.step_dev(y_dev[k % T])
+
+            def step_host(k):  # the north_star call pf_step(h, y_host): y travels in the launch
+                f.step(ys32[k % T])
 
             def estimate():
                 return f.estimate(pf.PF_PHI_X, pf.PF_EST_FILTER)
@@ -254,18 +297,15 @@ def run_ours(args):
             # strong scaling: the global N of the configuration is split over the ranks
             f = pfd.LibBackend(params, cfg.N, cfg.M, args.seed, rank, world, stream=stream)
             tr = pfd.TorchTransport()
-            if args.exchange == "peer":
-                try:
-                    pfd.peer_connect(f, tr)
-                    ok = True
-                except pf.PFError as e:
-                    print(f"[bench] rank {rank}: peer mapping failed ({e}); pull exchange", file=sys.stderr)
-                    ok = False
-                if not all(tr.allgather_object(ok)):
-                    args.exchange = "pull"
+            if args.exchange == "peer" and not pfd.peer_connect(f, tr):
+                print(f"[bench] rank {rank}: peer mapping failed on some rank; pull exchange", file=sys.stderr)
+                args.exchange = "pull"
 
-            def step(k, yd=None):
-                pfd.sharded_step(f, tr, None, y_dev[k % T] if yd is None else yd, exchange=args.exchange)
+            def step(k):
+                pfd.sharded_step(f, tr, None, y_dev[k % T], exchange=args.exchange)
+
+            def step_host(k):
+                pfd.sharded_step(f, tr, ys32[k % T], exchange=args.exchange)
 
             def estimate():
                 return f.estimate(pf.PF_PHI_X, pf.PF_EST_FILTER)
@@ -342,19 +382,28 @@ def run_ours(args):
             if wi is not None and plain:
                 v["issue_frac"] = round(wi / sec / issue_peak(), 4)
         roofline["issue_frac_dominant"] = kernels.get(dom, {}).get("issue_frac")
+        # which roofline bounds the dominant kernel: the larger of its HBM fraction (algorithmic
+        # bytes) and its issue fraction (ncu warp instructions / the SMs' issue peak,
+        # 148 SMs x 4 schedulers x clock) -- "alu" when the issue slots bind
+        iss = roofline["issue_frac_dominant"]
+        if roofline["bound"] == "hbm" and iss is not None and iss > roofline["frac"]:
+            roofline.update({"bound": "alu", "hbm_frac": roofline["frac"], "achieved": round(iss * issue_peak(), 1),
+                             "peak": issue_peak(), "unit": "warp-inst/s", "frac": iss,
+                             "peak_source": "148 SMs x 4 schedulers x sm_max_mhz (MEASURED_PEAKS.json), one "
+                                            "warp instruction per scheduler per cycle"})
 
-        # end-to-end through the public API: pinned H2D of y_n, step, D2H of the estimate
+        # end-to-end through the public API, the north_star calls: pf_step(h, y_host) -- the
+        # observation (host memory) is copied into the launch parameters -- then
+        # pf_estimate(h, PF_PHI_X, PF_EST_FILTER, out_host), which reads the estimate back
+        # (device -> host) and synchronises.  Timed by the host clock, max over ranks.
         e2e = None
         if not args.no_e2e:
-            y_pin = torch.tensor(np.asarray(ys, np.float32)).pin_memory()
-            y_slot = torch.empty(cfg.dy, dtype=torch.float32, device=dev)
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             for k in range(args.steps):
-                y_slot.copy_(y_pin[(args.warmup + k) % T], non_blocking=True)
-                step(args.warmup + k, y_slot)
+                step_host(args.warmup + k)
                 est = estimate()
             torch.cuda.synchronize()
             te = time.perf_counter() - t0
@@ -363,13 +412,14 @@ def run_ours(args):
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 te = float(t.item())
             e2e = {"value": cfg.N * args.steps / te, "unit": UNIT, "h2d_bytes_per_step": 4 * cfg.dy,
-                   "d2h_bytes_per_step": 8 * cfg.d, "last_filter_mean": [float(v) for v in est]}
+                   "d2h_bytes_per_step": 8 * cfg.d, "api": "pf_step(h, y_host) + pf_estimate(h, PF_PHI_X, "
+                   "PF_EST_FILTER, out_host)", "last_filter_mean": [float(v) for v in est]}
         f.close()
 
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
-            cpu = oracle_sample(cfg, min(cfg.N, 1 << 21), 2)
+            cpu = cpu_baseline(cfg)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",

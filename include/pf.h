@@ -163,10 +163,17 @@ int pf_set_multinomial(pf_handle* h, int on);
 /* estimate kinds (reading R8) */
 #define PF_EST_FILTER 1  /* sum_i g_n(x^i) phi(x^i) / sum_i g_n(x^i): pi_hat_n */
 #define PF_EST_PREDICT 2 /* N^-1 sum_i phi(x^i): pi_n^N */
+#define PF_EST_RESAMPLED 3 /* N^-1 sum_i phi(x_hat^i): the empirical measure of the resampled
+                              sample, pi_hat_n^N; evaluated on demand from the
+                              step's output (through the island map after an AIRPF step; after
+                              an early-stopped adaptive step, of the S*-stage sample).  Sharded
+                              handles: the mean over THIS shard's N/G particles (shards are
+                              equally sized; dist.py averages them in rank order) */
 
 /* Synchronise the handle's stream and write the d estimates of the last completed
- * step into out (HOST, d doubles).  Errors: PF_ESTATE before the first step,
- * PF_EINVAL, PF_ECUDA. */
+ * step into out (HOST, d doubles).  FILTER and PREDICT are computed by the step itself;
+ * RESAMPLED launches k_moments + k_moments_final over x_hat first (fixed order,
+ * deterministic).  Errors: PF_ESTATE before the first step, PF_EINVAL, PF_ECUDA. */
 int pf_estimate(pf_handle* h, int phi, int kind, double* out);
 
 /* Release the handle (not the workspace, not the stream). NULL is a no-op. */
@@ -277,7 +284,8 @@ int pf_guard_check(pf_handle* h, unsigned char fill, uint64_t* bad_bytes);
 #define PF_DBG_LOGW 2      /* log g_n(x_n^i), N fp32 (needs PF_FLAG_DEBUG) */
 #define PF_DBG_ANC_STAGE 3 /* a_s(i), N int32, stage = s in 1..S (needs PF_FLAG_DEBUG) */
 #define PF_DBG_ANC_FINAL 4 /* A(i) = a_1(...a_S(i)), N int32 (needs PF_FLAG_DEBUG) */
-#define PF_DBG_XHAT 5      /* x_hat_n = x_n[A(i)], N x d fp32 */
+#define PF_DBG_XHAT 5      /* x_hat_n = x_n[A(i)], N x d fp32; before the first step: x_0 of
+                              pf_init (Alg. 1 l.1-3) */
 #define PF_DBG_LOGV 6      /* log V_s per block, all levels s = 1..S, m-1 fp64
                               (level s at offset m - m/2^{s-1}, m/2^s entries) */
 #define PF_DBG_ESS 8       /* E_0..E_S of the last adaptive step, S+1 fp64 (PF_FLAG_ADAPTIVE) */

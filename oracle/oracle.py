@@ -49,6 +49,7 @@ def lib():
         _lib.orc_normal.argtypes = [u64, u32, u32, u64]
         _lib.orc_normal.restype = ctypes.c_double
         _lib.orc_init.argtypes = [vp, u64, u64, vp]
+        _lib.orc_init_rows.argtypes = [vp, u64, u64, vp, vp]
         _lib.orc_mutate.argtypes = [vp, u64, u64, u32, vp, vp]
         _lib.orc_logweight.argtypes = [vp, u64, vp, vp, vp]
         _lib.orc_augmented_resample.argtypes = [u64, u64, u64, u32, vp, vp, vp, vp, vp]
@@ -117,6 +118,15 @@ def init(params: dict, N: int, seed: int) -> np.ndarray:
     mdl = make_model(params)
     x = np.zeros((N, mdl.d), np.float64)
     lib().orc_init(ctypes.byref(mdl), N, seed, _ptr(x))
+    return x
+
+
+def init_rows(params: dict, seed: int, rows: np.ndarray) -> np.ndarray:
+    """x_0 of the particles rows[] (orc_init restricted to those indices)."""
+    mdl = make_model(params)
+    r = np.ascontiguousarray(rows, dtype=np.int64)
+    x = np.zeros((r.size, mdl.d), np.float64)
+    lib().orc_init_rows(ctypes.byref(mdl), seed, r.size, _ptr(r), _ptr(x))
     return x
 
 

@@ -116,24 +116,34 @@ typedef struct {
 } orc_model;
 
 /* Alg. 1 l.296-298: zeta_0^i iid pi_0.  LG: m0 + L0 z; SV: m0 + s0 z. */
-void orc_init(const orc_model* mdl, uint64_t N, uint64_t seed, double* x0)
+/* x_0 of particle i (global index: the INIT counter). */
+static void init_one(const orc_model* mdl, uint64_t seed, uint64_t i, double* x)
 {
     int d = mdl->d;
-    for (uint64_t i = 0; i < N; ++i) {
-        double z[8];
-        for (int k = 0; k < d; ++k)
-            z[k] = orc_normal(seed, ORC_DOMAIN_INIT, 0u, i * (uint64_t)d + (uint64_t)k);
-        for (int k = 0; k < d; ++k) {
-            double v;
-            if (mdl->kind == 2) {
-                v = (double)mdl->sv_m0 + (double)mdl->sv_s0 * z[k];
-            } else {
-                v = (double)mdl->m0[k];
-                for (int j = 0; j < d; ++j) v += (double)mdl->L0[k * d + j] * z[j];
-            }
-            x0[i * d + k] = v;
+    double z[8];
+    for (int k = 0; k < d; ++k)
+        z[k] = orc_normal(seed, ORC_DOMAIN_INIT, 0u, i * (uint64_t)d + (uint64_t)k);
+    for (int k = 0; k < d; ++k) {
+        double v;
+        if (mdl->kind == 2) {
+            v = (double)mdl->sv_m0 + (double)mdl->sv_s0 * z[k];
+        } else {
+            v = (double)mdl->m0[k];
+            for (int j = 0; j < d; ++j) v += (double)mdl->L0[k * d + j] * z[j];
         }
+        x[k] = v;
     }
+}
+
+void orc_init(const orc_model* mdl, uint64_t N, uint64_t seed, double* x0)
+{
+    for (uint64_t i = 0; i < N; ++i) init_one(mdl, seed, i, x0 + i * (uint64_t)mdl->d);
+}
+
+/* orc_init evaluated on k given particle indices rows[] (full-size sampled parity). */
+void orc_init_rows(const orc_model* mdl, uint64_t seed, uint64_t k, const int64_t* rows, double* x0)
+{
+    for (uint64_t r = 0; r < k; ++r) init_one(mdl, seed, (uint64_t)rows[r], x0 + r * (uint64_t)mdl->d);
 }
 
 /* Alg. 1 l.302-303: zeta_n^i ~ f(zhat_{n-1}^i, .).

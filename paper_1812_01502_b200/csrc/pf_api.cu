@@ -207,6 +207,7 @@ struct Layout {
     size_t shard_rec, recs, top_logV, top_thr, top_scratch;
     size_t pull_src, pull_rank, pull_counts, pull_fill, pull_off, pull_req, pull_outpos, pull_serve;  // world > 1
     size_t dbg_x, dbg_lw, dbg_anc, dbg_A;
+    size_t mom_part, mom_out;          // PF_EST_RESAMPLED (k_moments)
     size_t guard_count;                // PF_FLAG_GUARD
     std::vector<size_t> gaps;          // PF_FLAG_GUARD: offsets of the PF_GUARD_BYTES gaps
     size_t total;
@@ -276,6 +277,8 @@ Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags, uint32
     L.dbg_anc = take(dbg ? (size_t)N * Sglobal * 4 : 0);
     (void)S;
     L.dbg_A = take(dbg ? N * 4 : 0);
+    L.mom_part = take((size_t)kMomPartDoubles * 8);
+    L.mom_out = take(16 * 8);
     L.guard_count = take(guard ? 16 : 0);
     L.total = off;
     return L;
@@ -1246,12 +1249,23 @@ int pf_run_dev(pf_handle* h, const float* y_dev, uint32_t T, double* est_dev) {
 int pf_estimate(pf_handle* h, int phi, int kind, double* out) {
     if (!h || !out) return fail(h, PF_EINVAL, "NULL argument");
     if (!h->have_step) return fail(h, PF_ESTATE, "no completed step");
-    if ((phi != PF_PHI_X && phi != PF_PHI_X2) || (kind != PF_EST_FILTER && kind != PF_EST_PREDICT))
+    if ((phi != PF_PHI_X && phi != PF_PHI_X2) ||
+        (kind != PF_EST_FILTER && kind != PF_EST_PREDICT && kind != PF_EST_RESAMPLED))
         return fail(h, PF_EINVAL, "bad phi / kind");
     const int D = h->plan.D;
-    const size_t off = (size_t)((kind == PF_EST_FILTER ? 0 : 2) + (phi == PF_PHI_X ? 0 : 1)) * D;
-    cudaError_t e = cudaMemcpyAsync(out, h->at<double>(h->lay.est) + off, sizeof(double) * D,
-                                    cudaMemcpyDeviceToHost, h->stream);
+    const double* src;
+    if (kind == PF_EST_RESAMPLED) {  // x_hat of the last step: X(cur) (through the island map after AIRPF)
+        double* part = h->at<double>(h->lay.mom_part);
+        double* res = h->at<double>(h->lay.mom_out);
+        const int32_t* isl = (h->airpf && h->isl_valid) ? h->at<int32_t>(h->lay.isl_A) : nullptr;
+        launch_moments(h->stream, D, h->X(h->cur), isl, h->b, h->N, part, res);
+        const int rc = check_cuda(h, "pf_estimate (resampled)");
+        if (rc != PF_OK) return rc;
+        src = res + (phi == PF_PHI_X ? 0 : D);
+    } else {
+        src = h->at<double>(h->lay.est) + (size_t)((kind == PF_EST_FILTER ? 0 : 2) + (phi == PF_PHI_X ? 0 : 1)) * D;
+    }
+    cudaError_t e = cudaMemcpyAsync(out, src, sizeof(double) * D, cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_estimate: ") + cudaGetErrorString(e));
     return PF_OK;
@@ -1293,7 +1307,9 @@ int pf_timing_read(pf_handle* h, double* ms, int* launches) {
 
 int pf_debug_ptr(pf_handle* h, int what, int stage, void** dev_out) {
     if (!h || !dev_out) return fail(h, PF_EINVAL, "NULL argument");
-    if (!h->have_step) return fail(h, PF_ESTATE, "no completed step");
+    // before the first step X(cur) holds x_0 (k_init): PF_DBG_XHAT reads it (A0 parity)
+    if (!h->have_step && !(what == PF_DBG_XHAT && h->n == 0 && !h->isl_valid))
+        return fail(h, PF_ESTATE, "no completed step");
     const bool dbg = h->flags & PF_FLAG_DEBUG;
     const int D = h->plan.D;
     switch (what) {
@@ -1416,8 +1432,11 @@ int pf_set_adaptive(pf_handle* h, double theta) {
         return fail(h, PF_EINVAL, "handle not created with PF_FLAG_ADAPTIVE");
     if (theta > 0.0 && h->world != 1) return fail(h, PF_EINVAL, "the fully adapted scheme needs world = 1");
     if (theta > 0.0 && (h->airpf || h->multinomial)) return fail(h, PF_EINVAL, "one resampling scheme at a time");
+    // an early-stopped step leaves weighted particles (R18): a plain step would treat them as
+    // equally weighted, so switching off is refused until a step has run all S stages
+    if (theta == 0.0 && h->carry_mode != 0)
+        return fail(h, PF_ESTATE, "particles carry weights of an early-stopped step: run one step with theta = 1 first");
     h->theta = theta;
-    if (theta == 0.0) h->carry_mode = 0;
     return PF_OK;
 }
 

@@ -177,6 +177,74 @@ void launch_block_gather(cudaStream_t st, const float* in, float* out, const int
     k_block_gather<<<1184, 256, 0, st>>>(in, out, A, N, b, D);
 }
 
+// ---- PF_EST_RESAMPLED: N^-1 sum_i phi(x_hat^i), phi in {x, x^2} ----------
+// Computed on demand from the step's output buffer (through the island map of an AIRPF
+// step, whose x_hat is never materialised).  Fixed grid, fixed order: thread partials in
+// fp32 over a strided range, warp and CTA sums in fp64, then one CTA sums the CTA
+// partials in index order -- deterministic.
+constexpr uint32_t kMomGrid = 592, kMomThreads = 256;
+
+template <int D>
+__global__ void __launch_bounds__(kMomThreads) k_moments(const float* __restrict__ x, const int32_t* __restrict__ isl,
+                                                         uint32_t b, uint64_t N, double* __restrict__ part) {
+    __shared__ double red[kMomThreads / 32][2 * D];
+    float s1[D], s2[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) s1[k] = s2[k] = 0.0f;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t src = i;
+        if (isl) src = ((uint64_t)__ldg(isl + (i >> b)) << b) | (i & ((1ull << b) - 1ull));
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const float v = __ldg(x + src * D + k);
+            s1[k] += v;
+            s2[k] = fmaf(v, v, s2[k]);
+        }
+    }
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        double a = s1[k], q = s2[k];
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            q += __shfl_xor_sync(0xffffffffu, q, o);
+        }
+        if (lane == 0) {
+            red[warp][k] = a;
+            red[warp][D + k] = q;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 2u * D) {
+        double t = 0.0;
+        for (uint32_t w = 0; w < kMomThreads / 32; ++w) t += red[w][threadIdx.x];
+        part[(uint64_t)blockIdx.x * 2 * D + threadIdx.x] = t;
+    }
+}
+
+template <int D>
+__global__ void k_moments_final(const double* __restrict__ part, uint64_t N, double* __restrict__ out) {
+    if (threadIdx.x < 2u * D) {
+        double t = 0.0;
+        for (uint32_t c = 0; c < kMomGrid; ++c) t += part[(uint64_t)c * 2 * D + threadIdx.x];
+        out[threadIdx.x] = t / (double)N;
+    }
+}
+
+void launch_moments(cudaStream_t st, int D, const float* x, const int32_t* isl, uint32_t b, uint64_t N, double* part,
+                    double* out) {
+    switch (D) {
+        case 1: k_moments<1><<<kMomGrid, kMomThreads, 0, st>>>(x, isl, b, N, part);
+                k_moments_final<1><<<1, 32, 0, st>>>(part, N, out); break;
+        case 2: k_moments<2><<<kMomGrid, kMomThreads, 0, st>>>(x, isl, b, N, part);
+                k_moments_final<2><<<1, 32, 0, st>>>(part, N, out); break;
+        case 4: k_moments<4><<<kMomGrid, kMomThreads, 0, st>>>(x, isl, b, N, part);
+                k_moments_final<4><<<1, 32, 0, st>>>(part, N, out); break;
+        default: k_moments<8><<<kMomGrid, kMomThreads, 0, st>>>(x, isl, b, N, part);
+                 k_moments_final<8><<<1, 32, 0, st>>>(part, N, out); break;
+    }
+}
+
 // ---- pull exchange (PullArgs in pf_kernels.cuh) ---------------------------------------
 // Requests per owner: a shared-memory histogram per CTA, one global atomic per bin per CTA
 // (G <= 64 bins).

@@ -56,6 +56,9 @@ void launch_block_gather(cudaStream_t st, const float* in, float* out, const int
 void launch_init(int D, int kind, const LaunchCfg& c, const InitArgs& a);
 void launch_top(int D, const LaunchCfg& c, const TopArgs& a);
 void launch_cross(int payload, bool dbg, const LaunchCfg& c, const CrossArgs& a);
+constexpr uint32_t kMomPartDoubles = 592u * 2u * 8u;  // k_moments CTA partials (grid x 2 D, D <= 8)
+void launch_moments(cudaStream_t st, int D, const float* x, const int32_t* isl, uint32_t b, uint64_t N, double* part,
+                    double* out);
 void launch_debug_compose(const LaunchCfg& c, const int32_t* anc, uint64_t N, uint32_t S, int32_t* A);
 
 }  // namespace pfk

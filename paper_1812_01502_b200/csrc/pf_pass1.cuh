@@ -416,10 +416,14 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : 1) 
                                   : rng_block(a.key, c0t + q, a.n, kDomainResample, 1u);
             const uint32_t pb = valid ? (((4u * q) >> pool_sh) << pool_sh) : 0u;
             const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
+            // the search target scales the pool total AS STORED in the CDF (same summation
+            // order as the entries it is compared with), so t <= C_{2M-1} and a zero-weight
+            // last entry can never be selected (reading R3)
+            const float totc = valid ? w[pb + 4u * Z - 1u] : 0.0f;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 lo[it][e] = pb;
-                tq[it][e] = valid ? u01f(r[e]) * tot[it] : -1.0f;
+                tq[it][e] = valid ? u01f(r[e]) * totc : -1.0f;
             }
         }
         for (uint32_t step = 2u * Z; step >= 1u; step >>= 1) {

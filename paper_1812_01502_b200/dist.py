@@ -243,6 +243,11 @@ class LibBackend:
         pf = self.pf
         return pf.pf_estimate(self.h, self.d, phi or pf.PF_PHI_X, kind or pf.PF_EST_FILTER)
 
+    def set_state(self, xhat_local: np.ndarray, n: int):
+        """This shard's x_hat_{n-1} (N/G x d fp32, HOST): the next step is time step n."""
+        nloc = self.N // self.world
+        self.pf.pf_debug_set_state(self.h, np.asarray(xhat_local, np.float32).reshape(nloc, self.d), n)
+
     def debug_get(self, what: int, stage: int = 0) -> np.ndarray:
         pf = self.pf
         ptr = pf.pf_debug_ptr(self.h, what, stage)
@@ -279,20 +284,33 @@ def sharded_step(backend, transport, y, y_dev=None, exchange: str = "pairwise") 
     whole-buffer swaps with the butterfly partner) or "pull" (one all-to-all of exactly
     the states each rank's outputs read) or "peer" (one kernel reads them straight from
     the owners' memory over NVLink; peer_connect first)."""
-    rec = backend.step_local(y) if y_dev is None else backend.step_local_dev(y_dev)
-    backend.step_top(transport.allgather(rec))
-    if exchange == "peer":
-        peer_exchange(backend, transport)
-        return
-    if exchange == "pull":
-        pull_exchange(backend, transport)
-        return
-    world = transport.world
-    L = world.bit_length() - 1
-    for t in range(1, L + 1):
-        buf = backend.cross_buffer()
-        recv = transport.exchange(buf, partner(transport.rank, t))
-        backend.cross_stage(t, recv)
+    with _on_stream(backend):  # every transport call is ordered on the backend's stream
+        rec = backend.step_local(y) if y_dev is None else backend.step_local_dev(y_dev)
+        backend.step_top(transport.allgather(rec))
+        if exchange == "peer":
+            peer_exchange(backend, transport)
+            return
+        if exchange == "pull":
+            pull_exchange(backend, transport)
+            return
+        world = transport.world
+        L = world.bit_length() - 1
+        for t in range(1, L + 1):
+            buf = backend.cross_buffer()
+            recv = transport.exchange(buf, partner(transport.rank, t))
+            backend.cross_stage(t, recv)
+
+
+def _on_stream(backend):
+    """Context that makes the backend's CUDA stream torch's current stream, so NCCL
+    collectives issued by the transport are stream-ordered after the library's kernels
+    (a no-op for CPU stand-ins)."""
+    import contextlib
+    st = getattr(backend, "stream", None)
+    if st is None or not hasattr(st, "cuda_stream"):
+        return contextlib.nullcontext()
+    import torch
+    return torch.cuda.stream(st)
 
 
 def pull_exchange(backend, transport) -> None:
@@ -311,11 +329,26 @@ def pull_exchange(backend, transport) -> None:
     backend.pull_finish(states)
 
 
-def peer_connect(backend, transport) -> None:
-    """Set-up of the peer-memory exchange: all-gather every rank's (IPC handle, offset) and
-    map the other ranks' workspaces (include/pf.h pf_peer_export / pf_peer_open)."""
-    got = transport.allgather_object(backend.peer_export())
-    backend.peer_open([g[0] for g in got], [g[1] for g in got])
+def peer_connect(backend, transport) -> bool:
+    """Set-up of the peer-memory exchange: all-gather every rank's (ok, IPC handle, offset)
+    ONCE and map the other ranks' workspaces (include/pf.h pf_peer_export / pf_peer_open).
+    A rank whose export fails still takes part in the gather, so every rank sees the same
+    verdict; the mapping results are agreed in a second gather.  Returns True when every
+    rank mapped its peers (else the caller uses another exchange on every rank)."""
+    try:
+        hd, off = backend.peer_export()
+        mine = (True, hd, off)
+    except Exception:  # noqa: BLE001 -- any export failure means "no peer exchange here"
+        mine = (False, b"", 0)
+    got = transport.allgather_object(mine)
+    if not all(g[0] for g in got):
+        return False
+    try:
+        backend.peer_open([g[1] for g in got], [g[2] for g in got])
+        ok = True
+    except Exception:  # noqa: BLE001
+        ok = False
+    return all(transport.allgather_object(ok))
 
 
 def peer_exchange(backend, transport) -> None:
@@ -325,6 +358,16 @@ def peer_exchange(backend, transport) -> None:
     barrier after the gather keeps every rank's next step from overwriting them early."""
     backend.cross_peer()
     transport.device_barrier(getattr(backend, "stream", None))
+
+
+def resampled_estimate(backend, transport, phi: int) -> np.ndarray:
+    """PF_EST_RESAMPLED of the whole sharded sample: every rank's shard mean (equal shard
+    sizes), all-gathered and averaged in rank order (the same value on every rank)."""
+    import torch
+    loc = backend.estimate(phi, backend.pf.PF_EST_RESAMPLED)
+    t = torch.tensor(loc, dtype=torch.float64, device=transport_device(transport))
+    allm = transport.allgather(t).cpu().numpy()
+    return allm.sum(axis=0) / allm.shape[0]
 
 
 def loopback_peer(backends: Sequence) -> None:

@@ -26,7 +26,7 @@ PF_FLAG_AIRPF = 4
 PF_FLAG_MULTINOMIAL = 8
 PF_FLAG_GUARD = 16
 PF_PHI_X, PF_PHI_X2 = 1, 2
-PF_EST_FILTER, PF_EST_PREDICT = 1, 2
+PF_EST_FILTER, PF_EST_PREDICT, PF_EST_RESAMPLED = 1, 2, 3
 PF_DBG_X, PF_DBG_LOGW, PF_DBG_ANC_STAGE, PF_DBG_ANC_FINAL, PF_DBG_XHAT, PF_DBG_LOGV, PF_DBG_THRESH = 1, 2, 3, 4, 5, 6, 7
 PF_DBG_ESS = 8
 PF_DBG_ISLAND_A, PF_DBG_ISLAND_CHOICE, PF_DBG_ISLAND_LOGW = 9, 10, 11

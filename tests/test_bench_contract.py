@@ -20,7 +20,11 @@ def test_reference_arm_line():
         assert k in line, k
     assert line["impl"] == "reference" and line["steps"] == 2 and line["value"] > 0
     assert line["config"]["workload"] == "C1"
-    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] == 1
+    # the printed config is the one timed (the sample), with the workload it samples
+    assert line["config"]["N"] <= line["config"]["sample_of"]["N"]
+    assert line["config"]["N"] == line["config"]["M"] * line["config"]["m"]
+    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
+    assert line["cpu_baseline"]["value"] == line["value"]
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
 
 

@@ -160,9 +160,16 @@ def _worker(rank, world, port, q, exchange="pairwise", peer_dir=None):
         N, M = 256, 16
         be = OracleShard(params, N, M, 5, rank, world, peer_dir=peer_dir)
         tr = pfd.TorchTransport()
+        if exchange == "peer_fail":  # one rank cannot export: every rank agrees on "no peer"
+            if rank == world - 1:
+                def bad_export():
+                    raise RuntimeError("no IPC on this rank")
+                be.peer_export = bad_export
+            assert pfd.peer_connect(be, tr) is False
+            exchange = "pull"
         if exchange == "peer":
             dist.barrier()  # every rank's buffer file exists
-            pfd.peer_connect(be, tr)
+            assert pfd.peer_connect(be, tr) is True
         _, ys = inputs.simulate(cfg, T=3)
         for y in ys:
             pfd.sharded_step(be, tr, y, exchange=exchange)
@@ -183,7 +190,7 @@ def _free_port():
 
 
 @pytest.mark.parametrize("world,exchange", [(2, "pairwise"), (4, "pairwise"), (2, "pull"), (4, "pull"),
-                                            (2, "peer"), (4, "peer")])
+                                            (2, "peer"), (4, "peer"), (4, "peer_fail")])
 def test_gloo_sharded_sequence(world, exchange, tmp_path):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

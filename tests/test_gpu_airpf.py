@@ -31,7 +31,8 @@ def _snap(f, d):
                 logW=f.debug_get(pfb.PF_DBG_ISLAND_LOGW), logV=f.debug_get(pfb.PF_DBG_LOGV),
                 choice=np.stack([f.debug_get(pfb.PF_DBG_ISLAND_CHOICE, s) for s in range(1, S + 1)]),
                 A=f.debug_get(pfb.PF_DBG_ISLAND_A), xhat=f.debug_get(pfb.PF_DBG_XHAT),
-                filt=f.estimate(pfb.PF_PHI_X, pfb.PF_EST_FILTER), pred=f.estimate(pfb.PF_PHI_X, pfb.PF_EST_PREDICT))
+                filt=f.estimate(pfb.PF_PHI_X, pfb.PF_EST_FILTER), pred=f.estimate(pfb.PF_PHI_X, pfb.PF_EST_PREDICT),
+                res=f.estimate(pfb.PF_PHI_X, pfb.PF_EST_RESAMPLED))
 
 
 def _check(g, o, N, M, d):
@@ -67,6 +68,14 @@ def _check(g, o, N, M, d):
     pu.check_x(g["xhat"].reshape(N, d)[rows], o["xhat"][rows])
     pu.check_estimate(g["filt"], o["filter"][:d], o["filter"][d:])
     pu.check_estimate(g["pred"], o["predict"][:d], o["predict"][d:])
+    # PF_EST_RESAMPLED through the island map = the mean of the materialised x_hat; against
+    # the oracle's x_hat with an allowance for the flagged rows
+    xh = g["xhat"].reshape(N, d).astype(np.float64)
+    if np.all(np.isfinite(xh)):
+        assert np.allclose(g["res"], xh.mean(axis=0), rtol=1e-5, atol=1e-6)
+        nfl = N - int(rows.sum())
+        pu.check_estimate_allow(g["res"], o["xhat"].mean(axis=0), (o["xhat"] ** 2).mean(axis=0),
+                                nfl / N * np.ptp(o["x"], axis=0))
     return int(path_fl.sum()) + int((~ok_w).sum())
 
 

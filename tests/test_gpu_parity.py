@@ -39,6 +39,8 @@ def _gpu_step(params, N, M, seed, n, xhat, y):
         filt2=f.estimate(pfb.PF_PHI_X2, pfb.PF_EST_FILTER),
         pred=f.estimate(pfb.PF_PHI_X, pfb.PF_EST_PREDICT),
         pred2=f.estimate(pfb.PF_PHI_X2, pfb.PF_EST_PREDICT),
+        res=f.estimate(pfb.PF_PHI_X, pfb.PF_EST_RESAMPLED),
+        res2=f.estimate(pfb.PF_PHI_X2, pfb.PF_EST_RESAMPLED),
         launches=f.launches(),
     )
     f.close()
@@ -68,6 +70,14 @@ def _compare(orc, cfg_name, N, M, n, seed=1234, cloud_seed=99, outlier=0.0, xhat
     pu.check_estimate(g["pred"], o["predict"][:d], o["predict"][d:])
     assert np.all(np.abs(g["filt2"] - o["filter"][d:]) <= 1e-4 * np.abs(o["filter"][d:]) + 1e-12)
     assert np.all(np.abs(g["pred2"] - o["predict"][d:]) <= 1e-4 * np.abs(o["predict"][d:]) + 1e-12)
+    # PF_EST_RESAMPLED: N^-1 sum phi(x_hat) against the oracle's resampled leg; outputs whose
+    # (flagged) path picked another ancestor may move it by at most their share of the range
+    nmis = int((g["A"] != o["A"]).sum())
+    span = np.ptp(o["x"], axis=0) if N > 1 else np.zeros(d)
+    allow = nmis / N * span
+    pu.check_estimate_allow(g["res"], o["resampled"][:d], o["resampled"][d:], allow)
+    pu.check_estimate_allow(g["res2"], o["resampled"][d:], None, nmis / N * np.ptp(o["x"] ** 2, axis=0),
+                            second=False)
     return dict(stats=stats, flagged_paths=int(flagged.sum()), launches=g["launches"])
 
 

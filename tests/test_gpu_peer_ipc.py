@@ -48,7 +48,7 @@ def _worker(rank, world, port, q, name, N, M):
         _, ys = inputs.simulate(cfg, T=3)
         be = pfd.LibBackend(p, N, M, 33, rank, world, debug=True)
         tr = HostGatherTransport()
-        pfd.peer_connect(be, tr)
+        assert pfd.peer_connect(be, tr)
         out = []
         for y in ys:
             pfd.sharded_step(be, tr, y, exchange="peer")

@@ -69,3 +69,37 @@ def test_peer_exchange_errors():
     single.close()
     for b in shards:
         b.close()
+
+
+@pytest.mark.parametrize("exchange", ["pairwise", "pull", "peer"])
+@pytest.mark.parametrize("name,N,M,G,n", [("C4", 1 << 15, 64, 4, 1), ("C3", 1 << 14, 32, 8, 3),
+                                          ("C2", 1 << 14, 256, 2, 2), ("C1", 1024, 16, 8, 0)])
+def test_shards_match_oracle(orc, name, N, M, G, n, exchange):
+    """Every shard against the fp64 oracle (not only against the one-GPU CUDA path): the
+    shards start from slices of one seeded cloud; each stage's ancestor table (local
+    stages from k_pass1 / k_stages, cross stages from k_cross / k_pull_compose /
+    k_peer_gather) is bit-exact wherever the oracle's draw is >= 1e-6 from its boundary,
+    x_hat matches on outputs whose path holds no flagged draw, estimates within R15."""
+    from . import parity_util as pu
+    cfg = inputs.CONFIGS[name]
+    p = inputs.model_params(cfg)
+    d = int(p["d"])
+    S = int(np.log2(N // M))
+    xin = inputs.particle_cloud(cfg, N, 31).reshape(N, d)
+    y = inputs.observation_for_step(cfg, 40 + n)
+    o = orc.step(p, N, M, 77, n, y, xin)
+    nloc = N // G
+    shards = [pfd.LibBackend(p, N, M, 77, r, G, debug=True) for r in range(G)]
+    for r, b in enumerate(shards):
+        b.set_state(xin[r * nloc:(r + 1) * nloc], n)
+    pfd.loopback_step(shards, y, exchange=exchange)
+    a = np.stack([np.concatenate([b.debug_get(pfb.PF_DBG_ANC_STAGE, s) for b in shards]) for s in range(1, S + 1)])
+    pu.check_stage_tables(a, o["a"], o["delta"])
+    flagged = pu.path_flags(o["a"], o["delta"])
+    xg = np.concatenate([b.debug_get(pfb.PF_DBG_XHAT) for b in shards]).reshape(N, d)
+    pu.check_x(xg[~flagged], o["xhat"][~flagged])
+    for b in shards:
+        pu.check_estimate(b.estimate(pfb.PF_PHI_X, pfb.PF_EST_FILTER), o["filter"][:d], o["filter"][d:])
+        pu.check_estimate(b.estimate(pfb.PF_PHI_X, pfb.PF_EST_PREDICT), o["predict"][:d], o["predict"][d:])
+        b.close()
+    assert flagged.mean() < 0.05

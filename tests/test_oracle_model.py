@@ -125,3 +125,12 @@ def test_paper_raw_observation_mse_closed_form():
     # (y - xbar) is Gaussian with variance per => sum of squares has sd per*sqrt(2*d*n_max)
     sd = per * np.sqrt(2 * 7 * 8000)
     assert abs(2396 - expected) < 2 * sd
+
+
+def test_init_rows_is_init_restricted(orc):
+    """orc_init_rows (full-size sampled parity) evaluates exactly orc_init's rows."""
+    for name in ("C4", "C3", "C2"):
+        p = inputs.model_params(inputs.CONFIGS[name])
+        full = orc.init(p, 256, 17)
+        rows = np.array([0, 1, 5, 128, 255])
+        assert np.array_equal(orc.init_rows(p, 17, rows), full[rows])
