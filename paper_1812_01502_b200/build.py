@@ -43,9 +43,31 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _deps(src: str):
+    """Headers a unit includes (nvcc -M, cached next to its object; refreshed when stale):
+    a kernel edit rebuilds only the units that include it."""
+    dfile = _obj(src) + ".d"
+    if os.path.exists(dfile) and not _stale(dfile, [src]):
+        with open(dfile) as f:
+            deps = [d for d in f.read().split() if os.path.exists(d)]
+        if deps and not _stale(dfile, deps):
+            return deps
+    r = subprocess.run([nvcc()] + NVCC_FLAGS + ["-M", src], cwd=HERE, capture_output=True, text=True)
+    if r.returncode != 0:
+        return HEADERS
+    toks = r.stdout.replace("\\\n", " ").split()
+    deps = [os.path.abspath(os.path.join(HERE, t)) for t in toks
+            if t.endswith((".cuh", ".h", ".inc")) and (CSRC in os.path.abspath(os.path.join(HERE, t))
+                                                       or t.endswith("pf.h"))]
+    os.makedirs(OBJ, exist_ok=True)
+    with open(dfile, "w") as f:
+        f.write("\n".join(deps))
+    return deps
+
+
 def needs_build() -> bool:
     objs = [_obj(s) for s in sources()]
-    return _stale(LIB, sources() + HEADERS) or any(_stale(o, [s] + HEADERS) for s, o in zip(sources(), objs))
+    return _stale(LIB, sources() + HEADERS) or any(_stale(o, [s] + _deps(s)) for s, o in zip(sources(), objs))
 
 
 def _compile(src: str, verbose: bool) -> str:
@@ -61,7 +83,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     os.makedirs(OBJ, exist_ok=True)
-    todo = [s for s in sources() if force or _stale(_obj(s), [s] + HEADERS)]
+    todo = [s for s in sources() if force or _stale(_obj(s), [s] + _deps(s))]
     with cf.ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 4))) as ex:
         logs = list(ex.map(lambda s: _compile(s, verbose), todo))
     if verbose:

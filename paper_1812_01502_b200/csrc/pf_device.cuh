@@ -247,4 +247,10 @@ __device__ __forceinline__ void pair_level_fast(double vl, double vr, int b, dou
     *P = (uint32_t)(p * __int_as_float((127 + 32 - b) << 23));  // floor(p 2^(32-b)), p 2^(32-b) >= 0
 }
 
+// Four consecutive payload elements moved as one vector.
+template <typename T>
+struct __align__(4 * sizeof(T) <= 16 ? 4 * sizeof(T) : 16) Vec4 {
+    T v[4];
+};
+
 }  // namespace pfk

@@ -2,6 +2,7 @@
 #include <algorithm>
 
 #include "pf_launch.h"
+#include "pf_kernels.cuh"
 
 namespace pfk {
 

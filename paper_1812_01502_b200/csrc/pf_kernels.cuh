@@ -29,11 +29,10 @@
 #include <cstdint>
 
 #include "pf_device.cuh"
-#include "pf_pass1.cuh"
+#include "pf_args.h"
 
 namespace pfk {
 
-constexpr int kCascadeThreads = 1024;
 constexpr uint32_t FULL = 0xffffffffu;
 
 
@@ -80,14 +79,6 @@ __device__ __forceinline__ void store_quad(float* __restrict__ x, uint64_t i0, c
 }
 
 // -------------------------------------------------------------------------------------
-struct InitArgs {
-    ModelParams mp;
-    Key key;
-    uint64_t N;     // particles of this shard
-    uint32_t pos0;  // global index of its first particle (multiple of 4)
-    float* x;
-};
-
 template <int D, int KIND>
 __global__ void __launch_bounds__(256) k_init(const __grid_constant__ InitArgs a) {
     const uint64_t nq = a.N >> 2;
@@ -105,18 +96,6 @@ __global__ void __launch_bounds__(256) k_init(const __grid_constant__ InitArgs a
 }
 
 // -------------------------------------------------------------------------------------
-struct CascadeArgs {
-    double* logV;
-    uint32_t* thr;
-    const double* part;  // NT tile partials
-    double* scratch;     // >= NT + 2 partials (tree levels)
-    double* est;         // outputs: filter[2D], predict[2D] (single shard)
-    double* shard_rec;   // sharded runs: {log V at level S (= S_loc), root partial[2+4D]}
-    uint32_t* ticket;
-    uint64_t N;
-    uint32_t m, S, k1, b, NT, LPC;
-};
-
 template <int D>
 __device__ __forceinline__ void combine_partial(const double* x, const double* y, double* out) {
     constexpr int PS = 2 + 4 * D;
@@ -250,29 +229,6 @@ __global__ void __launch_bounds__(kCascadeThreads) k_cascade(const __grid_consta
 //                 the global max of lw (V_s <= max w, so no term overflows); fixed order
 //   k_ess_final   one thread per level sums its chunks in order -> E_s; thread 0 -> S*,
 //                 log V_S; resets the running max for the next step
-constexpr uint32_t kEssChunk = 4096;
-constexpr int kEssThreads = 256;
-
-struct EssArgs {
-    const double* ess_part;  // NT x 3
-    const double* logV;      // level table (m - 1)
-    unsigned int* lmax;      // running max of lw (float_order_bits), reset by k_ess_final
-    double* chunks;          // 2 per chunk
-    double* out;             // E_0..E_S, S*, log V_S
-    uint64_t N;
-    uint32_t NT, m, S;
-    double theta;
-};
-
-__host__ __device__ inline uint32_t ess_level_count(const EssArgs& a, uint32_t s) {
-    return s == 0 ? a.NT : (a.m >> s);
-}
-__host__ __device__ inline uint32_t ess_chunks_total(const EssArgs& a) {
-    uint32_t t = 0;
-    for (uint32_t s = 0; s <= a.S; ++s) t += (ess_level_count(a, s) + kEssChunk - 1) / kEssChunk;
-    return t;
-}
-
 // -------------------------------------------------------------------------------------
 // AIRPF island stages (Alg. 6 / Alg. 7; R20, R21).
 //   k_island_draw     thread per (stage s, quad of islands): the four islands' side draws
@@ -281,39 +237,9 @@ __host__ __device__ inline uint32_t ess_chunks_total(const EssArgs& a) {
 //                     block when the partner lies in another quad); writes one nibble per
 //                     quad: bit e = island 4 quad + e takes its partner's block
 //   k_island_compose  thread per island: walks stages S..1 through the nibbles -> A_isl
-struct IslandArgs {
-    Key key;
-    uint32_t n, m, S;
-    int modified;
-    const uint32_t* thr;   // side thresholds, level-table layout (stage s at level_offset(m, s))
-    uint8_t* choice;       // S x nq nibbles (nq = ceil(m / 4))
-    int32_t* A;            // m: island map
-};
-
 // -------------------------------------------------------------------------------------
 // Multinomial resampling, Alg. 2 (kernels in pf_multinomial.cu).
-constexpr uint32_t kMnTile = 1024;  // particles per CDF tile (one CTA of 1024 threads)
-
-struct MultinomialArgs {
-    Key key;
-    uint32_t n, NT;              // NT: CDF tiles of kMnTile particles
-    uint64_t N;
-    float* cdf;                  // N: per-tile local CDFs
-    float* cdf32;                // N / 32: the local CDF at every 32nd particle (chunk ends)
-    double* trec;                // NT x {tile max, tile total}
-    double* off;                 // NT + 1: tile offsets in the global CDF, off[NT] = C
-    const unsigned int* lmax;    // max lw (order-preserving bits; from the weigh pass)
-    const float* x;              // x_n (N x d)
-    float* xhat;                 // x_hat_n (N x d)
-    int32_t* dbg_anc;            // ancestors (debug) or nullptr
-};
-
 // -------------------------------------------------------------------------------------
-template <typename T>
-struct __align__(4 * sizeof(T) <= 16 ? 4 * sizeof(T) : 16) Vec4 {
-    T v[4];
-};
-
 // -------------------------------------------------------------------------------------
 // Sharded runs (G = 2^L GPUs, shard r owns groups [r m/G, (r+1) m/G)).
 //
@@ -323,16 +249,6 @@ struct __align__(4 * sizeof(T) <= 16 ? 4 * sizeof(T) : 16) Vec4 {
 // estimate (perfect binary tree over the shard partials = the upper levels of the
 // single-GPU tree over tiles).  Top level t (= stage S_loc + t) has G >> t entries at
 // offset G - (G >> (t-1)).
-struct TopArgs {
-    const double* recs;  // G x (1 + PS)
-    double* top_logV;    // G - 1
-    uint32_t* top_thr;   // G - 1
-    double* est;
-    double* scratch;     // >= 2 G partials
-    uint64_t Nglobal;
-    uint32_t G, L, b;
-};
-
 template <int D>
 __global__ void __launch_bounds__(1024) k_top(const __grid_constant__ TopArgs a) {
     constexpr int PS = 2 + 4 * D;
@@ -376,18 +292,6 @@ __global__ void __launch_bounds__(1024) k_top(const __grid_constant__ TopArgs a)
 // local group gl pairs with the SAME local group of the partner.  Every output's draw
 // (side, index) is counter-based, so each output reads its source state from this
 // shard's or the partner's stage-(s-1) buffer (the partner's arrives whole over NVLink).
-struct CrossArgs {
-    Key key;
-    uint32_t n, s, t, rank, b, M;
-    uint64_t Nloc;
-    uint32_t pos0, pos0_partner;
-    const uint32_t* thr;    // the stage threshold (device): top_thr entry of block rank >> t
-    const void* own_in;
-    const void* partner_in;
-    void* out;
-    int32_t* dbg_anc;       // this shard's stage tables (global source positions)
-};
-
 template <typename T, bool DBG>
 __global__ void __launch_bounds__(256) k_cross(const __grid_constant__ CrossArgs a) {
     const T* own = reinterpret_cast<const T*>(a.own_in);
@@ -428,30 +332,6 @@ __global__ void __launch_bounds__(256) k_cross(const __grid_constant__ CrossArgs
 // (rank, local position) of its stage-S_loc source; the requests are grouped by owner
 // rank, exchanged in one all-to-all, served by a gather on the owner, and the states come
 // back in a second all-to-all.  Same draws and the same x_hat as the pairwise rounds.
-struct PullArgs {
-    Key key;
-    uint32_t n, S_loc, L, rank, b, M;
-    uint64_t Nloc;
-    const uint32_t* top_thr;  // G - 1 top thresholds (top level t at G - (G >> (t-1)))
-    uint32_t G;
-    uint32_t* src_local;      // Nloc: local position of the source on its owner
-    uint32_t* src_rank;       // Nloc: owner rank
-    unsigned long long* counts;  // G: requests per owner rank
-    uint32_t* fill;           // G: slots used (pack)
-    const unsigned long long* offsets;  // G: start of each owner's requests (pack)
-    uint32_t* req;            // Nloc: requests grouped by owner rank
-    uint32_t* outpos;         // Nloc: request slot of output l (where its state arrives)
-    int32_t* dbg_anc;         // stage tables (debug) or nullptr
-};
-
-// Peer-memory exchange (pf_cross_peer): every rank's stage-S_loc state buffer, mapped into
-// this process (CUDA IPC over NVLink, or local pointers for shards on one GPU).
-constexpr uint32_t kPeerMaxG = 64;
-struct PeerArgs {
-    const float* x[kPeerMaxG];  // x[r] = rank r's X(cur), Nloc x d fp32
-    float* out;                 // this shard's x_hat (X(cur ^ 1))
-};
-
 // -------------------------------------------------------------------------------------
 // Debug helpers (not on the timed path).
 template <int UNUSED>

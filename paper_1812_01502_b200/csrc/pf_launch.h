@@ -4,8 +4,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
-#include "pf_kernels.cuh"
-#include "pf_stages.cuh"
+#include "pf_args.h"
 
 namespace pfk {
 

@@ -11,6 +11,7 @@
 //                  a(i) = #{k < N-1 : C_k <= t}; gathers x_hat^i = x^{a(i)} (the one random
 //                  HBM access of this algorithm)
 #include "pf_launch.h"
+#include "pf_kernels.cuh"
 
 namespace pfk {
 

@@ -4,7 +4,8 @@
 //   load xhat_{n-1} (coalesced) -> mutate (Alg. 1 l.303) -> log g_n
 //    -> stage 1 over the pairs (2p, 2p+1) (Alg. 3 l.346-349): pair max,
 //   weights c = exp(lw - max), warp-shuffle segmented inclusive scan, branch-free binary
-//   searches of the inverse CDF -> V level 1 per pair; then every warp redundantly builds
+//   searches of the inverse CDF (pools of <= 32 quads: over the CDF held in the lanes'
+//   registers, by shuffles; wider pools: in shared memory) -> V level 1 per pair; then every warp redundantly builds
 //   the tile's V levels 2..k1 and side thresholds in its lanes (log-domain pair means,
 //   eq. V_defn_proofs) -> draws of stages 2..k1 into per-stage tables ->
 //   each output walks its ancestry back through the tables and writes its state, already
@@ -22,100 +23,9 @@
 #include <cstdint>
 #include <cstring>
 
-#include "pf_device.cuh"
+#include "pf_args.h"
 
 namespace pfk {
-
-constexpr uint32_t kFull = 0xffffffffu;
-constexpr uint32_t kPass1MaxGroups = 64;  // T1 <= 64: the V tree of a tile fits one warp's lanes
-
-struct Pass1Smem {
-    uint32_t xs, w, L1, tab, chunk, lv1, red, ess, total;
-};
-__host__ __device__ inline Pass1Smem pass1_smem(int D, uint32_t P1, uint32_t M, uint32_t k1, uint32_t threads,
-                                                uint32_t tb) {
-    Pass1Smem s;
-    uint32_t off = 0;
-    auto take = [&](uint32_t bytes) {
-        const uint32_t o = off;
-        off += (bytes + 15u) & ~15u;
-        return o;
-    };
-    const uint32_t T1 = P1 / M;
-    s.xs = take(P1 * 4u * (uint32_t)D);
-    s.w = take(P1 * 4u);
-    s.L1 = take(P1 * tb);
-    s.tab = take(k1 >= 2 ? (k1 - 1u) * P1 * tb : 0u);
-    s.chunk = take(M > 64 ? (P1 / 128u) * 4u : 0u);  // per-warp-chunk maxima / totals
-    s.lv1 = take(T1 * 8u);  // pair (or, AIRPF, island) log-means
-    s.red = take((threads / 32u) * (2u + 4u * (uint32_t)D) * 4u);
-    s.ess = take((threads / 32u) * 4u);  // per-warp sum of squared weights (kPass1Weigh)
-    s.total = off;
-    return s;
-}
-
-struct Pass1Args {
-    ModelParams mp;
-    Key key;
-    uint32_t n;
-    int do_mutate;
-    const float* y_dev;  // if non-null, y is read from device memory
-    float y[8];
-    uint64_t N;           // particles of this shard
-    uint32_t pos0;        // global index of the shard's first particle (RNG counters)
-    uint32_t m, M, b, S, k1, P1, T1;
-    Pass1Smem sl;         // shared-memory layout (pass1_smem)
-    const float* x_in;    // xhat_{n-1} (or x_0)
-    float* x_out;         // particles moved to their stage-k1 positions
-    double* logV;         // level table (m - 1)
-    uint32_t* thr;        // threshold table (m - 1)
-    double* part;         // per-tile estimate partials, (2 + 4D) doubles each
-    float* dbg_x;
-    float* dbg_lw;
-    int32_t* dbg_anc;
-    // fully adapted scheme (R17/R18; modes below)
-    float* lw_out;          // kPass1Weigh: log-weights lw = carry + log g (N fp32)
-    const float* lw_in;     // kPass1Resample: the same log-weights, read back
-    int carry_mode;         // 0 none, 1 particle carry lw_prev[i] - c, 2 block carry lvl[g >> shift] - c
-    const float* carry_lw;  // previous step's lw (carry_mode 1)
-    const double* carry_lv; // previous step's level-S* values (carry_mode 2)
-    uint32_t carry_shift;   // block index of group g: (g >> carry_shift) & carry_mask (carry_mode 2)
-    uint32_t carry_mask;
-    uint32_t out_rot;       // stage rotation (R23): the tile is written to the next layout,
-                            // group g -> rotr_S(g, out_rot); 0 = no move (needs M >= 4)
-    double carry_c;         // log V_S of the previous step
-    double* ess_part;       // kPass1Weigh: per tile {max lw, sum e^{lw-max}, sum e^{2(lw-max)}}
-    unsigned int* ess_lmax; // kPass1Weigh: running max of lw (order-preserving float bits)
-    // AIRPF (kPass1Airpf; R19-R21)
-    const int32_t* isl_src; // previous step's island map A_isl (group g reads block isl_src[g]); null = identity
-    double* logW;           // log island means (m)
-};
-
-// Order-preserving map of float bits to unsigned (atomicMax of floats).
-__host__ __device__ inline unsigned int float_order_bits(float f) {
-#ifdef __CUDA_ARCH__
-    const unsigned int u = __float_as_uint(f);
-#else
-    unsigned int u;
-    memcpy(&u, &f, 4);
-#endif
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-
-// k_pass1 modes: the fused step (mutate, weight, stages 1..k1, tile written moved) or the
-// two halves of a fully adapted step, which must know every ESS before its first draw:
-//   kPass1Weigh    mutate, weight (+ carried weight), V levels 1..k1 and thresholds,
-//                  estimate and ESS partials; writes x_n (natural order) and lw
-//   kPass1Resample stage 1 and stages 2..k1 from x_n and lw (no mutation, no weighting)
-constexpr int kPass1Fused = 0;
-constexpr int kPass1Weigh = 1;
-constexpr int kPass1Resample = 2;
-//   kPass1Airpf    AIRPF (Alg. 4): mutate the island blocks named by the previous island
-//                  map, weight, within-island resample (Alg. 5: pool = the island's M
-//                  particles, WITHIN draws), island log-means, island levels 1..k1 and the
-//                  island side thresholds (31-bit, R20); writes the within-resampled
-//                  sample in natural order (the island stages run in k_island_*)
-constexpr int kPass1Airpf = 3;
 
 // Sum of NV = 2^v values over the 32 lanes of a warp by recursive halving: after the
 // call, lane l holds the total of value (l >> (5 - v)) in v[0].
@@ -395,43 +305,81 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : 1) 
     for (int it = 0; it < QPT; ++it) {
         const uint32_t q = tid + it * threads;
         if (q >= nq) continue;
-        reinterpret_cast<float4*>(w)[q] =
-            make_float4(excl[it] + run[it][0], excl[it] + run[it][1], excl[it] + run[it][2], excl[it] + run[it][3]);
+        if (Z > 32u)  // pools wider than a warp are searched in shared memory
+            reinterpret_cast<float4*>(w)[q] =
+                make_float4(excl[it] + run[it][0], excl[it] + run[it][1], excl[it] + run[it][2], excl[it] + run[it][3]);
         if (((4u * q) & ((1u << pool_sh) - 1u)) == 0u) {  // first quad of its pool: log mean of the pool
             const double lm = pm[it] == -CUDART_INF_F ? -CUDART_INF : (double)pm[it] + (double)(logf(tot[it]) - log2M);
             lv1[(4u * q) >> pool_sh] = lm;
             if constexpr (AIR) a.logW[((uint64_t)base >> b) + ((4u * q) >> b)] = lm;
         }
     }
-    if (Z <= 32u) __syncwarp();  // a pair's CDF was written by this warp
-    else __syncthreads();
+    if (Z > 32u) __syncthreads();  // the CDF of a multi-warp pool is in shared memory
     if constexpr (MODE != kPass1Weigh) {  // all QPT x 4 branch-free binary searches advance together
+        // a(i) = #{k < 2M-1 : C_k <= t}, t = u C_{2M-1}; C is the pool's fp32 CDF (excl + run)
         uint32_t lo[QPT][4];
-        float tq[QPT][4];
+        if (Z <= 32u) {
+            // the pool is a segment of Z lanes, lane j holding C_{4j..4j+3} in registers:
+            // search the Z-1 quad ends (C_{4j+3}, j < Z-1) by shuffles, then count the
+            // quad's first three entries -- no shared memory, no bank conflicts
+            const uint32_t seg0 = lane & ~(Z - 1u);
 #pragma unroll
-        for (int it = 0; it < QPT; ++it) {
-            const uint32_t q = tid + it * threads;
-            const bool valid = q < nq;
-            const uint4 blk = AIR ? rng_block(a.key, c0t + q, a.n, kDomainWithin, 0u)
-                                  : rng_block(a.key, c0t + q, a.n, kDomainResample, 1u);
-            const uint32_t pb = valid ? (((4u * q) >> pool_sh) << pool_sh) : 0u;
-            const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
-            // the search target scales the pool total AS STORED in the CDF (same summation
-            // order as the entries it is compared with), so t <= C_{2M-1} and a zero-weight
-            // last entry can never be selected (reading R3)
-            const float totc = valid ? w[pb + 4u * Z - 1u] : 0.0f;
+            for (int it = 0; it < QPT; ++it) {
+                const uint32_t q = tid + it * threads;
+                const bool valid = q < nq;
+                const uint4 blk = AIR ? rng_block(a.key, c0t + q, a.n, kDomainWithin, 0u)
+                                      : rng_block(a.key, c0t + q, a.n, kDomainResample, 1u);
+                const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
+                const float c0 = excl[it] + run[it][0], c1 = excl[it] + run[it][1], c2 = excl[it] + run[it][2],
+                            c3 = excl[it] + run[it][3];
+                // the target scales the pool total AS STORED in the CDF (same summation order
+                // as the entries it is compared with): t <= C_{2M-1}, so a zero-weight last
+                // entry is never selected (reading R3)
+                const float totc = __shfl_sync(kFull, c3, seg0 + Z - 1u);
+                float t[4];
+                uint32_t jq[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                lo[it][e] = pb;
-                tq[it][e] = valid ? u01f(r[e]) * totc : -1.0f;
+                for (int e = 0; e < 4; ++e) {
+                    t[e] = valid ? u01f(r[e]) * totc : -1.0f;
+                    jq[e] = 0u;
+                }
+                for (uint32_t step = Z >> 1; step >= 1u; step >>= 1)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (__shfl_sync(kFull, c3, seg0 + jq[e] + step - 1u) <= t[e]) jq[e] += step;
+                const uint32_t pb = valid ? (((4u * q) >> pool_sh) << pool_sh) : 0u;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t src = seg0 + jq[e];
+                    const float v0 = __shfl_sync(kFull, c0, src), v1 = __shfl_sync(kFull, c1, src),
+                                v2 = __shfl_sync(kFull, c2, src);
+                    lo[it][e] = pb + 4u * jq[e] + (uint32_t)(v0 <= t[e]) + (uint32_t)(v1 <= t[e]) + (uint32_t)(v2 <= t[e]);
+                }
             }
-        }
-        for (uint32_t step = 2u * Z; step >= 1u; step >>= 1) {
+        } else {
+            float tq[QPT][4];
 #pragma unroll
-            for (int it = 0; it < QPT; ++it)
+            for (int it = 0; it < QPT; ++it) {
+                const uint32_t q = tid + it * threads;
+                const bool valid = q < nq;
+                const uint4 blk = AIR ? rng_block(a.key, c0t + q, a.n, kDomainWithin, 0u)
+                                      : rng_block(a.key, c0t + q, a.n, kDomainResample, 1u);
+                const uint32_t pb = valid ? (((4u * q) >> pool_sh) << pool_sh) : 0u;
+                const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
+                const float totc = valid ? w[pb + 4u * Z - 1u] : 0.0f;  // as above (R3)
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (w[lo[it][e] + step - 1u] <= tq[it][e]) lo[it][e] += step;
+                for (int e = 0; e < 4; ++e) {
+                    lo[it][e] = pb;
+                    tq[it][e] = valid ? u01f(r[e]) * totc : -1.0f;
+                }
+            }
+            for (uint32_t step = 2u * Z; step >= 1u; step >>= 1) {
+#pragma unroll
+                for (int it = 0; it < QPT; ++it)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (w[lo[it][e] + step - 1u] <= tq[it][e]) lo[it][e] += step;
+            }
         }
 #pragma unroll
         for (int it = 0; it < QPT; ++it) {

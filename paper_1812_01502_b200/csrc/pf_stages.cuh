@@ -24,34 +24,9 @@
 #pragma once
 #include <cstdint>
 
-#include "pf_kernels.cuh"
+#include "pf_args.h"
 
 namespace pfk {
-
-struct StageArgs {
-    Key key;
-    uint32_t n;
-    uint64_t N;     // particles of this shard
-    uint32_t pos0;  // global index of the shard's first particle (RNG counters)
-    uint32_t m, M, b, s0, k, P, lowbits;
-    uint32_t pipe;        // 1: software-pipelined (two buffers of everything); 0: one buffer
-    uint32_t out_rot;     // stage rotation (R23): outputs go to group rotr_S(g, out_rot)
-    uint32_t out_S;       //   of the next layout (0: no move; needs M >= 4)
-    const void* pin;      // states at stage s0-1 (packed AoS, shard-local)
-    void* pout;           // states at stage s0+k-1
-    const uint32_t* thr;  // side thresholds, level-table layout (level_offset)
-    int32_t* dbg_anc;     // per-stage ancestor tables (debug) or nullptr
-};
-
-// Shared memory: two tile-state buffers, two table sets (tile t-1 is walked while tile t
-// is drawn), two threshold copies, two mbarriers; one of each when not pipelined.
-__host__ __device__ inline uint32_t stages_smem(uint32_t P, uint32_t state_bytes, uint32_t k, uint32_t tb,
-                                                uint32_t pipe = 1u) {
-    const uint32_t st = (P * state_bytes + 15u) & ~15u;
-    const uint32_t tab = (k * P * tb + 15u) & ~15u;
-    const uint32_t nb = pipe ? 2u : 1u;
-    return nb * (st + tab + 4u * (1u << k)) + 16u;
-}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -151,21 +126,25 @@ __device__ __forceinline__ void stage_draws(const StageArgs& a, const StageTile&
             for (uint32_t st = 0; st < k; ++st) {
                 const uint32_t s = a.s0 + st, bit = 1u << st;
                 const uint4 blk = rng_block(a.key, c0, a.n, kDomainResample, s);
-                const uint32_t Pt = ths[toff + (j >> (st + 1))];
+                // (r >> b) >= P  <=>  r >= P << b  (P < 2^{32-b}, so P << b is exact): one
+                // shift per block instead of one per draw
+                const uint32_t Pb = ths[toff + (j >> (st + 1))] << b;
                 toff += (1u << k) >> (st + 1);
                 const uint32_t rw[4] = {blk.x, blk.y, blk.z, blk.w};
-                const uint32_t blo = (j & ~bit) << b, bhi = (j | bit) << b;
+                const uint32_t blo = (j & ~bit) << b, bitb = bit << b;
                 uint32_t en[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const bool hi = (rw[e] >> b) >= Pt;
+                    const bool hi = rw[e] >= Pb;
                     if constexpr (TB == 1) en[e] = (rw[e] & mask) | (hi ? 0x80u : 0u);
-                    else en[e] = (hi ? bhi : blo) | (rw[e] & mask);
+                    else en[e] = ((rw[e] & mask) | blo) | (hi ? bitb : 0u);
                 }
                 if constexpr (TB == 1)
-                    *reinterpret_cast<uint32_t*>(tabs + st * P + l0) = en[0] | (en[1] << 8) | (en[2] << 16) | (en[3] << 24);
+                    *reinterpret_cast<uint32_t*>(tabs + st * P + l0) =
+                        __byte_perm(__byte_perm(en[0], en[1], 0x0040u), __byte_perm(en[2], en[3], 0x0040u), 0x5410u);
                 else
-                    *reinterpret_cast<uint2*>(tabs + 2u * (st * P + l0)) = make_uint2(en[0] | (en[1] << 16), en[2] | (en[3] << 16));
+                    *reinterpret_cast<uint2*>(tabs + 2u * (st * P + l0)) =
+                        make_uint2(__byte_perm(en[0], en[1], 0x5410u), __byte_perm(en[2], en[3], 0x5410u));
                 if constexpr (DBG) {
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
