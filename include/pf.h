@@ -273,6 +273,29 @@ int pf_peer_open(pf_handle* h, const void* ipc_handles, const uint64_t* offsets)
 int pf_peer_set(pf_handle* h, const uint64_t* dev_workspaces);
 int pf_cross_peer(pf_handle* h);
 
+/* Relabelled exchange of cross stage t (1..L), the BPF variant of SURVEY.md §8(f)3 (the
+ * count-imbalance / surplus sketch of PAPER.md:826-850; reading R24).  Every
+ * output first takes its Alg. 3 draw of stage s = S_loc + t (pairing shard r with
+ * r' = r ^ 2^{t-1}); the k-th output of r that drew from r' and the k-th output of r'
+ * that drew from r (both in increasing position) exchange draws for k < min of the two
+ * counts, so each reads its own shard, and only the surplus crosses the pair.  Both
+ * ranks evaluate both shards' counter-based draws, so the lists need no communication;
+ * the output is NOT bitwise the plain exchange's (a permutation within the pair block,
+ * on which V_s is constant: Prop. 1 unbiasedness is kept, pinned by the oracle's
+ * orc_relabel_stage).  Per stage, on every rank of the pair, after pf_step_top:
+ *   pf_relabel_begin(h, t, counts, &send, &n_send, &n_recv)
+ *       counts: HOST uint64[2] = {own outputs drawing from r', r' outputs drawing from r};
+ *       send: DEVICE, n_send states (n_send x d fp32, the handle's workspace, valid until
+ *       the next call) this rank sends to r'; n_recv: states to receive from r'.
+ *       Synchronises once (the counts size the transfer).
+ *   <send n_send states to r', receive n_recv from r' into a DEVICE buffer>
+ *   pf_relabel_end(h, t, recv)   recv: DEVICE, n_recv x d fp32 (NULL if n_recv = 0)
+ * Errors: PF_EINVAL (t out of range, NULL), PF_ESTATE (not sharded, before pf_step_top,
+ * end without begin), PF_ECUDA. */
+int pf_relabel_begin(pf_handle* h, int t, uint64_t* host_counts, const void** dev_send, uint64_t* n_send,
+                     uint64_t* n_recv);
+int pf_relabel_end(pf_handle* h, int t, const void* dev_recv);
+
 /* PF_FLAG_GUARD handles: count the bytes of the inter-region gaps that differ from
  * `fill` (the byte the caller filled the workspace with before pf_init).  A nonzero
  * count means some kernel wrote outside its region.  Synchronises.  Errors: PF_EINVAL,

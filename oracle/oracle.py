@@ -74,6 +74,10 @@ def lib():
         _lib.orc_step_multinomial.argtypes = [vp, u64, u64, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         _lib.orc_step_adaptive.argtypes = [vp, u64, u64, u64, u32, vp, vp, vp, ctypes.c_double, vp, vp, vp, vp,
                                            vp, vp, vp, vp, vp, vp, vp, vp]
+        _lib.orc_relabel_stage.argtypes = [u64, u64, ctypes.c_int, vp, vp]
+        _lib.orc_augmented_resample_relabel.argtypes = [u64, u64, u64, u64, u32, vp, vp, vp, vp, vp, vp]
+        _lib.orc_step_relabel.argtypes = [vp, u64, u64, u64, u64, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                          vp, vp]
         _lib.orc_step_adaptive_rot.argtypes = [vp, u64, u64, u64, u32, vp, vp, vp, ctypes.c_double, ctypes.c_int,
                                                vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     return _lib
@@ -484,6 +488,68 @@ def run_filter_multinomial(params: dict, N: int, seed: int, ys: np.ndarray, x0: 
     means = np.zeros((len(ys), d))
     for n, y in enumerate(ys):
         r = step_multinomial(params, N, seed, n, y, x)
+        means[n] = r["filter"][:d]
+        x = r["xhat"].astype(np.float32)
+    return means
+
+
+# ----------------------------------------------------------------------------- relabelled exchange
+def relabel_stage(table: np.ndarray, G: int, t: int):
+    """orc_relabel_stage on one cross stage's table (output -> source), returning
+    (relabelled table, excess[G])."""
+    a = np.ascontiguousarray(table, dtype=np.int32).copy()
+    ex = np.zeros(G, np.uint64)
+    rc = lib().orc_relabel_stage(a.size, G, int(t), _ptr(a), _ptr(ex))
+    if rc != 0:
+        raise ValueError(f"orc_relabel_stage rc={rc}")
+    return a, ex.astype(np.int64)
+
+
+def augmented_resample_relabel(lw: np.ndarray, M: int, G: int, seed: int, n: int) -> dict:
+    lw = np.ascontiguousarray(lw, dtype=np.float64)
+    N = lw.shape[0]
+    m = N // M
+    S, L = int(round(np.log2(m))), int(round(np.log2(G)))
+    out = dict(a=np.zeros((S, N), np.int32), delta=np.zeros((S, N), np.float32), logV=np.zeros(m - 1),
+               A=np.zeros(N, np.int64), excess=np.zeros((L, G), np.uint64))
+    rc = lib().orc_augmented_resample_relabel(N, M, G, seed, n, _ptr(lw), _ptr(out["a"]), _ptr(out["delta"]),
+                                              _ptr(out["logV"]), _ptr(out["A"]), _ptr(out["excess"]))
+    if rc != 0:
+        raise ValueError(f"orc_augmented_resample_relabel rc={rc}")
+    out["excess"] = out["excess"].astype(np.int64)
+    return out
+
+
+def step_relabel(params: dict, N: int, M: int, G: int, seed: int, n: int, y: np.ndarray, xin: np.ndarray) -> dict:
+    """One step with the relabelled exchange on G shards (orc_step_relabel)."""
+    mdl = make_model(params)
+    d = mdl.d
+    m = N // M
+    S, L = int(round(np.log2(m))), int(round(np.log2(G)))
+    xin = np.ascontiguousarray(xin, dtype=np.float32).reshape(N, d)
+    yy = np.ascontiguousarray(y, dtype=np.float32)
+    out = dict(x=np.zeros((N, d)), lw=np.zeros(N), a=np.zeros((S, N), np.int32), delta=np.zeros((S, N), np.float32),
+               logV=np.zeros(m - 1), A=np.zeros(N, np.int64), xhat=np.zeros((N, d)), filter=np.zeros(2 * d),
+               predict=np.zeros(2 * d), resampled=np.zeros(2 * d), excess=np.zeros((L, G), np.uint64))
+    rc = lib().orc_step_relabel(ctypes.byref(mdl), N, M, G, seed, n, _ptr(yy), _ptr(xin), _ptr(out["x"]),
+                                _ptr(out["lw"]), _ptr(out["a"]), _ptr(out["delta"]), _ptr(out["logV"]), _ptr(out["A"]),
+                                _ptr(out["xhat"]), _ptr(out["filter"]), _ptr(out["predict"]), _ptr(out["resampled"]),
+                                _ptr(out["excess"]))
+    if rc != 0:
+        raise ValueError(f"orc_step_relabel rc={rc}")
+    out["excess"] = out["excess"].astype(np.int64)
+    out["S"], out["m"] = S, m
+    return out
+
+
+def run_filter_relabel(params: dict, M: int, m: int, G: int, seed: int, ys: np.ndarray):
+    """Alg. 1 + Alg. 3 with the relabelled exchange on G shards; per-step filter means."""
+    N = M * m
+    d = int(params["d"])
+    x = init(params, N, seed).astype(np.float32)
+    means = np.zeros((len(ys), d))
+    for n, y in enumerate(ys):
+        r = step_relabel(params, N, M, G, seed, n, y, x)
         means[n] = r["filter"][:d]
         x = r["xhat"].astype(np.float32)
     return means

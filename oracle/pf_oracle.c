@@ -1089,3 +1089,117 @@ int orc_step_multinomial_sampled(const orc_model* mdl, uint64_t N, uint64_t seed
     free(lw); free(C);
     return ORC_OK;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Relabelled exchange across G shards ("keeps resampled particles on
+ * the GPU holding their ancestor, ships only the per-GPU count imbalance"; the disabled
+ * surplus sketch of PAPER.md:826-850: "the PEs with more resampled particles send the
+ * surplus particles to the paired PE with fewer than M resampled particles";
+ * DESIGN.md reading R24).
+ *
+ * The N particles form G = 2^L equal shards, shard r = positions [r N/G, (r+1) N/G).
+ * Stage s = S - L + t (t = 1..L) pairs every group of shard r with the same local group
+ * of shard r' = r ^ 2^{t-1}.  At such a stage every output first takes its Alg. 3 draw
+ * (stage_s_draw).  With A_r the outputs of r whose draw lies in r' and A_r' the outputs
+ * of r' whose draw lies in r, both in increasing position, the k-th outputs of the two
+ * lists exchange their draws for k < min(|A_r|, |A_r'|): each then reads a particle of
+ * its own shard, and only the |A_r| - |A_r'| unmatched outputs of the longer list read
+ * across the pair.  The exchange permutes outputs inside a block on which V_s is
+ * constant (Lemma facts_about_Vs), so the V-weighted sample after the stage -- and with
+ * it the unbiasedness of Prop. 1, eq. aug_res_lack_of_bias -- is that
+ * of Alg. 3 (pinned in rationals by enumeration, tests/test_oracle_relabel.py).
+ *
+ * orc_relabel_stage applies the exchange to one cross stage's table `as` (N entries:
+ * output position -> source position at stage s-1) in place; excess[r] = the number of
+ * outputs of shard r that still read across the pair (unmatched). */
+int orc_relabel_stage(uint64_t N, uint64_t G, int t, int32_t* as, uint64_t* excess)
+{
+    int L = ilog2_exact(G);
+    if (L < 1 || t < 1 || t > L || N % G != 0) return ORC_EINVAL;
+    uint64_t nl = N / G;
+    uint64_t half = 1ull << (t - 1);
+    uint64_t* lr = (uint64_t*)malloc(sizeof(uint64_t) * nl);
+    uint64_t* lp = (uint64_t*)malloc(sizeof(uint64_t) * nl);
+    if (!lr || !lp) {
+        free(lr); free(lp);
+        return ORC_ENOMEM;
+    }
+    for (uint64_t r = 0; r < G; ++r) {
+        if (r & half) continue; /* visit each pair once, from its lower shard */
+        uint64_t rp = r | half;
+        uint64_t nr = 0, np = 0;
+        for (uint64_t i = r * nl; i < (r + 1) * nl; ++i)
+            if ((uint64_t)as[i] / nl == rp) lr[nr++] = i;
+        for (uint64_t i = rp * nl; i < (rp + 1) * nl; ++i)
+            if ((uint64_t)as[i] / nl == r) lp[np++] = i;
+        uint64_t k0 = nr < np ? nr : np;
+        for (uint64_t k = 0; k < k0; ++k) {
+            int32_t tmp = as[lr[k]];
+            as[lr[k]] = as[lp[k]];
+            as[lp[k]] = tmp;
+        }
+        if (excess) {
+            excess[r] = nr - k0;
+            excess[rp] = np - k0;
+        }
+    }
+    free(lr); free(lp);
+    return ORC_OK;
+}
+
+/* Alg. 3 on log-weights lw with the last L = log2 G stages relabelled (orc_relabel_stage):
+ * tables a (S x N, relabelled), delta (the Alg. 3 draws' boundary distances), logV, the
+ * composed ancestors A, and excess (L x G). */
+int orc_augmented_resample_relabel(uint64_t N, uint64_t M, uint64_t G, uint64_t seed, uint32_t n, const double* lw,
+                                   int32_t* a, float* delta, double* logV, int64_t* A, uint64_t* excess)
+{
+    uint64_t m = (M == 0) ? 0 : N / M;
+    int S = ilog2_exact(m), L = ilog2_exact(G);
+    if (S < 1 || L < 1 || (m / G) < 2 || m % G != 0) return ORC_EINVAL;
+    int32_t* as = (int32_t*)malloc(sizeof(int32_t) * N * (uint64_t)S);
+    if (!as) return ORC_ENOMEM;
+    int rc = augmented_resample_upto(N, M, seed, n, lw, S, as, delta, logV, NULL);
+    for (int t = 1; t <= L && rc == ORC_OK; ++t)
+        rc = orc_relabel_stage(N, G, t, as + (uint64_t)(S - L + t - 1) * N, excess ? excess + (uint64_t)(t - 1) * G : NULL);
+    if (rc == ORC_OK) {
+        if (A)
+            for (uint64_t i = 0; i < N; ++i) {
+                uint64_t j = i;
+                for (int s = S; s >= 1; --s) j = (uint64_t)as[(uint64_t)(s - 1) * N + j];
+                A[i] = (int64_t)j;
+            }
+        if (a) memcpy(a, as, sizeof(int32_t) * N * (uint64_t)S);
+    }
+    free(as);
+    return rc;
+}
+
+/* One step of Alg. 1 deploying Alg. 3 with the relabelled exchange on G shards (same
+ * outputs as orc_step, plus excess). */
+int orc_step_relabel(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t G, uint64_t seed, uint32_t n,
+                     const float* y, const float* xin, double* x, double* lw, int32_t* a, float* delta,
+                     double* logV, int64_t* A, double* xhat_out, double* filt, double* pred, double* resamp,
+                     uint64_t* excess)
+{
+    int d = mdl->d;
+    double* xprev = (double*)malloc(sizeof(double) * N * (uint64_t)d);
+    int64_t* Aloc = (int64_t*)malloc(sizeof(int64_t) * N);
+    if (!xprev || !Aloc) {
+        free(xprev); free(Aloc);
+        return ORC_ENOMEM;
+    }
+    for (uint64_t i = 0; i < N * (uint64_t)d; ++i) xprev[i] = (double)xin[i];
+    if (n == 0) memcpy(x, xprev, sizeof(double) * N * (uint64_t)d);
+    else orc_mutate(mdl, N, seed, n, xprev, x);
+    orc_logweight(mdl, N, y, x, lw);
+    int rc = orc_augmented_resample_relabel(N, M, G, seed, n, lw, a, delta, logV, Aloc, excess);
+    if (rc == ORC_OK) {
+        if (A) memcpy(A, Aloc, sizeof(int64_t) * N);
+        if (xhat_out)
+            for (uint64_t i = 0; i < N; ++i)
+                for (int k = 0; k < d; ++k) xhat_out[i * d + k] = x[(uint64_t)Aloc[i] * d + k];
+        orc_estimates(d, N, lw, x, Aloc, filt, pred, resamp);
+    }
+    free(xprev); free(Aloc);
+    return rc;
+}

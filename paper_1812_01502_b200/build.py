@@ -32,6 +32,16 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+# experiment builds (tools/build_variant.sh): PF_BUILD_VARIANT=name PF_BUILD_DEFINES="-DX=1 ..."
+# build libpf_<name>.so from build_obj_<name>/ (loaded with PF_LIB=...); the product build
+# is the default one
+VARIANT = os.environ.get("PF_BUILD_VARIANT", "")
+if VARIANT:
+    OBJ = os.path.join(HERE, "build_obj_" + VARIANT)
+    LIB = os.path.join(HERE, f"libpf_{VARIANT}.so")
+    NVCC_FLAGS = NVCC_FLAGS + os.environ.get("PF_BUILD_DEFINES", "").split()
+
+
 def _obj(src: str) -> str:
     return os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
 

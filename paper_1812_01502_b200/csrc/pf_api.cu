@@ -208,6 +208,7 @@ struct Layout {
     size_t pull_src, pull_rank, pull_counts, pull_fill, pull_off, pull_req, pull_outpos, pull_serve;  // world > 1
     size_t dbg_x, dbg_lw, dbg_anc, dbg_A;
     size_t mom_part, mom_out;          // PF_EST_RESAMPLED (k_moments)
+    size_t rl_cnt, rl_off, rl_own, rl_par, rl_send;  // relabelled exchange (world > 1)
     size_t guard_count;                // PF_FLAG_GUARD
     std::vector<size_t> gaps;          // PF_FLAG_GUARD: offsets of the PF_GUARD_BYTES gaps
     size_t total;
@@ -277,6 +278,14 @@ Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags, uint32
     L.dbg_anc = take(dbg ? (size_t)N * Sglobal * 4 : 0);
     (void)S;
     L.dbg_A = take(dbg ? N * 4 : 0);
+    {
+        const size_t nch = (N + kRlChunk - 1) / kRlChunk;
+        L.rl_cnt = take(sh ? 2 * nch * 4 : 0);
+        L.rl_off = take(sh ? (2 * nch + 2) * 4 : 0);
+        L.rl_own = take(sh ? N * 4 : 0);
+        L.rl_par = take(sh ? N * 4 : 0);
+        L.rl_send = take(sh ? xb : 0);
+    }
     L.mom_part = take((size_t)kMomPartDoubles * 8);
     L.mom_out = take(16 * 8);
     L.guard_count = take(guard ? 16 : 0);
@@ -324,6 +333,9 @@ struct pf_handle {
     // peer-memory exchange (pf_peer_open / pf_peer_set / pf_cross_peer)
     std::vector<unsigned char*> peer_ws;    // every rank's workspace, mapped here
     std::vector<void*> peer_ipc;            // IPC mappings to close (allocation bases)
+    // relabelled exchange in progress (pf_relabel_begin -> pf_relabel_end)
+    int rl_t = 0;
+    uint64_t rl_own = 0, rl_kmin = 0;
     // kernel timing
     bool timing;
     struct Rec {
@@ -1200,6 +1212,80 @@ int pf_cross_peer(pf_handle* h) {
     h->mark(PF_KERNEL_CROSS, false);
     h->cur ^= 1;
     return check_cuda(h, "pf_cross_peer");
+}
+
+// ---- relabelled exchange of the cross stages (include/pf.h; reading R24) ----
+static RelabelArgs relabel_args(pf_handle* h, int t) {
+    RelabelArgs a;
+    a.key = make_key(h->seed);
+    a.n = h->step_n;
+    a.s = h->S + (uint32_t)t;
+    a.b = h->b;
+    a.M = h->M;
+    a.Nloc = h->N;
+    a.rank = h->rank;
+    a.partner = h->rank ^ (1u << (t - 1));
+    a.own_is_low = ((h->rank >> (t - 1)) & 1u) == 0u ? 1u : 0u;
+    a.thr = h->at<uint32_t>(h->lay.top_thr) + (h->world - (h->world >> (t - 1))) + (h->rank >> t);
+    a.nchunks = (uint32_t)((h->N + kRlChunk - 1) / kRlChunk);
+    a.cnt = h->at<uint32_t>(h->lay.rl_cnt);
+    a.off = h->at<uint32_t>(h->lay.rl_off);
+    a.own = h->at<uint32_t>(h->lay.rl_own);
+    a.par = h->at<uint32_t>(h->lay.rl_par);
+    a.x = h->X(h->cur);
+    a.out = h->X(h->cur ^ 1);
+    a.send = h->at<float>(h->lay.rl_send);
+    a.recv = nullptr;
+    a.kmin = 0;
+    a.nsend = 0;
+    a.dbg_anc = (h->flags & PF_FLAG_DEBUG) ? h->at<int32_t>(h->lay.dbg_anc) + (size_t)(a.s - 1) * h->N : nullptr;
+    return a;
+}
+
+int pf_relabel_begin(pf_handle* h, int t, uint64_t* host_counts, const void** dev_send, uint64_t* n_send,
+                     uint64_t* n_recv) {
+    if (!h || !host_counts || !dev_send || !n_send || !n_recv) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
+    if (t < 1 || (uint32_t)t > h->L) return fail(h, PF_EINVAL, "cross stage out of range");
+    if (!h->top_done) return fail(h, PF_ESTATE, "pf_step_top must run first");
+    RelabelArgs a = relabel_args(h, t);
+    h->mark(PF_KERNEL_CROSS, true);
+    launch_relabel_plan(h->stream, a);
+    uint32_t tot[2] = {0u, 0u};
+    cudaError_t e = cudaMemcpyAsync(tot, a.off + 2ull * a.nchunks, sizeof(tot), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_relabel_begin: ") + cudaGetErrorString(e));
+    launch_relabel_lists(h->stream, a);
+    const uint64_t no = tot[0], np = tot[1], kmin = no < np ? no : np;
+    a.kmin = kmin;
+    a.nsend = np - kmin;  // the partner's surplus outputs read these states of this shard
+    launch_relabel_move(h->stream, (int)h->plan.D, a, true, 0, false);
+    h->mark(PF_KERNEL_CROSS, false);
+    h->rl_t = t;
+    h->rl_own = no;
+    h->rl_kmin = kmin;
+    host_counts[0] = no;
+    host_counts[1] = np;
+    *dev_send = a.send;
+    *n_send = np - kmin;
+    *n_recv = no - kmin;
+    return check_cuda(h, "pf_relabel_begin");
+}
+
+int pf_relabel_end(pf_handle* h, int t, const void* dev_recv) {
+    if (!h) return fail(h, PF_EINVAL, "NULL handle");
+    if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
+    if (t != h->rl_t) return fail(h, PF_ESTATE, "pf_relabel_begin(t) must run first");
+    if (!dev_recv && h->rl_own > h->rl_kmin) return fail(h, PF_EINVAL, "NULL receive buffer");
+    RelabelArgs a = relabel_args(h, t);
+    a.kmin = h->rl_kmin;
+    a.recv = dev_recv;
+    h->mark(PF_KERNEL_CROSS, true);
+    launch_relabel_move(h->stream, (int)h->plan.D, a, false, h->rl_own, (h->flags & PF_FLAG_DEBUG) != 0);
+    h->mark(PF_KERNEL_CROSS, false);
+    h->cur ^= 1;
+    h->rl_t = 0;
+    return check_cuda(h, "pf_relabel_end");
 }
 
 int pf_guard_check(pf_handle* h, unsigned char fill, uint64_t* bad_bytes) {

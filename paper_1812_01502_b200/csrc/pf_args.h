@@ -237,6 +237,33 @@ struct PullArgs {
     int32_t* dbg_anc;         // stage tables (debug) or nullptr
 };
 
+// Relabelled exchange of one cross stage (pf_relabel_begin / pf_relabel_end; DESIGN.md
+// reading R24).  Shard r pairs with r' = r ^ 2^{t-1} at stage s = S_loc + t;
+// both ranks evaluate both shards' counter-based draws, so each knows the two ordered lists
+//   own  = this shard's outputs whose draw lies in r'      (positions, increasing)
+//   par  = r''s outputs whose draw lies in r               (their sources in r, in order)
+// without communication; the k-th entries of the lists swap draws for k < min, and only the
+// surplus crosses the pair.
+constexpr uint32_t kRlChunk = 2048;   // positions per counting chunk (512 quads, one CTA)
+struct RelabelArgs {
+    Key key;
+    uint32_t n, s, b, M;
+    uint64_t Nloc;
+    uint32_t rank, partner, own_is_low;
+    const uint32_t* thr;         // the stage's side threshold (top_thr entry of block rank >> t)
+    uint32_t nchunks;
+    uint32_t* cnt;               // 2 x nchunks: per chunk {own wanting r', r' wanting own}
+    uint32_t* off;               // 2 x nchunks + 2: exclusive offsets, then the totals
+    uint32_t* own;               // Nloc: list own
+    uint32_t* par;               // Nloc: list par (local source index in this shard)
+    const void* x;               // stage s-1 states of this shard (Nloc x d)
+    void* out;                   // stage s states
+    void* send;                  // packed surplus this rank sends (par[k], k >= kmin)
+    const void* recv;            // surplus received (own[k], k >= kmin)
+    uint64_t kmin, nsend;
+    int32_t* dbg_anc;            // this stage's table (global source positions) or nullptr
+};
+
 // Peer-memory exchange (pf_cross_peer): every rank's stage-S_loc state buffer, mapped into
 // this process (CUDA IPC over NVLink, or local pointers for shards on one GPU).
 constexpr uint32_t kPeerMaxG = 64;

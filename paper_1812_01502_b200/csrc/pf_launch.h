@@ -58,6 +58,10 @@ void launch_cross(int payload, bool dbg, const LaunchCfg& c, const CrossArgs& a)
 constexpr uint32_t kMomPartDoubles = 592u * 2u * 8u;  // k_moments CTA partials (grid x 2 D, D <= 8)
 void launch_moments(cudaStream_t st, int D, const float* x, const int32_t* isl, uint32_t b, uint64_t N, double* part,
                     double* out);
+void launch_relabel_plan(cudaStream_t st, const RelabelArgs& a);
+void launch_relabel_lists(cudaStream_t st, const RelabelArgs& a);
+// pack = true: the surplus this rank sends; false: assemble the stage's outputs (nown = |own|)
+void launch_relabel_move(cudaStream_t st, int D, const RelabelArgs& a, bool pack, uint64_t nown, bool dbg);
 void launch_debug_compose(const LaunchCfg& c, const int32_t* anc, uint64_t N, uint32_t S, int32_t* A);
 
 }  // namespace pfk

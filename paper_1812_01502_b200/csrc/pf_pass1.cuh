@@ -4,8 +4,7 @@
 //   load xhat_{n-1} (coalesced) -> mutate (Alg. 1 l.303) -> log g_n
 //    -> stage 1 over the pairs (2p, 2p+1) (Alg. 3 l.346-349): pair max,
 //   weights c = exp(lw - max), warp-shuffle segmented inclusive scan, branch-free binary
-//   searches of the inverse CDF (pools of <= 32 quads: over the CDF held in the lanes'
-//   registers, by shuffles; wider pools: in shared memory) -> V level 1 per pair; then every warp redundantly builds
+//   searches of the inverse CDF -> V level 1 per pair; then every warp redundantly builds
 //   the tile's V levels 2..k1 and side thresholds in its lanes (log-domain pair means,
 //   eq. V_defn_proofs) -> draws of stages 2..k1 into per-stage tables ->
 //   each output walks its ancestry back through the tables and writes its state, already
@@ -63,8 +62,17 @@ __device__ __forceinline__ uint32_t xs_swz(uint32_t s) {
     else return s;
 }
 
+// experiment knobs (tools/build_variant.sh): the register budget of the fused mode and the
+// largest state block kept in registers for the estimate
+#ifndef PF_P1_MINB
+#define PF_P1_MINB 1
+#endif
+#ifndef PF_KEEPX_MAX
+#define PF_KEEPX_MAX 32
+#endif
+
 template <int D, int KIND, bool DBG, int QPT, int TB, int MODE = kPass1Fused>
-__global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : 1) k_pass1(const __grid_constant__ Pass1Args a) {
+__global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : PF_P1_MINB) k_pass1(const __grid_constant__ Pass1Args a) {
     constexpr int PS = 2 + 4 * D;  // partial: max, sw, s1[D], s2[D], p1[D], p2[D]
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t threads = blockDim.x;
@@ -118,7 +126,7 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : 1) 
 
     // ---- 2. mutate, weight ---------------------------------------------------------------
     float lw[QPT][4];
-    constexpr bool KEEPX = 4 * D * QPT <= 32;  // states stay in registers for the estimate
+    constexpr bool KEEPX = 4 * D * QPT <= PF_KEEPX_MAX;  // states stay in registers for the estimate
     float xr[KEEPX ? QPT : 1][KEEPX ? 4 * D : 1];
 #pragma unroll
     for (int it = 0; it < QPT; ++it) {
@@ -305,81 +313,43 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : 1) 
     for (int it = 0; it < QPT; ++it) {
         const uint32_t q = tid + it * threads;
         if (q >= nq) continue;
-        if (Z > 32u)  // pools wider than a warp are searched in shared memory
-            reinterpret_cast<float4*>(w)[q] =
-                make_float4(excl[it] + run[it][0], excl[it] + run[it][1], excl[it] + run[it][2], excl[it] + run[it][3]);
+        reinterpret_cast<float4*>(w)[q] =
+            make_float4(excl[it] + run[it][0], excl[it] + run[it][1], excl[it] + run[it][2], excl[it] + run[it][3]);
         if (((4u * q) & ((1u << pool_sh) - 1u)) == 0u) {  // first quad of its pool: log mean of the pool
             const double lm = pm[it] == -CUDART_INF_F ? -CUDART_INF : (double)pm[it] + (double)(logf(tot[it]) - log2M);
             lv1[(4u * q) >> pool_sh] = lm;
             if constexpr (AIR) a.logW[((uint64_t)base >> b) + ((4u * q) >> b)] = lm;
         }
     }
-    if (Z > 32u) __syncthreads();  // the CDF of a multi-warp pool is in shared memory
+    if (Z <= 32u) __syncwarp();  // a pair's CDF was written by this warp
+    else __syncthreads();
     if constexpr (MODE != kPass1Weigh) {  // all QPT x 4 branch-free binary searches advance together
-        // a(i) = #{k < 2M-1 : C_k <= t}, t = u C_{2M-1}; C is the pool's fp32 CDF (excl + run)
         uint32_t lo[QPT][4];
-        if (Z <= 32u) {
-            // the pool is a segment of Z lanes, lane j holding C_{4j..4j+3} in registers:
-            // search the Z-1 quad ends (C_{4j+3}, j < Z-1) by shuffles, then count the
-            // quad's first three entries -- no shared memory, no bank conflicts
-            const uint32_t seg0 = lane & ~(Z - 1u);
+        float tq[QPT][4];
 #pragma unroll
-            for (int it = 0; it < QPT; ++it) {
-                const uint32_t q = tid + it * threads;
-                const bool valid = q < nq;
-                const uint4 blk = AIR ? rng_block(a.key, c0t + q, a.n, kDomainWithin, 0u)
-                                      : rng_block(a.key, c0t + q, a.n, kDomainResample, 1u);
-                const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
-                const float c0 = excl[it] + run[it][0], c1 = excl[it] + run[it][1], c2 = excl[it] + run[it][2],
-                            c3 = excl[it] + run[it][3];
-                // the target scales the pool total AS STORED in the CDF (same summation order
-                // as the entries it is compared with): t <= C_{2M-1}, so a zero-weight last
-                // entry is never selected (reading R3)
-                const float totc = __shfl_sync(kFull, c3, seg0 + Z - 1u);
-                float t[4];
-                uint32_t jq[4];
+        for (int it = 0; it < QPT; ++it) {
+            const uint32_t q = tid + it * threads;
+            const bool valid = q < nq;
+            const uint4 blk = AIR ? rng_block(a.key, c0t + q, a.n, kDomainWithin, 0u)
+                                  : rng_block(a.key, c0t + q, a.n, kDomainResample, 1u);
+            const uint32_t pb = valid ? (((4u * q) >> pool_sh) << pool_sh) : 0u;
+            const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
+            // the search target scales the pool total AS STORED in the CDF (same summation
+            // order as the entries it is compared with), so t <= C_{2M-1} and a zero-weight
+            // last entry can never be selected (reading R3)
+            const float totc = valid ? w[pb + 4u * Z - 1u] : 0.0f;
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    t[e] = valid ? u01f(r[e]) * totc : -1.0f;
-                    jq[e] = 0u;
-                }
-                for (uint32_t step = Z >> 1; step >= 1u; step >>= 1)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        if (__shfl_sync(kFull, c3, seg0 + jq[e] + step - 1u) <= t[e]) jq[e] += step;
-                const uint32_t pb = valid ? (((4u * q) >> pool_sh) << pool_sh) : 0u;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const uint32_t src = seg0 + jq[e];
-                    const float v0 = __shfl_sync(kFull, c0, src), v1 = __shfl_sync(kFull, c1, src),
-                                v2 = __shfl_sync(kFull, c2, src);
-                    lo[it][e] = pb + 4u * jq[e] + (uint32_t)(v0 <= t[e]) + (uint32_t)(v1 <= t[e]) + (uint32_t)(v2 <= t[e]);
-                }
+            for (int e = 0; e < 4; ++e) {
+                lo[it][e] = pb;
+                tq[it][e] = valid ? u01f(r[e]) * totc : -1.0f;
             }
-        } else {
-            float tq[QPT][4];
+        }
+        for (uint32_t step = 2u * Z; step >= 1u; step >>= 1) {
 #pragma unroll
-            for (int it = 0; it < QPT; ++it) {
-                const uint32_t q = tid + it * threads;
-                const bool valid = q < nq;
-                const uint4 blk = AIR ? rng_block(a.key, c0t + q, a.n, kDomainWithin, 0u)
-                                      : rng_block(a.key, c0t + q, a.n, kDomainResample, 1u);
-                const uint32_t pb = valid ? (((4u * q) >> pool_sh) << pool_sh) : 0u;
-                const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
-                const float totc = valid ? w[pb + 4u * Z - 1u] : 0.0f;  // as above (R3)
+            for (int it = 0; it < QPT; ++it)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    lo[it][e] = pb;
-                    tq[it][e] = valid ? u01f(r[e]) * totc : -1.0f;
-                }
-            }
-            for (uint32_t step = 2u * Z; step >= 1u; step >>= 1) {
-#pragma unroll
-                for (int it = 0; it < QPT; ++it)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        if (w[lo[it][e] + step - 1u] <= tq[it][e]) lo[it][e] += step;
-            }
+                for (int e = 0; e < 4; ++e)
+                    if (w[lo[it][e] + step - 1u] <= tq[it][e]) lo[it][e] += step;
         }
 #pragma unroll
         for (int it = 0; it < QPT; ++it) {

@@ -126,25 +126,21 @@ __device__ __forceinline__ void stage_draws(const StageArgs& a, const StageTile&
             for (uint32_t st = 0; st < k; ++st) {
                 const uint32_t s = a.s0 + st, bit = 1u << st;
                 const uint4 blk = rng_block(a.key, c0, a.n, kDomainResample, s);
-                // (r >> b) >= P  <=>  r >= P << b  (P < 2^{32-b}, so P << b is exact): one
-                // shift per block instead of one per draw
-                const uint32_t Pb = ths[toff + (j >> (st + 1))] << b;
+                const uint32_t Pt = ths[toff + (j >> (st + 1))];
                 toff += (1u << k) >> (st + 1);
                 const uint32_t rw[4] = {blk.x, blk.y, blk.z, blk.w};
-                const uint32_t blo = (j & ~bit) << b, bitb = bit << b;
+                const uint32_t blo = (j & ~bit) << b, bhi = (j | bit) << b;
                 uint32_t en[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const bool hi = rw[e] >= Pb;
+                    const bool hi = (rw[e] >> b) >= Pt;
                     if constexpr (TB == 1) en[e] = (rw[e] & mask) | (hi ? 0x80u : 0u);
-                    else en[e] = ((rw[e] & mask) | blo) | (hi ? bitb : 0u);
+                    else en[e] = (hi ? bhi : blo) | (rw[e] & mask);
                 }
                 if constexpr (TB == 1)
-                    *reinterpret_cast<uint32_t*>(tabs + st * P + l0) =
-                        __byte_perm(__byte_perm(en[0], en[1], 0x0040u), __byte_perm(en[2], en[3], 0x0040u), 0x5410u);
+                    *reinterpret_cast<uint32_t*>(tabs + st * P + l0) = en[0] | (en[1] << 8) | (en[2] << 16) | (en[3] << 24);
                 else
-                    *reinterpret_cast<uint2*>(tabs + 2u * (st * P + l0)) =
-                        make_uint2(__byte_perm(en[0], en[1], 0x5410u), __byte_perm(en[2], en[3], 0x5410u));
+                    *reinterpret_cast<uint2*>(tabs + 2u * (st * P + l0)) = make_uint2(en[0] | (en[1] << 16), en[2] | (en[3] << 16));
                 if constexpr (DBG) {
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {

@@ -87,6 +87,30 @@ class TorchTransport:
         return recv
 
 
+    def sendrecv(self, send, n_recv: int, peer: int):
+        """Variable-size exchange with one peer: send the 1-D tensor `send` (may be empty),
+        receive n_recv elements of its dtype (NCCL over NVLink on GPUs, gloo on CPU)."""
+        import torch
+        recv = torch.empty(int(n_recv), dtype=send.dtype, device=send.device)
+        ops = []
+        if self.nccl:
+            if send.numel():
+                ops.append(self.dist.P2POp(self.dist.isend, send.contiguous(), peer, group=self.group))
+            if n_recv:
+                ops.append(self.dist.P2POp(self.dist.irecv, recv, peer, group=self.group))
+            if ops:
+                for r in self.dist.batch_isend_irecv(ops):
+                    r.wait()
+        else:
+            reqs = []
+            if send.numel():
+                reqs.append(self.dist.isend(send.contiguous(), peer, group=self.group))
+            if n_recv:
+                reqs.append(self.dist.irecv(recv, peer, group=self.group))
+            for r in reqs:
+                r.wait()
+        return recv
+
     def allgather_object(self, obj):
         out = [None] * self.world
         self.dist.all_gather_object(out, obj, group=self.group)
@@ -223,6 +247,25 @@ class LibBackend:
     def cross_peer(self):
         self.pf._check(self.pf.lib().pf_cross_peer(self.h), self.h)
 
+    # relabelled exchange (include/pf.h pf_relabel_begin / pf_relabel_end)
+    def relabel_begin(self, t: int):
+        """Returns (send: uint8 view of the surplus states this rank sends, n_recv states)."""
+        cnt = np.zeros(2, np.uint64)
+        p = ctypes.c_void_p()
+        ns, nr = np.zeros(1, np.uint64), np.zeros(1, np.uint64)
+        self.pf._check(self.pf.lib().pf_relabel_begin(self.h, int(t), cnt.ctypes.data, ctypes.byref(p), ns.ctypes.data,
+                                                      nr.ctypes.data), self.h)
+        self.last_counts = cnt.astype(np.int64)
+        n_send = int(ns[0])
+        send = self._view(int(p.value), 4 * self.d * n_send, self.torch.uint8) if n_send else \
+            self.torch.empty(0, dtype=self.torch.uint8, device="cuda")
+        return send, int(nr[0])
+
+    def relabel_end(self, t: int, recv):
+        self._keep_r = recv
+        ptr = recv.data_ptr() if recv is not None and recv.numel() else None
+        self.pf._check(self.pf.lib().pf_relabel_end(self.h, int(t), ptr), self.h)
+
     def step_local_dev(self, y_dev):
         self.pf._check(self.pf.lib().pf_step_local(self.h, None, y_dev.data_ptr()), self.h)
         p = ctypes.c_void_p()
@@ -293,6 +336,9 @@ def sharded_step(backend, transport, y, y_dev=None, exchange: str = "pairwise") 
         if exchange == "pull":
             pull_exchange(backend, transport)
             return
+        if exchange == "relabel":
+            relabel_exchange(backend, transport)
+            return
         world = transport.world
         L = world.bit_length() - 1
         for t in range(1, L + 1):
@@ -311,6 +357,19 @@ def _on_stream(backend):
         return contextlib.nullcontext()
     import torch
     return torch.cuda.stream(st)
+
+
+def relabel_exchange(backend, transport) -> None:
+    """The L cross stages as relabelled pairwise rounds (include/pf.h pf_relabel_*; DESIGN.md
+    reading R24): per stage each rank learns, without communication, which of its outputs
+    and of its partner's cross the pair, swaps matched draws, and only the surplus states
+    travel (a variable-size send/recv with the butterfly partner)."""
+    L = transport.world.bit_length() - 1
+    sb = 4 * backend.d
+    for t in range(1, L + 1):
+        send, n_recv = backend.relabel_begin(t)
+        recv = transport.sendrecv(send, n_recv * sb, partner(transport.rank, t))
+        backend.relabel_end(t, recv)
 
 
 def pull_exchange(backend, transport) -> None:
@@ -410,6 +469,24 @@ def loopback_pull(backends: Sequence) -> None:
         b.pull_finish(torch.cat(parts).contiguous())
 
 
+def loopback_relabel(backends: Sequence) -> List[np.ndarray]:
+    """relabel_exchange for G shards on one GPU: every shard's begin (its lists and its
+    surplus sends) runs before any shard's end; the partner's send buffer is the receive
+    buffer.  Returns the per-stage surplus counts (L x G states received)."""
+    G = len(backends)
+    L = G.bit_length() - 1
+    recvd = []
+    for t in range(1, L + 1):
+        sends = [b.relabel_begin(t) for b in backends]
+        for r, b in enumerate(backends):
+            send_p, _ = sends[partner(r, t)]
+            n_recv = sends[r][1]
+            assert send_p.numel() == n_recv * 4 * b.d, "surplus sizes disagree between partners"
+            b.relabel_end(t, send_p.clone() if n_recv else None)
+        recvd.append(np.array([s[1] for s in sends], np.int64))
+    return recvd
+
+
 def loopback_step(backends: Sequence, y, exchange: str = "pairwise") -> None:
     """The same collective sequence for G shards held by one process on one GPU (the
     exchange is a pointer hand-over; every kernel is stream-ordered, none waits on
@@ -424,6 +501,10 @@ def loopback_step(backends: Sequence, y, exchange: str = "pairwise") -> None:
         return
     if exchange == "peer":
         loopback_peer(backends)
+        return
+    if exchange == "relabel":
+        for b, r in zip(backends, zip(*loopback_relabel(backends))):
+            b.surplus = np.array(r)
         return
     world = len(backends)
     L = world.bit_length() - 1

@@ -17,6 +17,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpf.so")
+if os.environ.get("PF_LIB"):  # an experiment build of the same sources (tools/build_variant.sh)
+    LIB_PATH = os.path.join(_HERE, os.path.basename(os.environ["PF_LIB"]))
 
 PF_OK, PF_EINVAL, PF_EWORKSPACE, PF_ECUDA, PF_EOBS, PF_ESTATE = 0, -1, -2, -3, -4, -5
 PF_LG, PF_SV = 1, 2
@@ -99,6 +101,8 @@ def lib() -> ctypes.CDLL:
         L.pf_cross_peer.argtypes = [vp]
         L.pf_guard_check.argtypes = [vp, ctypes.c_ubyte, vp]
         L.pf_run_dev.argtypes = [vp, vp, ctypes.c_uint32, vp]
+        L.pf_relabel_begin.argtypes = [vp, ctypes.c_int, vp, ctypes.POINTER(vp), vp, vp]
+        L.pf_relabel_end.argtypes = [vp, ctypes.c_int, vp]
         _lib = L
     return _lib
 
@@ -110,7 +114,7 @@ EXPORTED = ["pf_workspace_bytes", "pf_init", "pf_step", "pf_step_dev", "pf_estim
             "pf_set_adaptive", "pf_last_stages", "pf_set_airpf", "pf_set_multinomial", "pf_set_rotation",
             "pf_rotation_offset", "pf_cross_pull_plan", "pf_cross_pull_pack", "pf_cross_pull_serve",
             "pf_cross_pull_finish", "pf_peer_export", "pf_peer_open", "pf_peer_set", "pf_cross_peer",
-            "pf_guard_check", "pf_run_dev"]
+            "pf_guard_check", "pf_run_dev", "pf_relabel_begin", "pf_relabel_end"]
 PF_IPC_HANDLE_BYTES = 64
 GUARD_BYTES = 1 << 16  # guard band behind a poisoned workspace (ParticleFilter(poison=...))
 PF_KERNEL_KINDS = 5

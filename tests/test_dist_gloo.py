@@ -67,7 +67,10 @@ class OracleShard:
         return self.r["x"][pos].astype(np.float32)
 
     def step_local(self, y):
-        self.r = self.orc.step(self.params, self.N, self.M, self.seed, self.n, y, self.xhat)
+        if getattr(self, "relabel", False):  # the relabelled exchange's realisation (R24)
+            self.r = self.orc.step_relabel(self.params, self.N, self.M, self.world, self.seed, self.n, y, self.xhat)
+        else:
+            self.r = self.orc.step(self.params, self.N, self.M, self.seed, self.n, y, self.xhat)
         self.stage = self.Sloc
         self.buf = self._states_at(self.Sloc)[self.pos0: self.pos0 + self.nloc].copy()
         if self.peer_dir:
@@ -97,6 +100,39 @@ class OracleShard:
             owner = src // self.nloc
             assert owner in (self.rank, peer), "cross-stage source outside own/partner shard"
             out[l] = self.buf[src - self.pos0] if owner == self.rank else pbuf[src - peer * self.nloc]
+        self.buf = out
+
+    # relabelled exchange (dist.relabel_exchange): only the surplus travels
+    def relabel_begin(self, t):
+        s = self.Sloc + t
+        peer = pfd.partner(self.rank, t)
+        a = self.r["a"][s - 1]
+        mine = np.arange(self.pos0, self.pos0 + self.nloc)
+        theirs = np.arange(peer * self.nloc, (peer + 1) * self.nloc)
+        # partner outputs (increasing position) that read this shard: their states, in order
+        want = [int(a[i]) - self.pos0 for i in theirs if int(a[i]) // self.nloc == self.rank]
+        self._remote = [l for l, i in enumerate(mine) if int(a[i]) // self.nloc == peer]
+        # the stand-in checks the exchange's own invariants on the oracle's relabelled table
+        assert min(len(want), len(self._remote)) == 0, "matched outputs still cross the pair"
+        send = self.buf[np.array(want, np.int64)] if want else np.zeros((0, self.d), np.float32)
+        self._t = t
+        return torch.from_numpy(send.view(np.uint8).reshape(-1).copy()), len(self._remote)
+
+    def relabel_end(self, t, recv):
+        assert t == self._t
+        s = self.Sloc + t
+        a = self.r["a"][s - 1]
+        rc = recv.numpy().view(np.float32).reshape(-1, self.d)
+        assert rc.shape[0] == len(self._remote), "surplus size mismatch"
+        out = np.empty_like(self.buf)
+        k = 0
+        for l in range(self.nloc):
+            src = int(a[self.pos0 + l])
+            if src // self.nloc == self.rank:
+                out[l] = self.buf[src - self.pos0]
+            else:
+                out[l] = rc[k]
+                k += 1
         self.buf = out
 
     # pull exchange (dist.pull_exchange)
@@ -159,6 +195,7 @@ def _worker(rank, world, port, q, exchange="pairwise", peer_dir=None):
         params = inputs.model_params(cfg)
         N, M = 256, 16
         be = OracleShard(params, N, M, 5, rank, world, peer_dir=peer_dir)
+        be.relabel = exchange == "relabel"
         tr = pfd.TorchTransport()
         if exchange == "peer_fail":  # one rank cannot export: every rank agrees on "no peer"
             if rank == world - 1:
@@ -190,7 +227,8 @@ def _free_port():
 
 
 @pytest.mark.parametrize("world,exchange", [(2, "pairwise"), (4, "pairwise"), (2, "pull"), (4, "pull"),
-                                            (2, "peer"), (4, "peer"), (4, "peer_fail")])
+                                            (2, "peer"), (4, "peer"), (4, "peer_fail"), (2, "relabel"),
+                                            (4, "relabel")])
 def test_gloo_sharded_sequence(world, exchange, tmp_path):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
