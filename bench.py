@@ -428,7 +428,8 @@ def run_ours(args):
                                    "stages_run_mean": float(np.mean(stages)),
                                    "stages_run_hist": np.bincount(stages, minlength=cfg.S + 1).tolist()}
                                   if args.theta > 0 else {}),
-                               **({"algorithm": {1: "AIRPF (Alg. 4 + 5 + 7)", 2: "AIRPF (Alg. 4 + 5 + 6)"}[args.airpf]}
+                               **({"algorithm": {1: "AIRPF (Alg. 4 + 5 + 7)", 2: "AIRPF (Alg. 4 + 5 + 6)"}[args.airpf]
+                                   + (" with the fully adapted scheme: AIRPF2" if args.theta > 0 else "")}
                                   if args.airpf else {}),
                                **({"algorithm": "plain BPF (Alg. 1 + 2, multinomial)"} if args.multinomial else {})),
                 "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,

@@ -144,8 +144,14 @@ int pf_rotation_offset(const pf_handle* h);
  * previous step's island map, weights, resamples every island within itself (pool of M,
  * R19) and composes the S island stages over whole blocks of M (R20, R21); pf_estimate
  * gives the same estimates as for pf_step (before resampling).  Needs a handle created
- * with PF_FLAG_AIRPF, world = 1, M >= 4; exclusive with pf_set_adaptive.  Errors:
- * PF_EINVAL. */
+ * with PF_FLAG_AIRPF, world = 1, M >= 4.
+ * AIRPF2 ("AIRPF with the fully adapted resampling scheme"; DESIGN.md
+ * reading R26): with pf_set_adaptive(theta > 0) as well (handle created with
+ * PF_FLAG_AIRPF | PF_FLAG_ADAPTIVE), the within-island resample runs every step and the
+ * island stages run only up to S* = min{s : E_s >= theta}, E_0 the ESS of the m island
+ * weights, E_s of the level-s island block weights; the islands then carry V_bar_{S*}
+ * (S* = 0: their own island weight) into the next step.  pf_step synchronises once (S*).
+ * Errors: PF_EINVAL; PF_ESTATE when switching while weights are carried. */
 int pf_set_airpf(pf_handle* h, int mode);
 
 /* --- plain BPF: multinomial resampling (Alg. 2) -------------------

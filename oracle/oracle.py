@@ -78,6 +78,9 @@ def lib():
         _lib.orc_augmented_resample_relabel.argtypes = [u64, u64, u64, u64, u32, vp, vp, vp, vp, vp, vp]
         _lib.orc_step_relabel.argtypes = [vp, u64, u64, u64, u64, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                           vp, vp]
+        _lib.orc_island_resample_partial.argtypes = [u64, u64, u32, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp]
+        _lib.orc_step_airpf_adaptive.argtypes = [vp, u64, u64, u64, u32, vp, vp, vp, ctypes.c_double, ctypes.c_int,
+                                                 vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         _lib.orc_step_adaptive_rot.argtypes = [vp, u64, u64, u64, u32, vp, vp, vp, ctypes.c_double, ctypes.c_int,
                                                vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     return _lib
@@ -430,6 +433,65 @@ def run_filter_airpf(params: dict, M: int, m: int, seed: int, ys: np.ndarray, mo
         means[n] = r["filter"][:d]
         x = r["xhat"].astype(np.float32)
     return means
+
+
+def island_resample_partial(logW: np.ndarray, seed: int, n: int, S_exec: int, modified: bool = True) -> dict:
+    """Alg. 6/7 with island stages 1..S_exec (all V_bar levels)."""
+    lw = np.ascontiguousarray(logW, dtype=np.float64)
+    m = lw.shape[0]
+    S = int(round(np.log2(m)))
+    out = dict(src=np.zeros((S, m), np.int32), delta=np.zeros((S, m), np.float32), logVbar=np.zeros(m - 1),
+               Aisl=np.zeros(m, np.int64))
+    rc = lib().orc_island_resample_partial(m, seed, n, _ptr(lw), int(bool(modified)), int(S_exec), _ptr(out["src"]),
+                                           _ptr(out["delta"]), _ptr(out["logVbar"]), _ptr(out["Aisl"]))
+    if rc != 0:
+        raise ValueError(f"orc_island_resample_partial rc={rc}")
+    return out
+
+
+def step_airpf_adaptive(params: dict, N: int, M: int, seed: int, n: int, y: np.ndarray, xin: np.ndarray,
+                        lwc_in: np.ndarray, theta: float, modified: bool = True) -> dict:
+    """One AIRPF2 step (orc_step_airpf_adaptive, reading R26): island stages 1..S* only;
+    lwc = the weight every particle carries into the next step."""
+    mdl = make_model(params)
+    d = mdl.d
+    m = N // M
+    S = int(round(np.log2(m)))
+    xin = np.ascontiguousarray(xin, dtype=np.float32).reshape(N, d)
+    lwc = np.ascontiguousarray(lwc_in, dtype=np.float64).reshape(N)
+    yy = np.ascontiguousarray(y, dtype=np.float32)
+    out = dict(x=np.zeros((N, d)), lw=np.zeros(N), a_w=np.zeros(N, np.int64), wdelta=np.zeros(N, np.float32),
+               logW=np.zeros(m), src=np.zeros((S, m), np.int32), idelta=np.zeros((S, m), np.float32),
+               logVbar=np.zeros(m - 1), Aisl=np.zeros(m, np.int64), xhat=np.zeros((N, d)), lwc=np.zeros(N),
+               filter=np.zeros(2 * d), predict=np.zeros(2 * d), ess=np.zeros(S + 1))
+    ss = ctypes.c_int(-1)
+    rc = lib().orc_step_airpf_adaptive(ctypes.byref(mdl), N, M, seed, n, _ptr(yy), _ptr(xin), _ptr(lwc), float(theta),
+                                       int(bool(modified)), _ptr(out["x"]), _ptr(out["lw"]), _ptr(out["a_w"]),
+                                       _ptr(out["wdelta"]), _ptr(out["logW"]), _ptr(out["src"]), _ptr(out["idelta"]),
+                                       _ptr(out["logVbar"]), _ptr(out["Aisl"]), _ptr(out["xhat"]), _ptr(out["lwc"]),
+                                       _ptr(out["filter"]), _ptr(out["predict"]), _ptr(out["ess"]), ctypes.byref(ss))
+    if rc != 0:
+        raise ValueError(f"orc_step_airpf_adaptive rc={rc}")
+    out["S"], out["m"], out["sstar"] = S, m, int(ss.value)
+    return out
+
+
+def run_filter_airpf_adaptive(params: dict, M: int, m: int, seed: int, ys: np.ndarray, theta: float,
+                              modified: bool = True):
+    """AIRPF2 for len(ys) steps: per-step filter means and the island stages run."""
+    N = M * m
+    d = int(params["d"])
+    x = init(params, N, seed).astype(np.float32)
+    lwc = np.zeros(N)
+    means = np.zeros((len(ys), d))
+    stages = np.zeros(len(ys), np.int32)
+    for n, y in enumerate(ys):
+        r = step_airpf_adaptive(params, N, M, seed, n, y, x, lwc, theta, modified)
+        means[n] = r["filter"][:d]
+        stages[n] = r["sstar"]
+        x = r["xhat"].astype(np.float32)
+        lwc = r["lwc"]
+    return means, stages
 
 
 # ----------------------------------------------------------------------------- Alg. 2

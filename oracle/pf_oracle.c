@@ -758,11 +758,29 @@ int orc_within_island(uint64_t N, uint64_t M, uint64_t seed, uint32_t n, const d
  *   (lines 'loop'/'exchange'; reading R21).
  * src[(s-1) m + i] = the island whose stage-(s-1) block island i holds after stage s;
  * delta as for stage s >= 2; Aisl[i] = src_1(src_2(...src_S(i))). */
+static int island_resample_upto(uint64_t m, uint64_t seed, uint32_t n, const double* logW, int modified,
+                                int S_exec, int32_t* src, float* delta, double* logVbar, int64_t* Aisl);
+
 int orc_island_resample(uint64_t m, uint64_t seed, uint32_t n, const double* logW, int modified,
                         int32_t* src, float* delta, double* logVbar, int64_t* Aisl)
 {
+    return island_resample_upto(m, seed, n, logW, modified, ilog2_exact(m), src, delta, logVbar, Aisl);
+}
+
+/* Alg. 6/7 with only the island stages 1..S_exec executed (the fully adapted AIRPF,
+ * AIRPF2 of PAPER.md:1279; reading R26): every V_bar level is computed, the
+ * draws and the composition for s <= S_exec; src rows of later stages are untouched. */
+int orc_island_resample_partial(uint64_t m, uint64_t seed, uint32_t n, const double* logW, int modified,
+                                int S_exec, int32_t* src, float* delta, double* logVbar, int64_t* Aisl)
+{
+    return island_resample_upto(m, seed, n, logW, modified, S_exec, src, delta, logVbar, Aisl);
+}
+
+static int island_resample_upto(uint64_t m, uint64_t seed, uint32_t n, const double* logW, int modified,
+                                int S_exec, int32_t* src, float* delta, double* logVbar, int64_t* Aisl)
+{
     int S = ilog2_exact(m);
-    if (S < 1) return ORC_EINVAL;
+    if (S < 1 || S_exec < 0 || S_exec > S) return ORC_EINVAL;
     double* lv = (double*)malloc(sizeof(double) * (m - 1));
     int32_t* sr = (int32_t*)malloc(sizeof(int32_t) * m * (uint64_t)S);
     if (!lv || !sr) {
@@ -774,6 +792,7 @@ int orc_island_resample(uint64_t m, uint64_t seed, uint32_t n, const double* log
         const double* prev = (s == 1) ? logW : lv + level_offset(m, s - 1);
         double* cur = lv + level_offset(m, s);
         for (uint64_t bk = 0; bk < (m >> s); ++bk) cur[bk] = log_pair_mean(prev[2 * bk], prev[2 * bk + 1]);
+        if (s > S_exec) continue;
         uint64_t bit = 1ull << (s - 1);
         for (uint64_t i = 0; i < m; ++i) {
             uint64_t h = i ^ bit;
@@ -801,10 +820,10 @@ int orc_island_resample(uint64_t m, uint64_t seed, uint32_t n, const double* log
     }
     for (uint64_t i = 0; i < m; ++i) {
         uint64_t c = i;
-        for (int s = S; s >= 1; --s) c = (uint64_t)sr[(uint64_t)(s - 1) * m + c];
+        for (int s = S_exec; s >= 1; --s) c = (uint64_t)sr[(uint64_t)(s - 1) * m + c];
         Aisl[i] = (int64_t)c;
     }
-    if (src) memcpy(src, sr, sizeof(int32_t) * m * (uint64_t)S);
+    if (src) memcpy(src, sr, sizeof(int32_t) * m * (uint64_t)S_exec);
     if (logVbar) memcpy(logVbar, lv, sizeof(double) * (m - 1));
     free(lv); free(sr);
     return ORC_OK;
@@ -1201,5 +1220,64 @@ int orc_step_relabel(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t G, u
         orc_estimates(d, N, lw, x, Aloc, filt, pred, resamp);
     }
     free(xprev); free(Aloc);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------- */
+/* AIRPF with the fully adapted scheme, AIRPF2 ("AIRPF with the fully adapted
+ * resampling scheme"; the scheme of PAPER.md:570-576; reading R26).  One step:
+ *   mutate (n >= 1), weight: lw = log g_n + lwc_in (the weight carried from the previous
+ *   step, constant over each island), estimates (before resampling, with the carried
+ *   weights), within-island resample (Alg. 5, always), island log-means logW = log W_check;
+ *   the ESS of the island weights E_0 = ESS(W_check) over the m islands (every particle of
+ *   island k carries W_check_k after Alg. 5, so it is the particle-level ESS) and of every
+ *   level E_s = ESS(V_bar_s) over the m / 2^s blocks (orc_ess_levels with M = 1);
+ *   S* = min{s : E_s >= theta} (orc_stages_to_run, reading R17); the island stages
+ *   1..S* (Alg. 6/7); the islands carry V_bar_{S*} of their block (S* = 0: their own
+ *   W_check), normalised by V_bar_S (lwc_out per particle, reading R18). */
+int orc_step_airpf_adaptive(const orc_model* mdl, uint64_t N, uint64_t M, uint64_t seed, uint32_t n,
+                            const float* y, const float* xin, const double* lwc_in, double theta, int modified,
+                            double* x, double* lw, int64_t* a_w, float* wdelta, double* logW, int32_t* src,
+                            float* idelta, double* logVbar, int64_t* Aisl, double* xhat_out, double* lwc_out,
+                            double* filt, double* pred, double* ess, int* sstar)
+{
+    int d = mdl->d;
+    uint64_t m = N / M;
+    int S = ilog2_exact(m);
+    if (S < 1) return ORC_EINVAL;
+    double* xprev = (double*)malloc(sizeof(double) * N * (uint64_t)d);
+    double* lvb = (double*)malloc(sizeof(double) * (m - 1));
+    int64_t* Ai = (int64_t*)malloc(sizeof(int64_t) * m);
+    if (!xprev || !lvb || !Ai) {
+        free(xprev); free(lvb); free(Ai);
+        return ORC_ENOMEM;
+    }
+    for (uint64_t i = 0; i < N * (uint64_t)d; ++i) xprev[i] = (double)xin[i];
+    if (n == 0) memcpy(x, xprev, sizeof(double) * N * (uint64_t)d);
+    else orc_mutate(mdl, N, seed, n, xprev, x);
+    orc_logweight(mdl, N, y, x, lw);
+    for (uint64_t i = 0; i < N; ++i) lw[i] += lwc_in[i];
+    orc_estimates(d, N, lw, x, NULL, filt, pred, NULL);
+    int rc = orc_within_island(N, M, seed, n, lw, a_w, wdelta, logW);
+    if (rc == ORC_OK) rc = island_resample_upto(m, seed, n, logW, modified, 0, NULL, NULL, lvb, Ai);
+    if (rc == ORC_OK) {
+        orc_ess_levels(m, 1, logW, lvb, ess);
+        int ss = orc_stages_to_run(S, ess, theta);
+        *sstar = ss;
+        rc = island_resample_upto(m, seed, n, logW, modified, ss, src, idelta, logVbar, Ai);
+        if (rc == ORC_OK) {
+            double lvS = lvb[level_offset(m, S)];
+            for (uint64_t i = 0; i < m; ++i) {
+                Aisl[i] = Ai[i];
+                double c = (ss == 0) ? logW[i] - lvS : lvb[level_offset(m, ss) + (i >> ss)] - lvS;
+                for (uint64_t j = 0; j < M; ++j) {
+                    uint64_t a = (uint64_t)a_w[(uint64_t)Ai[i] * M + j];
+                    for (int k = 0; k < d; ++k) xhat_out[(i * M + j) * d + k] = x[a * d + k];
+                    lwc_out[i * M + j] = c;
+                }
+            }
+        }
+    }
+    free(xprev); free(lvb); free(Ai);
     return rc;
 }

@@ -189,7 +189,16 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, uint64
         sp.pipe = pipe;
         sp.tb = (env_u32("PF_STAGE_TB", 2u) == 2u && stages_smem(sp.P, sb, k, 2u, pipe) <= budget) ? 2u : tbmin;
         sp.threads = pick_threads(sp.P / 4, env_u32("PF_STAGE_THREADS", kStageThreadsDefault), &sp.qpt);
-        sp.smem = stages_smem(sp.P, sb, k, sp.tb, pipe);
+        // warp-specialised pass (k_stages_ws): half the CTA walks, half draws, each on QPT
+        // quads per thread; needs whole-quad groups (M >= 4), bulk-copied groups and a CTA
+        // of 2 x P/4/QPT <= 1024 threads
+        if (pipe && env_u32("PF_STAGE_WS", 1u) && M >= 4u && (uint64_t)M * sb >= 16u && sp.P / 4u >= 64u &&
+            stages_smem(sp.P, sb, k, sp.tb, 2u) <= budget) {
+            sp.pipe = 2u;
+            sp.qpt = 1u;  // unused: runtime loops
+            sp.threads = std::min<uint32_t>(1024u, sp.P / 4u * 2u);
+        }
+        sp.smem = stages_smem(sp.P, sb, k, sp.tb, sp.pipe);
         const uint32_t per_sm = std::max(1u, std::min(kSmemPerSM / (sp.smem + 1024u), 2048u / sp.threads));
         sp.grid = (uint32_t)std::min<uint64_t>(N / sp.P, (uint64_t)nsm * per_sm);
         p.passes.push_back(sp);
@@ -255,12 +264,13 @@ Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags, uint32
     L.pull_outpos = take(sh ? N * 4 : 0);
     L.pull_serve = take(sh ? xb * world : 0);  // worst case: every rank reads only this shard
     const bool ad = flags & PF_FLAG_ADAPTIVE;
+    const bool air_flag = flags & PF_FLAG_AIRPF;
     const bool mn = flags & PF_FLAG_MULTINOMIAL;
     L.lw0 = take((ad || mn) ? N * 4 : 0);
     L.lw1 = take(ad ? N * 4 : 0);
-    L.carry_lv = take(ad ? (m / 2) * 8 : 0);
+    L.carry_lv = take(ad ? (air_flag ? m : m / 2) * 8 : 0);
     L.ess_part = take((ad || mn) ? (size_t)p.NT * 3 * 8 : 0);
-    L.ess_chunks = take(ad ? (size_t)(p.NT / kEssChunk + 2 * m / kEssChunk + 64) * 2 * 8 : 0);
+    L.ess_chunks = take(ad ? (size_t)(p.NT / kEssChunk + 3 * m / kEssChunk + 64) * 2 * 8 : 0);
     L.ess_out = take(ad ? (size_t)(S + 3) * 8 : 0);
     L.ess_lmax = take((ad || mn) ? 16 : 0);
     const size_t nt_mn = (N + kMnTile - 1) / kMnTile;
@@ -520,7 +530,7 @@ static void launch_pass1(pf_handle* h, const Pass1Args& a, int mode = kPass1Fuse
 
 static void launch_cascade_k(pf_handle* h) {
     const Plan& p = h->plan;
-    CascadeArgs c;
+    CascadeArgs c{};
     c.logV = h->at<double>(h->lay.logV);
     c.thr = h->at<uint32_t>(h->lay.thr);
     c.part = h->at<double>(h->lay.part);
@@ -539,7 +549,7 @@ static void launch_cascade_k(pf_handle* h) {
 }
 
 static void launch_stages_k(pf_handle* h, const StagePass& cp, const void* pin, void* pout, uint32_t out_rot = 0u) {
-    StageArgs a;
+    StageArgs a{};
     a.key = make_key(h->seed);
     a.n = h->n;
     a.N = h->N;
@@ -552,6 +562,8 @@ static void launch_stages_k(pf_handle* h, const StagePass& cp, const void* pin, 
     a.P = cp.P;
     a.lowbits = cp.s0 - 1;
     a.pipe = cp.pipe;
+    // k_stages_ws: walkers = the given fraction (in 32ths) of the CTA, whole warps
+    a.ws_walkers = std::max<uint32_t>(32u, (cp.threads * env_u32("PF_STAGE_WS_WALK32", 10u) / 32u) & ~31u);
     a.out_rot = out_rot;
     a.out_S = h->S;
     a.pin = pin;
@@ -570,6 +582,14 @@ static StagePass stage_pass_for(const pf_handle* h, const StagePass& sp, uint32_
     q.k = k;
     q.P = h->M << k;
     q.threads = pick_threads(q.P / 4, env_u32("PF_STAGE_THREADS", kStageThreadsDefault), &q.qpt);
+    if (q.pipe == 2u) {
+        if (q.P / 4u >= 64u) {
+            q.qpt = 1u;
+            q.threads = std::min<uint32_t>(1024u, q.P / 4u * 2u);
+        } else {
+            q.pipe = 1u;
+        }
+    }
     q.smem = stages_smem(q.P, sb, k, q.tb, q.pipe);
     int nsm = 148, dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
@@ -626,7 +646,7 @@ static int run_step_adaptive(pf_handle* h, const float* y_host, const float* y_d
     const Plan& p = h->plan;
     const int src = h->cur, mid = h->cur ^ 1;
     float* lw = h->at<float>(h->lwi ? h->lay.lw1 : h->lay.lw0);
-    Pass1Args a;
+    Pass1Args a{};
     fill_pass1(h, a, y_host, y_dev);
     a.x_in = h->X(src);
     a.x_out = h->X(mid);  // x_n in natural order
@@ -645,7 +665,8 @@ static int run_step_adaptive(pf_handle* h, const float* y_host, const float* y_d
     int launches = 1;
     h->mark(PF_KERNEL_CASCADE, true);
     launch_cascade_k(h);
-    EssArgs e;
+    EssArgs e{};
+    e.lv0 = nullptr;  // level 0 = the particle weights (tile partials)
     e.ess_part = h->at<double>(h->lay.ess_part);
     e.logV = h->at<double>(h->lay.logV);
     e.lmax = h->at<unsigned int>(h->lay.ess_lmax);
@@ -670,7 +691,7 @@ static int run_step_adaptive(pf_handle* h, const float* y_host, const float* y_d
     // stage rotation (R23): the last kernel of the step writes the next layout
     const uint32_t rot = (h->rotate && ss >= 1u && ss < h->S) ? ss : 0u;
     if (ss >= 1u) {
-        Pass1Args r;
+        Pass1Args r{};
         fill_pass1(h, r, y_host, y_dev);
         r.do_mutate = 0;
         r.x_in = h->X(mid);
@@ -728,7 +749,7 @@ static int run_step_adaptive(pf_handle* h, const float* y_host, const float* y_d
 //   island thresholds) -> k_island_draw -> k_island_compose (the new island map).
 // x_hat is never materialised: the next step reads block A_isl[g] for island g.
 static int run_step_airpf(pf_handle* h, const float* y_host, const float* y_dev) {
-    Pass1Args a;
+    Pass1Args a{};
     fill_pass1(h, a, y_host, y_dev);
     a.x_in = h->X(h->cur);
     a.x_out = h->X(h->cur ^ 1);
@@ -738,30 +759,81 @@ static int run_step_airpf(pf_handle* h, const float* y_host, const float* y_dev)
     // launch bounds of kPass1Airpf) fits 8 CTAs per SM (C4: 4.79 -> 4.42 ms per pass; the
     // same change measured slower for d = 1)
     if (h->plan.D >= 4) a.sl = pass1_smem(h->plan.D, h->plan.P1, h->M, 1u, h->plan.pass1_threads, h->plan.tb);
+    const bool adaptive = h->theta > 0.0;  // AIRPF2 (reading R26)
+    if (adaptive) {
+        a.carry_mode = h->carry_mode;  // 0 or 2 (block carry: the island's V_bar_{S*} or W_check)
+        a.carry_lv = h->at<double>(h->lay.carry_lv);
+        a.carry_shift = h->carry_shift;
+        a.carry_mask = h->carry_mask;
+        a.carry_c = h->carry_c;
+        a.ess_lmax = h->at<unsigned int>(h->lay.ess_lmax);
+    }
     h->mark(PF_KERNEL_PASS1, true);
     launch_pass1(h, a, kPass1Airpf);
     h->mark(PF_KERNEL_PASS1, false);
     h->mark(PF_KERNEL_CASCADE, true);
     launch_cascade_k(h);
-    IslandArgs ia;
+    uint32_t ss = h->S;
+    double lvS = 0.0;
+    int launches = 4;
+    if (adaptive) {  // island ESS levels, S*: the island stages that run
+        EssArgs e{};
+        e.lv0 = h->at<double>(h->lay.isl_logW);
+        e.ess_part = nullptr;
+        e.logV = h->at<double>(h->lay.logV);
+        e.lmax = h->at<unsigned int>(h->lay.ess_lmax);
+        e.chunks = h->at<double>(h->lay.ess_chunks);
+        e.out = h->at<double>(h->lay.ess_out);
+        e.N = h->N;
+        e.NT = h->plan.NT;
+        e.m = h->m;
+        e.S = h->S;
+        e.theta = h->theta;
+        launch_ess(LaunchCfg{0u, 0u, 0u, h->stream}, e);
+        launches += 2;
+        double tail[2];
+        cudaError_t ce = cudaMemcpyAsync(tail, e.out + h->S + 1, sizeof(tail), cudaMemcpyDeviceToHost, h->stream);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(h->stream);
+        if (ce != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_step (AIRPF2): ") + cudaGetErrorString(ce));
+        ss = (uint32_t)tail[0];
+        lvS = tail[1];
+    }
+    IslandArgs ia{};
     ia.key = make_key(h->seed);
     ia.n = h->n;
     ia.m = h->m;
-    ia.S = h->S;
+    ia.S = ss;  // island stages 1..S* (all S unless AIRPF2 stops early)
     ia.modified = h->airpf == 1;
     ia.thr = h->at<uint32_t>(h->lay.thr);
     ia.choice = h->at<uint8_t>(h->lay.isl_choice);
     ia.A = h->at<int32_t>(h->lay.isl_A);
     launch_island(h->stream, ia);
     h->mark(PF_KERNEL_CASCADE, false);
+    if (adaptive) {  // the weights the islands carry into the next step (R18 / R26)
+        if (ss == 0u) {
+            h->carry_mode = 2;
+            h->carry_shift = 0u;
+            cudaMemcpyAsync(h->at<double>(h->lay.carry_lv), h->at<double>(h->lay.isl_logW), (size_t)h->m * 8,
+                            cudaMemcpyDeviceToDevice, h->stream);
+        } else if (ss < h->S) {
+            h->carry_mode = 2;
+            h->carry_shift = ss;
+            cudaMemcpyAsync(h->at<double>(h->lay.carry_lv), h->at<double>(h->lay.logV) + level_offset(h->m, (int)ss),
+                            (size_t)(h->m >> ss) * 8, cudaMemcpyDeviceToDevice, h->stream);
+        } else {
+            h->carry_mode = 0;
+        }
+        h->carry_mask = 0xffffffffu;
+        h->carry_c = lvS;
+    }
     h->cur ^= 1;
     h->isl_valid = true;
-    h->sstar_last = (int)h->S;
+    h->sstar_last = (int)ss;
     h->step_n = h->n;
     h->n += 1;
     h->have_step = true;
     h->top_done = true;
-    h->last_launches = 4;
+    h->last_launches = launches;
     return check_cuda(h, "pf_step (AIRPF)");
 }
 
@@ -770,7 +842,7 @@ static int run_step_airpf(pf_handle* h, const float* y_host, const float* y_dev)
 static int run_step_multinomial(pf_handle* h, const float* y_host, const float* y_dev) {
     const int src = h->cur, mid = h->cur ^ 1;
     float* lw = h->at<float>(h->lay.lw0);
-    Pass1Args a;
+    Pass1Args a{};
     fill_pass1(h, a, y_host, y_dev);
     a.x_in = h->X(src);
     a.x_out = h->X(mid);
@@ -783,7 +855,7 @@ static int run_step_multinomial(pf_handle* h, const float* y_host, const float* 
     h->mark(PF_KERNEL_CASCADE, true);
     launch_cascade_k(h);
     h->mark(PF_KERNEL_CASCADE, false);
-    MultinomialArgs mn;
+    MultinomialArgs mn{};
     mn.key = make_key(h->seed);
     mn.n = h->n;
     mn.N = h->N;
@@ -811,11 +883,11 @@ static int run_step_multinomial(pf_handle* h, const float* y_host, const float* 
 }
 
 static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
+    if (h->airpf) return run_step_airpf(h, y_host, y_dev);  // AIRPF, or AIRPF2 with theta > 0
     if (h->theta > 0.0) return run_step_adaptive(h, y_host, y_dev);
     if (h->multinomial) return run_step_multinomial(h, y_host, y_dev);
-    if (h->airpf) return run_step_airpf(h, y_host, y_dev);
     const Plan& p = h->plan;
-    Pass1Args a;
+    Pass1Args a{};
     fill_pass1(h, a, y_host, y_dev);
     const int src = h->cur, dst = h->cur ^ 1;
     a.x_in = h->X(src);
@@ -939,7 +1011,7 @@ static int init_core(const pf_model* model, uint64_t N, uint32_t M, uint64_t see
     if (flags & (PF_FLAG_ADAPTIVE | PF_FLAG_MULTINOMIAL))
         cudaMemsetAsync(h->at<uint32_t>(L.ess_lmax), 0, 16, h->stream);  // running max, reset after each use
     {
-        InitArgs ia;
+        InitArgs ia{};
         ia.mp = h->mp;
         ia.key = make_key(seed);
         ia.N = h->N;
@@ -995,7 +1067,7 @@ int pf_shard_record(pf_handle* h, const double** dev_rec) {
 int pf_step_top(pf_handle* h, const double* dev_all_recs) {
     if (!h || !dev_all_recs) return fail(h, PF_EINVAL, "NULL argument");
     if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
-    TopArgs t;
+    TopArgs t{};
     t.recs = dev_all_recs;
     t.top_logV = h->at<double>(h->lay.top_logV);
     t.top_thr = h->at<uint32_t>(h->lay.top_thr);
@@ -1027,7 +1099,7 @@ int pf_cross_stage(pf_handle* h, int t, const void* dev_partner_states) {
     if (!h->top_done) return fail(h, PF_ESTATE, "pf_step_top must run first");
     const uint32_t* top_thr = h->at<uint32_t>(h->lay.top_thr);
     const uint32_t G = h->world;
-    CrossArgs c;
+    CrossArgs c{};
     c.key = make_key(h->seed);
     c.n = h->step_n;
     c.s = h->S + (uint32_t)t;
@@ -1055,7 +1127,7 @@ int pf_cross_stage(pf_handle* h, int t, const void* dev_partner_states) {
 
 // ---- pull exchange of the cross stages (include/pf.h) --------------------
 static PullArgs pull_args(pf_handle* h) {
-    PullArgs a;
+    PullArgs a{};
     a.key = make_key(h->seed);
     a.n = h->step_n;
     a.S_loc = h->S;
@@ -1202,7 +1274,7 @@ int pf_cross_peer(pf_handle* h) {
     if (!h->top_done) return fail(h, PF_ESTATE, "pf_step_top must run first");
     if (h->peer_ws.size() != h->world) return fail(h, PF_ESTATE, "no peer mapping: pf_peer_open or pf_peer_set first");
     const PullArgs a = pull_args(h);
-    PeerArgs p;
+    PeerArgs p{};
     const size_t xoff = h->cur ? h->lay.X1 : h->lay.X0;  // same layout on every rank
     for (uint32_t r = 0; r < kPeerMaxG; ++r)
         p.x[r] = r < h->world ? reinterpret_cast<const float*>(h->peer_ws[r] + xoff) : nullptr;
@@ -1216,7 +1288,7 @@ int pf_cross_peer(pf_handle* h) {
 
 // ---- relabelled exchange of the cross stages (include/pf.h; reading R24) ----
 static RelabelArgs relabel_args(pf_handle* h, int t) {
-    RelabelArgs a;
+    RelabelArgs a{};
     a.key = make_key(h->seed);
     a.n = h->step_n;
     a.s = h->S + (uint32_t)t;
@@ -1500,7 +1572,9 @@ int pf_set_airpf(pf_handle* h, int mode) {
     if (!h) return fail(h, PF_EINVAL, "NULL handle");
     if (mode < 0 || mode > 2) return fail(h, PF_EINVAL, "mode must be 0 (off), 1 (Alg. 7) or 2 (Alg. 6)");
     if (mode && !(h->flags & PF_FLAG_AIRPF)) return fail(h, PF_EINVAL, "handle not created with PF_FLAG_AIRPF");
-    if (mode && (h->theta > 0.0 || h->multinomial)) return fail(h, PF_EINVAL, "one resampling scheme at a time");
+    if (mode && (h->multinomial || h->rotate)) return fail(h, PF_EINVAL, "one resampling scheme at a time");
+    if (h->airpf != mode && h->carry_mode != 0)  // carried weights belong to the scheme that made them
+        return fail(h, PF_ESTATE, "particles carry weights of an early-stopped step: run one step with theta = 1 first");
     if (!mode && h->isl_valid) {  // back to augmented resampling: materialise x_hat first
         launch_block_gather(h->stream, h->X(h->cur), h->X(h->cur ^ 1), h->at<int32_t>(h->lay.isl_A), h->N, h->b,
                             (uint32_t)h->plan.D);
@@ -1517,7 +1591,8 @@ int pf_set_adaptive(pf_handle* h, double theta) {
     if (theta > 0.0 && !(h->flags & PF_FLAG_ADAPTIVE))
         return fail(h, PF_EINVAL, "handle not created with PF_FLAG_ADAPTIVE");
     if (theta > 0.0 && h->world != 1) return fail(h, PF_EINVAL, "the fully adapted scheme needs world = 1");
-    if (theta > 0.0 && (h->airpf || h->multinomial)) return fail(h, PF_EINVAL, "one resampling scheme at a time");
+    if (theta > 0.0 && (h->multinomial || (h->airpf && h->rotate)))
+        return fail(h, PF_EINVAL, "one resampling scheme at a time");
     // an early-stopped step leaves weighted particles (R18): a plain step would treat them as
     // equally weighted, so switching off is refused until a step has run all S stages
     if (theta == 0.0 && h->carry_mode != 0)

@@ -108,9 +108,11 @@ struct StageArgs {
     uint64_t N;     // particles of this shard
     uint32_t pos0;  // global index of the shard's first particle (RNG counters)
     uint32_t m, M, b, s0, k, P, lowbits;
-    uint32_t pipe;        // 1: software-pipelined (two buffers of everything); 0: one buffer
+    uint32_t pipe;        // 2: warp-specialised (k_stages_ws); 1: software-pipelined (two buffers
+                          // of everything); 0: one buffer
     uint32_t out_rot;     // stage rotation (R23): outputs go to group rotr_S(g, out_rot)
     uint32_t out_S;       //   of the next layout (0: no move; needs M >= 4)
+    uint32_t ws_walkers;  // k_stages_ws: walker threads (the rest of the CTA draws)
     const void* pin;      // states at stage s0-1 (packed AoS, shard-local)
     void* pout;           // states at stage s0+k-1
     const uint32_t* thr;  // side thresholds, level-table layout (level_offset)
@@ -124,7 +126,7 @@ __host__ __device__ inline uint32_t stages_smem(uint32_t P, uint32_t state_bytes
     const uint32_t st = (P * state_bytes + 15u) & ~15u;
     const uint32_t tab = (k * P * tb + 15u) & ~15u;
     const uint32_t nb = pipe ? 2u : 1u;
-    return nb * (st + tab + 4u * (1u << k)) + 16u;
+    return nb * (st + tab + 4u * (1u << k)) + (pipe == 2u ? 64u : 16u);
 }
 
 
@@ -155,6 +157,7 @@ constexpr uint32_t kEssChunk = 4096;
 constexpr int kEssThreads = 256;
 
 struct EssArgs {
+    const double* lv0;       // AIRPF2: level 0 = the m island log-weights (R26); null: the tile partials
     const double* ess_part;  // NT x 3
     const double* logV;      // level table (m - 1)
     unsigned int* lmax;      // running max of lw (float_order_bits), reset by k_ess_final
@@ -166,7 +169,7 @@ struct EssArgs {
 };
 
 __host__ __device__ inline uint32_t ess_level_count(const EssArgs& a, uint32_t s) {
-    return s == 0 ? a.NT : (a.m >> s);
+    return s == 0 ? (a.lv0 ? a.m : a.NT) : (a.m >> s);
 }
 __host__ __device__ inline uint32_t ess_chunks_total(const EssArgs& a) {
     uint32_t t = 0;

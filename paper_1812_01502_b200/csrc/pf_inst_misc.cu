@@ -24,7 +24,11 @@ __global__ void __launch_bounds__(kEssThreads) k_ess_chunks(const __grid_constan
     double s1 = 0.0, s2 = 0.0;
     if (L != -CUDART_INF) {
         for (uint32_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-            if (s == 0) {
+            if (s == 0 && a.lv0) {  // AIRPF2: the island weights
+                const double f = exp(a.lv0[j] - L);
+                s1 += f;
+                s2 += f * f;
+            } else if (s == 0) {
                 const double* t = a.ess_part + (uint64_t)j * 3;
                 if (t[0] == -CUDART_INF) continue;
                 const double f = exp(t[0] - L);
@@ -70,7 +74,7 @@ __global__ void k_ess_final(const __grid_constant__ EssArgs a) {
             s1 += __shfl_xor_sync(0xffffffffu, s1, o);
             s2 += __shfl_xor_sync(0xffffffffu, s2, o);
         }
-        const double units = s == 0 ? (double)a.N : (double)(a.m >> s);
+        const double units = s == 0 ? (a.lv0 ? (double)a.m : (double)a.N) : (double)(a.m >> s);
         if (lane == 0) a.out[s] = (s2 > 0.0) ? s1 * s1 / (units * s2) : 1.0;  // no weight at all: equal
     }
     __syncthreads();
@@ -160,7 +164,7 @@ __global__ void __launch_bounds__(256) k_island_compose(const __grid_constant__ 
 
 void launch_island(cudaStream_t st, const IslandArgs& a) {
     const uint64_t work = (uint64_t)((a.m + 3u) >> 2) * a.S;
-    k_island_draw<<<(uint32_t)((work + 255) / 256), 256, 0, st>>>(a);
+    if (work) k_island_draw<<<(uint32_t)((work + 255) / 256), 256, 0, st>>>(a);  // S* = 0 (AIRPF2): no stage
     k_island_compose<<<(a.m + 255) / 256, 256, 0, st>>>(a);
 }
 

@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : PF_
 #pragma unroll
             for (int e = 0; e < 4; ++e) lw[it][e] = valid ? log_potential<D, KIND>(a.mp, y, x + e * D) : -CUDART_INF_F;
         }
-        if constexpr (MODE == kPass1Weigh) {  // carried weight of the previous step (R18)
+        if constexpr (MODE == kPass1Weigh || MODE == kPass1Airpf) {  // carried weight (R18; AIRPF2: R26)
             if (valid && a.carry_mode != 0) {
                 float cw[4];
                 if (a.carry_mode == 1) {
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : PF_
 #pragma unroll
                 for (int e = 0; e < 4; ++e) lw[it][e] += cw[e];
             }
-            if (valid) {
+            if (MODE == kPass1Weigh && valid) {
                 reinterpret_cast<float4*>(a.lw_out + i0)[0] = make_float4(lw[it][0], lw[it][1], lw[it][2], lw[it][3]);
 #pragma unroll
                 for (int c = 0; c < D; ++c)
@@ -562,6 +562,9 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : PF_
                 a.ess_part[(uint64_t)tile * 3 + 2] = sq;
                 atomicMax(a.ess_lmax, float_order_bits(tmax));
             }
+        }
+        if constexpr (MODE == kPass1Airpf) {  // AIRPF2: the running max of lw shifts the island ESS sums
+            if (lane == 0 && a.ess_lmax) atomicMax(a.ess_lmax, float_order_bits(tmax));
         }
     }
 }

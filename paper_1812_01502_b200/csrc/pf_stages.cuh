@@ -311,4 +311,200 @@ __global__ void __launch_bounds__(1024, 1) k_stages(const __grid_constant__ Stag
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// k_stages_ws: the same pass, warp-specialised so that the Philox-bound draws and the
+// shared-memory-bound walk run concurrently on every SM sub-partition instead of in
+// alternating phases separated by a CTA barrier.
+//   warps [0, nw/2)   walkers: wait for tile t's tables and states, walk and store the
+//                     outputs, release the slot; walker warp 0 then issues the TMA bulk
+//                     copies of tile t+2 into the slot it just released
+//   warps [nw/2, nw)  drawers: wait for the slot's release, copy tile t's thresholds
+//                     (drawer-only named barrier), draw the k stages into the slot's tables
+// Two slots of {states, tables, thresholds}; mbarriers per slot: st_full (TMA bytes),
+// tab_full (every drawer thread arrives), slot_free (every walker thread arrives); the
+// parity of tile t's phase is (t >> 1) & 1.  Same tables, same outputs as k_stages.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+// One stage's draws of quad l0 (tile position; M >= 4: the quad lies in one group j):
+// the table entry of each of its 4 outputs
+template <int TB>
+__device__ __forceinline__ void ws_entries(const StageArgs& a, const uint4 blk, uint32_t Pt, uint32_t j, uint32_t st,
+                                           unsigned char* tabs, uint32_t l0) {
+    const uint32_t b = a.b, mask = a.M - 1u, bit = 1u << st;
+    const uint32_t rw[4] = {blk.x, blk.y, blk.z, blk.w};
+    // the shifted group bases stay in registers (otherwise the shift is sunk below the
+    // select, one per draw); entries packed by PRMT
+    uint32_t blo = (j & ~bit) << b, bhi = (j | bit) << b;
+    asm volatile("" : "+r"(blo), "+r"(bhi));
+    uint32_t en[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const bool hi = (rw[e] >> b) >= Pt;
+        if constexpr (TB == 1) en[e] = (rw[e] & mask) | (hi ? 0x80u : 0u);
+        else en[e] = (hi ? bhi : blo) | (rw[e] & mask);
+    }
+    if constexpr (TB == 1)
+        *reinterpret_cast<uint32_t*>(tabs + st * a.P + l0) =
+            __byte_perm(__byte_perm(en[0], en[1], 0x0040u), __byte_perm(en[2], en[3], 0x0040u), 0x5410u);
+    else
+        *reinterpret_cast<uint2*>(tabs + 2u * (st * a.P + l0)) =
+            make_uint2(__byte_perm(en[0], en[1], 0x5410u), __byte_perm(en[2], en[3], 0x5410u));
+}
+
+// The drawers' share of a tile: the k x P/4 (stage, quad) blocks in flat order f = st P/4 + q
+// (consecutive threads: consecutive quads of one stage), f = rt, rt + nthr, ... -- balanced
+// to one block whatever the drawer count; two blocks per iteration (two independent Philox
+// chains in flight)
+template <int TB, bool DBG>
+__device__ __forceinline__ void ws_draws(const StageArgs& a, const StageTile& g, const uint32_t* ths,
+                                         unsigned char* tabs, uint32_t rt, uint32_t nthr) {
+    const uint32_t b = a.b, k = a.k, nq = a.P >> 2, lowbits = a.lowbits, mask = a.M - 1u;
+    const uint32_t tlo = g.tlo, thi = g.thi, nf = k * nq, lnq = b + k - 2u;  // P / 4 = 2^lnq
+    for (uint32_t f0 = rt; f0 < nf; f0 += 2u * nthr) {
+        const uint32_t f1 = f0 + nthr;
+        const bool two = f1 < nf;
+        uint4 blk[2];
+        uint32_t st[2], l[2], j[2], Pt[2], gp[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t f = (h == 0 || !two) ? f0 : f1;
+            st[h] = f >> lnq;
+            const uint32_t q = f & (nq - 1u);
+            l[h] = 4u * q;
+            j[h] = l[h] >> b;
+            gp[h] = ((tlo | (j[h] << lowbits) | thi) << b) | (l[h] & mask);
+            blk[h] = rng_block(a.key, (a.pos0 + gp[h]) >> 2, a.n, kDomainResample, a.s0 + st[h]);
+            Pt[h] = ths[(1u << k) - (1u << (k - st[h])) + (j[h] >> (st[h] + 1))];
+        }
+        ws_entries<TB>(a, blk[0], Pt[0], j[0], st[0], tabs, l[0]);
+        if (two) ws_entries<TB>(a, blk[1], Pt[1], j[1], st[1], tabs, l[1]);
+        if constexpr (DBG) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (h == 1 && !two) break;
+                const uint32_t bit = 1u << st[h], s = a.s0 + st[h];
+                const uint32_t rw[4] = {blk[h].x, blk[h].y, blk[h].z, blk[h].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const bool hi = (rw[e] >> b) >= Pt[h];
+                    const uint32_t jj = hi ? (j[h] | bit) : (j[h] & ~bit);
+                    const uint32_t gsrc = ((tlo | (jj << lowbits) | thi) << b) | (rw[e] & mask);
+                    a.dbg_anc[(uint64_t)(s - 1) * a.N + gp[h] + e] = (int32_t)(a.pos0 + gsrc);
+                }
+            }
+        }
+    }
+}
+
+template <typename T, int TB>
+__device__ __forceinline__ void ws_walk(const StageArgs& a, const StageTile& g, const T* xs, const unsigned char* tabs,
+                                        uint32_t tid, uint32_t nthr) {
+    const uint32_t M = a.M, b = a.b, k = a.k, P = a.P, mask = M - 1u, nq = P >> 2, lowbits = a.lowbits;
+    T* pout = reinterpret_cast<T*>(a.pout);
+    for (uint32_t q = tid; q < nq; q += nthr) {
+        const uint32_t l0 = 4u * q;
+        uint32_t tp[4] = {l0, l0 + 1u, l0 + 2u, l0 + 3u};
+        for (int st = (int)k - 1; st >= 0; --st) {
+            if constexpr (TB == 1) {
+                const unsigned char* Ts = tabs + (uint32_t)st * P;
+                const uint32_t sh = (uint32_t)st + b;
+                const uint32_t keep = ~(mask | (1u << sh));
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t en = Ts[tp[e]];
+                    tp[e] = (tp[e] & keep) | (en & 0x7fu) | ((en >> 7) << sh);
+                }
+            } else {
+                const uint16_t* Ts = reinterpret_cast<const uint16_t*>(tabs) + (uint32_t)st * P;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) tp[e] = Ts[tp[e]];
+            }
+        }
+        Vec4<T> v;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v.v[e] = xs[tp[e]];
+        const uint32_t j = l0 >> b;
+        uint32_t gp0 = ((g.tlo | (j << lowbits) | g.thi) << b) | (l0 & mask);
+        if (a.out_rot) gp0 = (rotr_group(gp0 >> b, a.out_rot, a.out_S) << b) | (gp0 & mask);
+        *reinterpret_cast<Vec4<T>*>(pout + gp0) = v;
+    }
+}
+
+// a.ws_walkers threads walk (a multiple of 32), the rest draw; QPT is unused (runtime
+// loops over the quads); needs M >= 4 and the bulk-copy path (M * sizeof(T) >= 16)
+template <typename T, int TB, bool DBG, int QPT>
+__global__ void __launch_bounds__(1024, 1) k_stages_ws(const __grid_constant__ StageArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t k = a.k, P = a.P;
+    const uint32_t ntiles = (uint32_t)(a.N / P);
+    const uint32_t stb = (P * (uint32_t)sizeof(T) + 15u) & ~15u;
+    const uint32_t ttb = (k * P * TB + 15u) & ~15u;
+    unsigned char* tab0 = smem + 2u * stb;
+    uint32_t* th0 = reinterpret_cast<uint32_t*>(tab0 + 2u * ttb);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(th0 + (2u << k));
+    uint64_t* st_full = bars;        // [2]
+    uint64_t* tab_full = bars + 2;   // [2]
+    uint64_t* slot_free = bars + 4;  // [2]
+    auto xbuf = [&](uint32_t sl) { return reinterpret_cast<T*>(smem + sl * stb); };
+    auto tbuf = [&](uint32_t sl) { return tab0 + sl * ttb; };
+    auto thbuf = [&](uint32_t sl) { return th0 + (sl << k); };
+
+    const uint32_t t0 = blockIdx.x;
+    if (t0 >= ntiles) return;
+    const uint32_t nt = (ntiles - t0 + gridDim.x - 1u) / gridDim.x;
+    const uint32_t nwalk = a.ws_walkers, ndraw = blockDim.x - nwalk;
+    const bool walker = threadIdx.x < nwalk;
+    const uint32_t rt = walker ? threadIdx.x : threadIdx.x - nwalk;  // thread index within the role
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(st_full + i, 1u);
+            mbar_init(tab_full + i, ndraw);
+            mbar_init(slot_free + i, nwalk);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (walker) {
+        // the first two tiles' states
+        for (uint32_t i = 0; i < 2u && i < nt; ++i)
+            stage_states_load<T>(a, stage_tile_geom(a, t0 + i * gridDim.x), xbuf(i), st_full + i);
+        for (uint32_t i = 0; i < nt; ++i) {
+            const uint32_t sl = i & 1u, par = (i >> 1) & 1u;
+            mbar_wait(st_full + sl, par);
+            mbar_wait(tab_full + sl, par);
+            ws_walk<T, TB>(a, stage_tile_geom(a, t0 + i * gridDim.x), xbuf(sl), tbuf(sl), rt, nwalk);
+            mbar_arrive(slot_free + sl);
+            if (i + 2u < nt && threadIdx.x < 32u) {  // refill the slot once every walker has left it
+                mbar_wait(slot_free + sl, par);
+                stage_states_load<T>(a, stage_tile_geom(a, t0 + (i + 2u) * gridDim.x), xbuf(sl), st_full + sl);
+            }
+        }
+    } else {
+        for (uint32_t i = 0; i < nt; ++i) {
+            const uint32_t sl = i & 1u, par = (i >> 1) & 1u;
+            if (i >= 2u) mbar_wait(slot_free + sl, par ^ 1u);  // tile i-2 walked
+            const StageTile g = stage_tile_geom(a, t0 + i * gridDim.x);
+            {  // this tile's thresholds (drawers only)
+                const uint32_t E = (1u << k) - 1u;
+                uint32_t* ths = thbuf(sl);
+                for (uint32_t e = rt; e < E; e += ndraw) {
+                    const uint32_t u = (1u << k) - e;
+                    const uint32_t st = k - (32u - __clz(u - 1u));
+                    const uint32_t off = (1u << k) - (1u << (k - st));
+                    const uint32_t s = a.s0 + st;
+                    ths[e] = __ldg(a.thr + level_offset(a.m, (int)s) + (g.thi >> s) + (e - off));
+                }
+                named_bar_sync(1u, ndraw);
+            }
+            ws_draws<TB, DBG>(a, g, thbuf(sl), tbuf(sl), rt, ndraw);
+            mbar_arrive(tab_full + sl);
+        }
+    }
+}
+
 }  // namespace pfk

@@ -9,6 +9,10 @@
 //   D5: D0 with the shifted group bases pinned in registers (the compiler otherwise sinks
 //       the shift below the select) and PRMT packing
 //   D6: byte entries (side << 7 | index), PRMT packing
+//   D7: 16-bit entries, side from the SIGN of (r >> b) - P (exact: both < 2^31), the sign
+//       replicated over each halfword by PRMT's sign-extension, entries assembled by LOP3
+//       two at a time
+//   D8: byte entries with the same sign trick
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o draw_bench draw_bench.cu
 #include <cstdint>
 #include <cstdio>
@@ -52,6 +56,25 @@ __device__ __forceinline__ uint2 draw(const uint4 blk, uint32_t Praw, uint32_t j
         for (int e = 0; e < 4; ++e) en[e] = (rw[e] & mask) | (((rw[e] >> b) >= Praw) ? 0x80u : 0u);
         const uint32_t w = __byte_perm(__byte_perm(en[0], en[1], 0x0040u), __byte_perm(en[2], en[3], 0x0040u), 0x5410u);
         return make_uint2(w, 0u);
+    } else if constexpr (V == 7) {
+        const uint32_t blo = (j & ~bit) << b, bitb = bit << b;
+        const uint32_t blo2 = blo | (blo << 16), bitb2 = bitb | (bitb << 16), mask2 = mask | (mask << 16);
+        int32_t dd[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dd[e] = (int32_t)(rw[e] >> b) - (int32_t)Praw;  // < 0: the lower side
+        const uint32_t s01 = __byte_perm((uint32_t)dd[0], (uint32_t)dd[1], 0xFFBBu);  // 0xffff where lower
+        const uint32_t s23 = __byte_perm((uint32_t)dd[2], (uint32_t)dd[3], 0xFFBBu);
+        const uint32_t w01 = __byte_perm(rw[0], rw[1], 0x5410u), w23 = __byte_perm(rw[2], rw[3], 0x5410u);
+        return make_uint2(((w01 & mask2) | blo2) | (~s01 & bitb2), ((w23 & mask2) | blo2) | (~s23 & bitb2));
+    } else if constexpr (V == 8) {
+        int32_t dd[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dd[e] = (int32_t)(rw[e] >> b) - (int32_t)Praw;
+        const uint32_t sg = __byte_perm(__byte_perm((uint32_t)dd[0], (uint32_t)dd[1], 0x00FBu),
+                                        __byte_perm((uint32_t)dd[2], (uint32_t)dd[3], 0x00FBu), 0x5410u);
+        const uint32_t w = __byte_perm(__byte_perm(rw[0], rw[1], 0x0040u), __byte_perm(rw[2], rw[3], 0x0040u), 0x5410u);
+        const uint32_t m4 = mask * 0x01010101u;
+        return make_uint2((w & m4) | (~sg & ~m4), 0u);
     } else if constexpr (V == 2 || V == 4) {
         const uint32_t T = Praw ? (Praw << b) - 1u : 0u;
         const uint32_t blo = (j & ~bit) << b, bitb = bit << b;
@@ -95,7 +118,7 @@ __global__ void __launch_bounds__(1024, 1) bench(const __grid_constant__ KS ks, 
                 *reinterpret_cast<uint2*>(tab + st * P + l0) = draw<V>(b0, ths[(j >> (st + 1)) & 63u], j, st, b);
                 *reinterpret_cast<uint2*>(tab + (st + 1) * P + l0) = draw<V>(b1, ths[(j >> (st + 2)) & 63u], j, st + 1, b);
             }
-        } else if constexpr (V == 6) {
+        } else if constexpr (V == 6 || V == 8) {
 #pragma unroll 1
             for (uint32_t st = 0; st < K; ++st) {
                 const uint4 blk = philox(make_uint4(c0, 7u, (3u << 24) | (st + 2u), 0u), ks);
@@ -113,7 +136,33 @@ __global__ void __launch_bounds__(1024, 1) bench(const __grid_constant__ KS ks, 
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+// exactness of the sign trick against the plain rule, over random words and edge thresholds
+__global__ void check(uint32_t b, uint32_t* bad) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t Ps[6] = {0u, 1u, (1u << (32 - b)) - 1u, 1u << (32 - b), 12345u << (20 - b), t >> b};
+    for (int pi = 0; pi < 6; ++pi) {
+        const uint32_t Pr = Ps[pi] > (1u << (32 - b)) ? (1u << (32 - b)) : Ps[pi];
+        uint4 blk = make_uint4(t * 2654435761u, ~t * 40503u, t ^ 0xdeadbeefu, t | 0xffffff00u);
+        if (t < 4) blk = make_uint4(0xffffffffu, 0u, (Pr << b) - 1u, Pr << b);
+        const uint32_t j = t & 63u, st = t % 6u;
+        const uint2 r0 = draw<0>(blk, Pr, j, st, b), r7 = draw<7>(blk, Pr, j, st, b);
+        const uint2 r6 = draw<6>(blk, Pr, j, st, b), r8 = draw<8>(blk, Pr, j, st, b);
+        if (r0.x != r7.x || r0.y != r7.y) atomicAdd(bad, 1u);
+        const uint32_t m4 = ((1u << b) - 1u) * 0x01010101u | 0x80808080u;
+        if ((r6.x & m4) != (r8.x & m4)) atomicAdd(bad + 1, 1u);
+    }
+}
+
 int main() {
+    {
+        uint32_t* bad;
+        cudaMalloc(&bad, 8);
+        cudaMemset(bad, 0, 8);
+        for (uint32_t b = 1; b <= 7; ++b) check<<<256, 256>>>(b, bad);
+        uint32_t hb[2];
+        cudaMemcpy(hb, bad, 8, cudaMemcpyDeviceToHost);
+        printf("sign-trick exactness: %u (16-bit) / %u (byte) mismatches\n", hb[0], hb[1]);
+    }
     const int blocks = 148, threads = 1024, tiles = 400;
     uint32_t* out;
     cudaMalloc(&out, blocks * threads * 4);
@@ -126,8 +175,9 @@ int main() {
     cudaEventCreate(&a);
     cudaEventCreate(&e);
     const char* names[] = {"D0 shift-compare", "P  Philox only", "D2 (r|mask)>T", "D3 carry on FMA pipe",
-                           "D4 D2 x2 interleaved", "D5 pinned bases+PRMT", "D6 byte entries"};
-    for (int v = 0; v < 7; ++v) {
+                           "D4 D2 x2 interleaved", "D5 pinned bases+PRMT", "D6 byte entries", "D7 sign trick 16-bit",
+                           "D8 sign trick bytes"};
+    for (int v = 0; v < 9; ++v) {
         for (int rep = 0; rep < 3; ++rep) {
             cudaEventRecord(a);
             switch (v) {
@@ -137,7 +187,9 @@ int main() {
                 case 3: bench<3><<<blocks, threads>>>(ks, tiles, 6, out); break;
                 case 4: bench<4><<<blocks, threads>>>(ks, tiles, 6, out); break;
                 case 5: bench<5><<<blocks, threads>>>(ks, tiles, 6, out); break;
-                default: bench<6><<<blocks, threads>>>(ks, tiles, 6, out); break;
+                case 6: bench<6><<<blocks, threads>>>(ks, tiles, 6, out); break;
+                case 7: bench<7><<<blocks, threads>>>(ks, tiles, 6, out); break;
+                default: bench<8><<<blocks, threads>>>(ks, tiles, 6, out); break;
             }
             cudaEventRecord(e);
             cudaEventSynchronize(e);
