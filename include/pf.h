@@ -213,6 +213,16 @@ int pf_init_sharded(const pf_model* model, uint64_t N, uint32_t M, uint64_t seed
 /* Local phase of one step; y as in pf_step (y_host) or pf_step_dev (y_dev): give one. */
 int pf_step_local(pf_handle* h, const float* y_host, const float* y_dev);
 
+/* pf_step_local in two halves, so that the records' all-gather overlaps the local stage
+ * passes: _begin enqueues k_pass1 + k_cascade (after which this shard's record and every
+ * local V level are final: each V_s is sigma(xi_0)-measurable, Lemma facts_about_Vs (a),
+ * PAPER.md:645); _end enqueues the k_stages passes.  pf_shard_record is valid after
+ * _begin; pf_step_top may run before or after _end (it touches only the top tables);
+ * the cross exchange must follow _end.  Sharded handles, plain scheme only.
+ * Errors: PF_EINVAL, PF_EOBS, PF_ESTATE (not sharded; _end without _begin; _begin twice). */
+int pf_step_local_begin(pf_handle* h, const float* y_host, const float* y_dev);
+int pf_step_local_end(pf_handle* h);
+
 /* DEVICE pointer of this shard's record (PF_SHARD_REC_DOUBLES(d) doubles), valid after
  * pf_step_local has run on the stream. */
 int pf_shard_record(pf_handle* h, const double** dev_rec);

@@ -193,7 +193,8 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, uint64
         // quads per thread; needs whole-quad groups (M >= 4), bulk-copied groups and a CTA
         // of 2 x P/4/QPT <= 1024 threads
         if (pipe && env_u32("PF_STAGE_WS", 1u) && M >= 4u && (uint64_t)M * sb >= 16u && sp.P / 4u >= 64u &&
-            stages_smem(sp.P, sb, k, sp.tb, 2u) <= budget) {
+            stages_smem(sp.P, sb, k, sp.tb, 2u) <= budget &&
+            (1u << k) <= std::min<uint32_t>(1024u, sp.P / 4u * 2u) / 2u) {  // one threshold per drawer
             sp.pipe = 2u;
             sp.qpt = 1u;  // unused: runtime loops
             sp.threads = std::min<uint32_t>(1024u, sp.P / 4u * 2u);
@@ -343,6 +344,7 @@ struct pf_handle {
     // peer-memory exchange (pf_peer_open / pf_peer_set / pf_cross_peer)
     std::vector<unsigned char*> peer_ws;    // every rank's workspace, mapped here
     std::vector<void*> peer_ipc;            // IPC mappings to close (allocation bases)
+    bool half_step = false;  // pf_step_local_begin ran, pf_step_local_end pending
     // relabelled exchange in progress (pf_relabel_begin -> pf_relabel_end)
     int rl_t = 0;
     uint64_t rl_own = 0, rl_kmin = 0;
@@ -563,7 +565,7 @@ static void launch_stages_k(pf_handle* h, const StagePass& cp, const void* pin, 
     a.lowbits = cp.s0 - 1;
     a.pipe = cp.pipe;
     // k_stages_ws: walkers = the given fraction (in 32ths) of the CTA, whole warps
-    a.ws_walkers = std::max<uint32_t>(32u, (cp.threads * env_u32("PF_STAGE_WS_WALK32", 10u) / 32u) & ~31u);
+    a.ws_walkers = std::max<uint32_t>(32u, (cp.threads * env_u32("PF_STAGE_WS_WALK32", 12u) / 32u) & ~31u);
     a.out_rot = out_rot;
     a.out_S = h->S;
     a.pin = pin;
@@ -617,6 +619,7 @@ static void fill_pass1(pf_handle* h, Pass1Args& a, const float* y_host, const fl
     a.k1 = p.k1;
     a.P1 = p.P1;
     a.T1 = p.P1 / h->M;
+    a.probe = env_u32("PF_PASS1_PROBE", 0u);
     a.sl = pass1_smem(p.D, p.P1, h->M, p.k1, p.pass1_threads, p.tb);
     a.logV = h->at<double>(h->lay.logV);
     a.thr = h->at<uint32_t>(h->lay.thr);
@@ -882,42 +885,59 @@ static int run_step_multinomial(pf_handle* h, const float* y_host, const float* 
     return check_cuda(h, "pf_step (multinomial)");
 }
 
+// The plain step in two halves (phase bit 1: k_pass1 + k_cascade, after which the shard
+// record and every V level of a sharded handle are final -- Lemma facts_about_Vs (a),
+// so the records' all-gather can overlap bit 2: the k_stages passes).
+static int run_step_plain(pf_handle* h, const float* y_host, const float* y_dev, int phase) {
+    const Plan& p = h->plan;
+    if (phase & 1) {
+        Pass1Args a{};
+        fill_pass1(h, a, y_host, y_dev);
+        const int src = h->cur, dst = h->cur ^ 1;
+        a.x_in = h->X(src);
+        a.x_out = h->X(dst);
+        h->mark(PF_KERNEL_PASS1, true);
+        launch_pass1(h, a);
+        h->mark(PF_KERNEL_PASS1, false);
+        h->mark(PF_KERNEL_CASCADE, true);
+        launch_cascade_k(h);
+        h->mark(PF_KERNEL_CASCADE, false);
+        h->cur = dst;
+        h->half_step = (phase & 2) == 0;
+        h->last_launches = 2;
+        if (h->world > 1) {  // this step's top levels are pending (pf_step_top)
+            h->top_done = false;
+            h->have_step = false;
+        }
+    }
+    if (phase & 2) {
+        // stages k1+1..S: state-moving tile passes
+        int xs = h->cur;
+        for (const StagePass& sp : p.passes) {
+            h->mark(PF_KERNEL_STAGES, true);
+            launch_stages_k(h, sp, h->X(xs), h->X(xs ^ 1));
+            h->mark(PF_KERNEL_STAGES, false);
+            xs ^= 1;
+        }
+        h->cur = xs;
+        h->half_step = false;
+        h->last_launches = (phase & 1 ? 2 : h->last_launches) + (int)p.passes.size();
+        h->sstar_last = (int)h->S;
+        h->step_n = h->n;
+        h->n += 1;
+        if (h->world == 1) {
+            h->have_step = true;
+            h->top_done = true;
+        }
+    }
+    return check_cuda(h, "pf_step");
+}
+
 static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
     if (h->airpf) return run_step_airpf(h, y_host, y_dev);  // AIRPF, or AIRPF2 with theta > 0
     if (h->theta > 0.0) return run_step_adaptive(h, y_host, y_dev);
     if (h->multinomial) return run_step_multinomial(h, y_host, y_dev);
-    const Plan& p = h->plan;
-    Pass1Args a{};
-    fill_pass1(h, a, y_host, y_dev);
-    const int src = h->cur, dst = h->cur ^ 1;
-    a.x_in = h->X(src);
-    a.x_out = h->X(dst);
-    h->mark(PF_KERNEL_PASS1, true);
-    launch_pass1(h, a);
-    h->mark(PF_KERNEL_PASS1, false);
-    int launches = 1;
-    h->mark(PF_KERNEL_CASCADE, true);
-    launch_cascade_k(h);
-    h->mark(PF_KERNEL_CASCADE, false);
-    ++launches;
-
-    // stages k1+1..S: state-moving tile passes
-    int xs = dst;
-    for (const StagePass& sp : p.passes) {
-        h->mark(PF_KERNEL_STAGES, true);
-        launch_stages_k(h, sp, h->X(xs), h->X(xs ^ 1));
-        h->mark(PF_KERNEL_STAGES, false);
-        xs ^= 1;
-        ++launches;
-    }
-    h->cur = xs;
-    h->sstar_last = (int)h->S;
-    h->step_n = h->n;
-    h->n += 1;
-    h->have_step = h->world == 1;
-    h->top_done = h->world == 1;
-    h->last_launches = launches;
-    return check_cuda(h, "pf_step");
+    return run_step_plain(h, y_host, y_dev, 3);
 }
 
 static int dispatch_step(pf_handle* h, const float* yh, const float* yd) { return run_step(h, yh, yd); }
@@ -1055,6 +1075,22 @@ int pf_step_local(pf_handle* h, const float* y_host, const float* y_dev) {
         for (int k = 0; k < h->mp.dy; ++k)
             if (!std::isfinite(y_host[k])) return fail(h, PF_EOBS, "non-finite observation");
     return dispatch_step(h, y_host, y_dev);
+}
+
+int pf_step_local_begin(pf_handle* h, const float* y_host, const float* y_dev) {
+    if (!h || (!y_host && !y_dev)) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
+    if (h->half_step) return fail(h, PF_ESTATE, "pf_step_local_end is pending");
+    if (y_host)
+        for (int k = 0; k < h->mp.dy; ++k)
+            if (!std::isfinite(y_host[k])) return fail(h, PF_EOBS, "non-finite observation");
+    return run_step_plain(h, y_host, y_dev, 1);
+}
+
+int pf_step_local_end(pf_handle* h) {
+    if (!h) return fail(h, PF_EINVAL, "NULL handle");
+    if (!h->half_step) return fail(h, PF_ESTATE, "pf_step_local_begin must run first");
+    return run_step_plain(h, nullptr, nullptr, 2);
 }
 
 int pf_shard_record(pf_handle* h, const double** dev_rec) {

@@ -47,6 +47,7 @@ struct Pass1Args {
     uint64_t N;           // particles of this shard
     uint32_t pos0;        // global index of the shard's first particle (RNG counters)
     uint32_t m, M, b, S, k1, P1, T1;
+    uint32_t probe;       // cost probes of experiment builds (-DPF_PROBES), else unused
     Pass1Smem sl;         // shared-memory layout (pass1_smem)
     const float* x_in;    // xhat_{n-1} (or x_0)
     float* x_out;         // particles moved to their stage-k1 positions

@@ -70,9 +70,26 @@ __device__ __forceinline__ uint32_t xs_swz(uint32_t s) {
 #ifndef PF_KEEPX_MAX
 #define PF_KEEPX_MAX 32
 #endif
+// cost probes (experiment builds with -DPF_PROBES only; a.probe from PF_PASS1_PROBE): bit 0
+// drops the mutation noise (no Philox, no Box-Muller), bit 1 the stage-1 searches, bit 2
+// the stage 2..k1 Philox blocks (identity draws), bit 3 the walk (tile written in place)
+#ifdef PF_PROBES
+#define PF_PROBE(bit) ((a.probe >> (bit)) & 1u)
+#else
+#define PF_PROBE(bit) false
+#endif
+
+#ifndef PF_P1_D4_MAXT  // launch bounds of the fused d = 4 pass (C4 runs it with 128 threads)
+#define PF_P1_D4_MAXT 512
+#define PF_P1_D4_MINB 1
+#endif
+constexpr int pass1_maxt(int D, int MODE) { return (D == 4 && MODE == kPass1Fused) ? PF_P1_D4_MAXT : 512; }
+constexpr int pass1_minb(int D, int MODE) {
+    return (MODE == kPass1Airpf && D >= 4) ? 2 : ((D == 4 && MODE == kPass1Fused) ? PF_P1_D4_MINB : PF_P1_MINB);
+}
 
 template <int D, int KIND, bool DBG, int QPT, int TB, int MODE = kPass1Fused>
-__global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : PF_P1_MINB) k_pass1(const __grid_constant__ Pass1Args a) {
+__global__ void __launch_bounds__(pass1_maxt(D, MODE), pass1_minb(D, MODE)) k_pass1(const __grid_constant__ Pass1Args a) {
     constexpr int PS = 2 + 4 * D;  // partial: max, sw, s1[D], s2[D], p1[D], p2[D]
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t threads = blockDim.x;
@@ -138,6 +155,11 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : PF_
             float z[4 * D];
 #pragma unroll
             for (int j = 0; j < D; ++j) {
+                if (PF_PROBE(0)) {
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) z[4 * j + w] = 0.0f;
+                    continue;
+                }
                 const uint4 blk = rng_block(a.key, ((a.pos0 + i0) >> 2) * D + j, a.n, kDomainMutate, 0u);
                 normals4(blk, z + 4 * j);
             }
@@ -344,7 +366,7 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : PF_
                 tq[it][e] = valid ? u01f(r[e]) * totc : -1.0f;
             }
         }
-        for (uint32_t step = 2u * Z; step >= 1u; step >>= 1) {
+        for (uint32_t step = 2u * Z; step >= 1u && !PF_PROBE(1); step >>= 1) {
 #pragma unroll
             for (int it = 0; it < QPT; ++it)
 #pragma unroll
@@ -451,7 +473,8 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : PF_
             const uint32_t Pq1 = __shfl_sync(kFull, thr[s], (j1 >> s) << (s - 1));
             if (!valid) continue;
             const uint32_t bit = 1u << (s - 1);
-            const uint4 blk = rng_block(a.key, c0t + q, a.n, kDomainResample, (uint32_t)s);
+            const uint4 blk = PF_PROBE(2) ? make_uint4(q, q + 1u, q + 2u, q + 3u)
+                                          : rng_block(a.key, c0t + q, a.n, kDomainResample, (uint32_t)s);
             const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
             uint32_t en[4];
 #pragma unroll
@@ -481,7 +504,7 @@ __global__ void __launch_bounds__(512, (MODE == kPass1Airpf && D >= 4) ? 2 : PF_
         const uint32_t q = tid + it * threads;
         if (q >= nq) continue;
         uint32_t tp[4] = {4u * q, 4u * q + 1u, 4u * q + 2u, 4u * q + 3u};
-        for (uint32_t s = AIR ? 1u : k1; s >= 2u; --s) {  // AIRPF: the within-island draw only
+        for (uint32_t s = AIR ? 1u : k1; s >= 2u && !PF_PROBE(3); --s) {  // AIRPF: the within-island draw only
             const unsigned char* Ts = tab + (s - 2u) * P1 * TB;
             if constexpr (TB == 1) {
                 const uint32_t sh = s - 1u + b;

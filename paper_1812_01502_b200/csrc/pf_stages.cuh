@@ -51,6 +51,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// The same wait with a suspend-time hint: a waiting warp sleeps until the phase completes
+// (or the hint elapses) instead of spinning -- in k_stages_ws the spinning waiters took
+// ~30% of the issued instructions from the working warps (ncu source page)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                      smem_u32(dst)),
@@ -356,45 +366,47 @@ __device__ __forceinline__ void ws_entries(const StageArgs& a, const uint4 blk, 
             make_uint2(__byte_perm(en[0], en[1], 0x5410u), __byte_perm(en[2], en[3], 0x5410u));
 }
 
-// The drawers' share of a tile: the k x P/4 (stage, quad) blocks in flat order f = st P/4 + q
-// (consecutive threads: consecutive quads of one stage), f = rt, rt + nthr, ... -- balanced
-// to one block whatever the drawer count; two blocks per iteration (two independent Philox
-// chains in flight)
+// The drawers' share of a tile: quads rt, rt + nthr, ...; two quads per iteration, their
+// Philox blocks of a stage computed side by side (two independent chains in flight).
+// (Measured against a flat (stage, quad) order balanced to one block per thread: that
+// was 6% slower, profiles/r2_k_stages_ws_variants.txt.)
 template <int TB, bool DBG>
 __device__ __forceinline__ void ws_draws(const StageArgs& a, const StageTile& g, const uint32_t* ths,
                                          unsigned char* tabs, uint32_t rt, uint32_t nthr) {
     const uint32_t b = a.b, k = a.k, nq = a.P >> 2, lowbits = a.lowbits, mask = a.M - 1u;
-    const uint32_t tlo = g.tlo, thi = g.thi, nf = k * nq, lnq = b + k - 2u;  // P / 4 = 2^lnq
-    for (uint32_t f0 = rt; f0 < nf; f0 += 2u * nthr) {
-        const uint32_t f1 = f0 + nthr;
-        const bool two = f1 < nf;
-        uint4 blk[2];
-        uint32_t st[2], l[2], j[2], Pt[2], gp[2];
+    const uint32_t tlo = g.tlo, thi = g.thi;
+    for (uint32_t q0 = rt; q0 < nq; q0 += 2u * nthr) {
+        const uint32_t q1 = q0 + nthr;
+        const bool two = q1 < nq;
+        const uint32_t l0 = 4u * q0, l1 = 4u * (two ? q1 : q0);
+        const uint32_t j0 = l0 >> b, j1 = l1 >> b;
+        const uint32_t gp0 = ((tlo | (j0 << lowbits) | thi) << b) | (l0 & mask);
+        const uint32_t gp1 = ((tlo | (j1 << lowbits) | thi) << b) | (l1 & mask);
+        const uint32_t c0 = (a.pos0 + gp0) >> 2, c1 = (a.pos0 + gp1) >> 2;
+        uint32_t toff = 0;
+        for (uint32_t st = 0; st < k; ++st) {
+            const uint32_t s = a.s0 + st;
+            const uint4 b0 = rng_block(a.key, c0, a.n, kDomainResample, s);
+            const uint4 b1 = rng_block(a.key, c1, a.n, kDomainResample, s);
+            const uint32_t P0 = ths[toff + (j0 >> (st + 1))], P1 = ths[toff + (j1 >> (st + 1))];
+            toff += (1u << k) >> (st + 1);
+            ws_entries<TB>(a, b0, P0, j0, st, tabs, l0);
+            if (two) ws_entries<TB>(a, b1, P1, j1, st, tabs, l1);
+            if constexpr (DBG) {
+                const uint32_t bit = 1u << st;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const uint32_t f = (h == 0 || !two) ? f0 : f1;
-            st[h] = f >> lnq;
-            const uint32_t q = f & (nq - 1u);
-            l[h] = 4u * q;
-            j[h] = l[h] >> b;
-            gp[h] = ((tlo | (j[h] << lowbits) | thi) << b) | (l[h] & mask);
-            blk[h] = rng_block(a.key, (a.pos0 + gp[h]) >> 2, a.n, kDomainResample, a.s0 + st[h]);
-            Pt[h] = ths[(1u << k) - (1u << (k - st[h])) + (j[h] >> (st[h] + 1))];
-        }
-        ws_entries<TB>(a, blk[0], Pt[0], j[0], st[0], tabs, l[0]);
-        if (two) ws_entries<TB>(a, blk[1], Pt[1], j[1], st[1], tabs, l[1]);
-        if constexpr (DBG) {
+                for (int h = 0; h < 2; ++h) {
+                    if (h == 1 && !two) break;
+                    const uint4 bb = h ? b1 : b0;
+                    const uint32_t jj0 = h ? j1 : j0, PP = h ? P1 : P0, gp = h ? gp1 : gp0;
+                    const uint32_t rw[4] = {bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (h == 1 && !two) break;
-                const uint32_t bit = 1u << st[h], s = a.s0 + st[h];
-                const uint32_t rw[4] = {blk[h].x, blk[h].y, blk[h].z, blk[h].w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const bool hi = (rw[e] >> b) >= Pt[h];
-                    const uint32_t jj = hi ? (j[h] | bit) : (j[h] & ~bit);
-                    const uint32_t gsrc = ((tlo | (jj << lowbits) | thi) << b) | (rw[e] & mask);
-                    a.dbg_anc[(uint64_t)(s - 1) * a.N + gp[h] + e] = (int32_t)(a.pos0 + gsrc);
+                    for (int e = 0; e < 4; ++e) {
+                        const bool hi = (rw[e] >> b) >= PP;
+                        const uint32_t jj = hi ? (jj0 | bit) : (jj0 & ~bit);
+                        const uint32_t gsrc = ((tlo | (jj << lowbits) | thi) << b) | (rw[e] & mask);
+                        a.dbg_anc[(uint64_t)(s - 1) * a.N + gp + e] = (int32_t)(a.pos0 + gsrc);
+                    }
                 }
             }
         }
@@ -475,33 +487,35 @@ __global__ void __launch_bounds__(1024, 1) k_stages_ws(const __grid_constant__ S
             stage_states_load<T>(a, stage_tile_geom(a, t0 + i * gridDim.x), xbuf(i), st_full + i);
         for (uint32_t i = 0; i < nt; ++i) {
             const uint32_t sl = i & 1u, par = (i >> 1) & 1u;
-            mbar_wait(st_full + sl, par);
-            mbar_wait(tab_full + sl, par);
+            mbar_wait_sleep(st_full + sl, par);
+            mbar_wait_sleep(tab_full + sl, par);
             ws_walk<T, TB>(a, stage_tile_geom(a, t0 + i * gridDim.x), xbuf(sl), tbuf(sl), rt, nwalk);
             mbar_arrive(slot_free + sl);
             if (i + 2u < nt && threadIdx.x < 32u) {  // refill the slot once every walker has left it
-                mbar_wait(slot_free + sl, par);
+                mbar_wait_sleep(slot_free + sl, par);
                 stage_states_load<T>(a, stage_tile_geom(a, t0 + (i + 2u) * gridDim.x), xbuf(sl), st_full + sl);
             }
         }
     } else {
+        // drawers; tile i+1's thresholds (<= 2^k - 1 entries, one per drawer thread) are
+        // loaded while tile i is drawn and stored into the other threshold slot afterwards
+        const uint32_t E = (1u << k) - 1u;
+        auto thr_of = [&](uint32_t tile_i) -> uint32_t {
+            const StageTile g = stage_tile_geom(a, t0 + tile_i * gridDim.x);
+            const uint32_t e = rt, u = (1u << k) - e;
+            const uint32_t st = k - (32u - __clz(u - 1u));
+            const uint32_t off = (1u << k) - (1u << (k - st));
+            const uint32_t s = a.s0 + st;
+            return __ldg(a.thr + level_offset(a.m, (int)s) + (g.thi >> s) + (e - off));
+        };
+        if (rt < E) thbuf(0)[rt] = thr_of(0);
         for (uint32_t i = 0; i < nt; ++i) {
             const uint32_t sl = i & 1u, par = (i >> 1) & 1u;
-            if (i >= 2u) mbar_wait(slot_free + sl, par ^ 1u);  // tile i-2 walked
-            const StageTile g = stage_tile_geom(a, t0 + i * gridDim.x);
-            {  // this tile's thresholds (drawers only)
-                const uint32_t E = (1u << k) - 1u;
-                uint32_t* ths = thbuf(sl);
-                for (uint32_t e = rt; e < E; e += ndraw) {
-                    const uint32_t u = (1u << k) - e;
-                    const uint32_t st = k - (32u - __clz(u - 1u));
-                    const uint32_t off = (1u << k) - (1u << (k - st));
-                    const uint32_t s = a.s0 + st;
-                    ths[e] = __ldg(a.thr + level_offset(a.m, (int)s) + (g.thi >> s) + (e - off));
-                }
-                named_bar_sync(1u, ndraw);
-            }
-            ws_draws<TB, DBG>(a, g, thbuf(sl), tbuf(sl), rt, ndraw);
+            if (i >= 2u) mbar_wait_sleep(slot_free + sl, par ^ 1u);  // tile i-2 walked
+            named_bar_sync(1u, ndraw);                               // tile i's thresholds stored
+            const uint32_t nxt = (rt < E && i + 1u < nt) ? thr_of(i + 1u) : 0u;  // in flight during the draws
+            ws_draws<TB, DBG>(a, stage_tile_geom(a, t0 + i * gridDim.x), thbuf(sl), tbuf(sl), rt, ndraw);
+            if (rt < E && i + 1u < nt) thbuf(sl ^ 1u)[rt] = nxt;
             mbar_arrive(tab_full + sl);
         }
     }

@@ -183,6 +183,21 @@ class LibBackend:
         off = ptr - self.ws.data_ptr()
         return self.ws[off: off + nbytes].view(dtype)
 
+    def step_local_begin(self, y, y_dev=None):
+        """k_pass1 + k_cascade: returns this shard's record (final after these two)."""
+        if y_dev is None:
+            yy = np.ascontiguousarray(y, dtype=np.float32)
+            self.pf._check(self.pf.lib().pf_step_local_begin(self.h, yy.ctypes.data, None), self.h)
+        else:
+            self.pf._check(self.pf.lib().pf_step_local_begin(self.h, None, y_dev.data_ptr()), self.h)
+        p = ctypes.c_void_p()
+        self.pf._check(self.pf.lib().pf_shard_record(self.h, ctypes.byref(p)), self.h)
+        return self._view(int(p.value), 8 * self.rec_len, self.torch.float64)
+
+    def step_local_end(self):
+        """The local k_stages passes."""
+        self.pf._check(self.pf.lib().pf_step_local_end(self.h), self.h)
+
     def step_local(self, y):
         yy = np.ascontiguousarray(y, dtype=np.float32)
         self.pf._check(self.pf.lib().pf_step_local(self.h, yy.ctypes.data, None), self.h)
@@ -328,8 +343,11 @@ def sharded_step(backend, transport, y, y_dev=None, exchange: str = "pairwise") 
     the states each rank's outputs read) or "peer" (one kernel reads them straight from
     the owners' memory over NVLink; peer_connect first)."""
     with _on_stream(backend):  # every transport call is ordered on the backend's stream
-        rec = backend.step_local(y) if y_dev is None else backend.step_local_dev(y_dev)
-        backend.step_top(transport.allgather(rec))
+        if hasattr(backend, "step_local_begin") and getattr(transport, "nccl", False):
+            _local_overlapped(backend, transport, y, y_dev)
+        else:
+            rec = backend.step_local(y) if y_dev is None else backend.step_local_dev(y_dev)
+            backend.step_top(transport.allgather(rec))
         if exchange == "peer":
             peer_exchange(backend, transport)
             return
@@ -345,6 +363,29 @@ def sharded_step(backend, transport, y, y_dev=None, exchange: str = "pairwise") 
             buf = backend.cross_buffer()
             recv = transport.exchange(buf, partner(transport.rank, t))
             backend.cross_stage(t, recv)
+
+
+def _local_overlapped(backend, transport, y, y_dev=None) -> None:
+    """The local phase with the records' all-gather off the critical path: after k_pass1 +
+    k_cascade the record is final (every V_s is sigma(xi_0)-measurable, Lemma
+    facts_about_Vs (a)), so the NCCL all-gather runs on a side stream while
+    the k_stages passes run on the backend's; k_top waits for both (stream events)."""
+    import torch
+    main = backend.stream
+    rec = backend.step_local_begin(y, y_dev)
+    if not hasattr(backend, "_comm"):
+        backend._comm = torch.cuda.Stream(device=rec.device)
+        backend._ev = (torch.cuda.Event(), torch.cuda.Event())
+    comm, (ev_rec, ev_gather) = backend._comm, backend._ev
+    ev_rec.record(main)
+    with torch.cuda.stream(comm):
+        comm.wait_event(ev_rec)
+        allr = transport.allgather(rec)
+        ev_gather.record(comm)
+    backend.step_local_end()            # the stage passes, concurrent with the all-gather
+    main.wait_event(ev_gather)
+    allr.record_stream(main)
+    backend.step_top(allr)
 
 
 def _on_stream(backend):

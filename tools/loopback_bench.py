@@ -1,7 +1,9 @@
 """Projection of the sharded step on one GPU: G shards of a configuration run back to back
 through the loopback transport (python tools/loopback_bench.py C4 8 [pull|pairwise|peer] [steps]).
 Reports the device time per step summed over the shards, per kernel kind, and the bytes the
-exchange would move between GPUs; a projection only (no NVLink, shards serialised)."""
+exchange would move between GPUs; a projection only (no NVLink, shards serialised).
+Modes: pull, pairwise, peer, relabel (the relabelled exchange: only the surplus crosses; its
+bytes are counted from the surplus every shard received)."""
 import os
 import sys
 import time
@@ -41,10 +43,19 @@ for b in shards:
         a[1] += c
 state = 4 * cfg.d
 moved = cfg.N * state * (1 - 1 / G) / G  # per rank, pull: states read from other shards
+if mode == "relabel":
+    sur = np.stack([b.surplus for b in shards], axis=1)  # L x G states received (last step)
+    moved = float(sur.sum(axis=0).max()) * state           # the busiest rank
+    print(f"relabel surplus per stage and rank (states): {sur.tolist()}; sqrt(N/G) = {np.sqrt(cfg.N / G):.0f}")
 print(f"{name} G={G} {mode}: {ms:.3f} ms per step for all {G} shards on one GPU "
       f"({ms / G:.3f} ms per shard); per kernel kind (ms per step, all shards): "
       + ", ".join(f"{k} {v[0]:.3f}" for k, v in kt.items() if v[1]))
 print(f"exchange per rank per step: pull ~{moved / 1e9:.3f} GB states + {cfg.N / G * (1 - 1 / G) * 4 / 1e9:.3f} GB requests; "
       f"pairwise {G.bit_length() - 1} x {cfg.N / G * state / 1e9:.3f} GB")
+nvl = 770.0e9  # B200_PROFILING.md: measured peer copy per direction per GPU
+local = ms / G
+print(f"projection per rank: {local:.3f} ms of kernels + {moved / nvl * 1e3:.3f} ms NVLink ({moved / 1e9:.3f} GB at "
+      f"770 GB/s) = {local + moved / nvl * 1e3:.3f} ms without overlap, {max(local, moved / nvl * 1e3):.3f} ms with "
+      f"full overlap")
 for b in shards:
     b.close()
