@@ -289,6 +289,24 @@ int pf_peer_open(pf_handle* h, const void* ipc_handles, const uint64_t* offsets)
 int pf_peer_set(pf_handle* h, const uint64_t* dev_workspaces);
 int pf_cross_peer(pf_handle* h);
 
+/* Sharded AIRPF (Alg. 4 over G GPUs with whole-block moves; reading R27): a
+ * handle created with PF_FLAG_AIRPF on world > 1 (m / world a multiple of 4) runs, in
+ * pf_step_local, the AIRPF pass (its island blocks read from their owners through the
+ * peer mapping: pf_peer_open / pf_peer_set first), the cascade and the local island
+ * stages; after pf_step_top (31-bit island thresholds), every cross island stage t = 1..L
+ * exchanges the island maps with partner rank ^ 2^{t-1}:
+ *   pf_island_map(h, &map)           DEVICE, m / world int32: this shard's island map
+ *                                    (global block ids; send it to the partner)
+ *   pf_island_cross(h, t, partner)   DEVICE, the partner's map: island i takes the partner
+ *                                    island's entry when it draws the partner's side, except
+ *                                    a pure exchange under Alg. 7 (mode 1)
+ * Only block ids move; the states cross NVLink once, when the next step reads a remote
+ * block (a contiguous M x d run).  Bitwise the one-GPU AIRPF step (global counters and
+ * the one-GPU operand order).  Errors: PF_EINVAL, PF_ESTATE (not sharded, no AIRPF step,
+ * before pf_step_top), PF_ECUDA. */
+int pf_island_map(pf_handle* h, const int32_t** dev_map);
+int pf_island_cross(pf_handle* h, int t, const int32_t* dev_partner_map);
+
 /* Relabelled exchange of cross stage t (1..L), the BPF variant of SURVEY.md §8(f)3 (the
  * count-imbalance / surplus sketch of PAPER.md:826-850; reading R24).  Every
  * output first takes its Alg. 3 draw of stage s = S_loc + t (pairing shard r with

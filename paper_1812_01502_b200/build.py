@@ -37,7 +37,7 @@ def sources():
 # is the default one
 VARIANT = os.environ.get("PF_BUILD_VARIANT", "")
 if VARIANT:
-    OBJ = os.path.join(HERE, "build_obj_" + VARIANT)
+    OBJ = os.path.join("/tmp", "pf_build_obj_" + VARIANT)  # outside the repo (not pushed to GPU boxes)
     LIB = os.path.join(HERE, f"libpf_{VARIANT}.so")
     NVCC_FLAGS = NVCC_FLAGS + os.environ.get("PF_BUILD_DEFINES", "").split()
 

@@ -86,14 +86,17 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, uint64
     Plan p;
     p.D = d;
     const uint32_t budget1 = env_u32("PF_PASS1_SMEM", d == 4 ? kPass1SmemBudgetD4 : kPass1SmemBudgetDefault);
-    const uint32_t threads1 = env_u32("PF_PASS1_THREADS", d == 4 ? kPass1ThreadsD4 : kPass1ThreadsDefault);
+    uint32_t threads1 = env_u32("PF_PASS1_THREADS", d == 4 ? kPass1ThreadsD4 : kPass1ThreadsDefault);
+    if (d == 4) threads1 = std::min(threads1, kPass1ThreadsD4);  // the d = 4 fused kernel's launch bounds
     const uint32_t maxqpt1 = env_u32("PF_PASS1_MAXQPT", 8u);
     // pass-1 tile: the largest 2^k1 <= 64 groups (k1 <= S) whose shared memory fits the budget
     uint32_t P1 = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(N, (uint64_t)kPass1MaxGroups * M),
                                                std::max<uint64_t>(2ull * M, Nglobal / kMaxShards));
+    const uint32_t maxthr1 = d == 4 ? kPass1ThreadsD4 : 512u;  // the kernels' launch bounds
     auto threads_for = [&](uint32_t P, uint32_t* q) {
-        uint32_t t = pick_threads(P / 4, threads1, q);
-        while (*q > maxqpt1 && t < 512u) {  // k_pass1 is instantiated for up to 8 quads per thread
+        uint32_t t = std::min(pick_threads(P / 4, threads1, q), maxthr1);
+        *q = std::max(1u, (P / 4) / t);
+        while (*q > maxqpt1 && t < maxthr1) {  // k_pass1 is instantiated for up to 8 quads per thread
             t *= 2;
             *q /= 2;
         }
@@ -104,7 +107,7 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, uint64
         uint32_t q;
         const uint32_t thr = threads_for(P, &q);
         if (tb == 1u && M > 128u) return false;
-        return thr <= 512u && pass1_smem(d, P, M, (uint32_t)ilog2_exact(P / M), thr, tb).total <= budget1;
+        return thr <= maxthr1 && q <= maxqpt1 && pass1_smem(d, P, M, (uint32_t)ilog2_exact(P / M), thr, tb).total <= budget1;
     };
     p.tb = M <= 128u ? 1u : 2u;
     for (;;) {
@@ -127,8 +130,8 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, uint64
         return false;
     }
     p.pass1_threads = threads_for(P1, &p.pass1_qpt);
-    if (p.pass1_threads > 512u) {
-        *err = "pass-1 tile needs more than 512 threads";
+    if (p.pass1_threads > maxthr1 || p.pass1_qpt > maxqpt1) {
+        *err = "pass-1 tile needs more threads than its kernel's launch bounds";
         return false;
     }
     p.pass1_smem = pass1_smem(d, P1, M, p.k1, p.pass1_threads, p.tb).total;
@@ -281,7 +284,7 @@ Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags, uint32
     L.mn_off = take(mn ? (nt_mn + 1) * 8 : 0);
     const bool air = flags & PF_FLAG_AIRPF;
     L.isl_A = take(air ? m * 4 : 0);
-    L.isl_choice = take(air ? (size_t)S * ((m + 3) / 4) : 0);
+    L.isl_choice = take(air ? (size_t)Sglobal * ((m + 3) / 4) : 0);  // sharded: the cross stages too
     L.isl_logW = take(air ? m * 8 : 0);
     const bool dbg = flags & PF_FLAG_DEBUG;
     L.dbg_x = take(dbg ? xb : 0);
@@ -547,7 +550,11 @@ static void launch_cascade_k(pf_handle* h) {
     c.b = h->airpf ? 1u : h->b;  // AIRPF: 31-bit island thresholds (R20)
     c.NT = p.NT;
     c.LPC = p.LPC;
-    launch_cascade(p.D, LaunchCfg{p.cascade_grid, (uint32_t)kCascadeThreads, 0u, h->stream}, c);
+    // threads: half the widest tree level the kernel builds (its leaves per CTA, or the CTA
+    // roots of the last CTA), at least 64 (per-thread copies of a partial)
+    uint32_t wide = std::max(p.LPC, p.cascade_grid), thr = 64;  // >= the partial size 2 + 4 d
+    while (thr < 1024u && 2u * thr < wide) thr *= 2;
+    launch_cascade(p.D, LaunchCfg{p.cascade_grid, thr, 0u, h->stream}, c);
 }
 
 static void launch_stages_k(pf_handle* h, const StagePass& cp, const void* pin, void* pout, uint32_t out_rot = 0u) {
@@ -758,6 +765,12 @@ static int run_step_airpf(pf_handle* h, const float* y_host, const float* y_dev)
     a.x_out = h->X(h->cur ^ 1);
     a.isl_src = h->isl_valid ? h->at<int32_t>(h->lay.isl_A) : nullptr;
     a.logW = h->at<double>(h->lay.isl_logW);
+    if (h->world > 1 && h->isl_valid) {  // sharded (R27): the blocks live on their owners
+        if (h->peer_ws.size() != h->world) return fail(h, PF_ESTATE, "sharded AIRPF needs the peer mapping (pf_peer_open/set)");
+        const size_t xoff = h->cur ? h->lay.X1 : h->lay.X0;  // same layout on every rank
+        for (uint32_t r = 0; r < h->world; ++r) a.xpeer[r] = reinterpret_cast<const float*>(h->peer_ws[r] + xoff);
+        a.peer_shift = h->S;  // m / world = 2^S_loc islands per rank
+    }
     // d >= 4: no stage tables in AIRPF mode; the smaller footprint (with <= 64 registers,
     // launch bounds of kPass1Airpf) fits 8 CTAs per SM (C4: 4.79 -> 4.42 ms per pass; the
     // same change measured slower for d = 1)
@@ -805,7 +818,8 @@ static int run_step_airpf(pf_handle* h, const float* y_host, const float* y_dev)
     ia.key = make_key(h->seed);
     ia.n = h->n;
     ia.m = h->m;
-    ia.S = ss;  // island stages 1..S* (all S unless AIRPF2 stops early)
+    ia.S = ss;  // island stages 1..S* (all S unless AIRPF2 stops early; sharded: the local ones)
+    ia.island0 = h->pos0 >> h->b;
     ia.modified = h->airpf == 1;
     ia.thr = h->at<uint32_t>(h->lay.thr);
     ia.choice = h->at<uint8_t>(h->lay.isl_choice);
@@ -834,8 +848,8 @@ static int run_step_airpf(pf_handle* h, const float* y_host, const float* y_dev)
     h->sstar_last = (int)ss;
     h->step_n = h->n;
     h->n += 1;
-    h->have_step = true;
-    h->top_done = true;
+    h->have_step = h->world == 1;  // sharded: pf_step_top and the cross island stages follow
+    h->top_done = h->world == 1;
     h->last_launches = launches;
     return check_cuda(h, "pf_step (AIRPF)");
 }
@@ -980,8 +994,9 @@ static int init_core(const pf_model* model, uint64_t N, uint32_t M, uint64_t see
     if (!shard_geometry(N, M, rank, world, &Nloc, &err)) return fail(nullptr, PF_EINVAL, err);
     if ((flags & PF_FLAG_ADAPTIVE) && world != 1) return fail(nullptr, PF_EINVAL, "PF_FLAG_ADAPTIVE needs world = 1");
     if ((flags & PF_FLAG_MULTINOMIAL) && world != 1) return fail(nullptr, PF_EINVAL, "PF_FLAG_MULTINOMIAL needs world = 1");
-    if ((flags & PF_FLAG_AIRPF) && (world != 1 || M < 4u))
-        return fail(nullptr, PF_EINVAL, "PF_FLAG_AIRPF needs world = 1 and M >= 4");
+    if ((flags & PF_FLAG_AIRPF) && (M < 4u || (world > 1 && ((N / M / (uint64_t)world) % 4u != 0 ||
+                                                           (flags & PF_FLAG_ADAPTIVE)))))
+        return fail(nullptr, PF_EINVAL, "PF_FLAG_AIRPF needs M >= 4; sharded: m / world a multiple of 4, no adaptive");
     Plan p;
     int nsm = 148, dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
@@ -1112,7 +1127,7 @@ int pf_step_top(pf_handle* h, const double* dev_all_recs) {
     t.Nglobal = h->Nglobal;
     t.G = h->world;
     t.L = h->L;
-    t.b = h->b;
+    t.b = h->airpf ? 1u : h->b;  // AIRPF: 31-bit island thresholds (R20)
     h->mark(PF_KERNEL_TOP, true);
     launch_top(h->plan.D, LaunchCfg{1u, 1024u, 0u, h->stream}, t);
     h->mark(PF_KERNEL_TOP, false);
@@ -1396,6 +1411,39 @@ int pf_relabel_end(pf_handle* h, int t, const void* dev_recv) {
     return check_cuda(h, "pf_relabel_end");
 }
 
+// ---- sharded AIRPF: the cross island stages (include/pf.h; reading R27) ------
+int pf_island_map(pf_handle* h, const int32_t** dev_map) {
+    if (!h || !dev_map) return fail(h, PF_EINVAL, "NULL argument");
+    if (!h->airpf || !h->isl_valid) return fail(h, PF_ESTATE, "no AIRPF step");
+    *dev_map = h->at<int32_t>(h->lay.isl_A);
+    return PF_OK;
+}
+
+int pf_island_cross(pf_handle* h, int t, const int32_t* dev_partner_map) {
+    if (!h || !dev_partner_map) return fail(h, PF_EINVAL, "NULL argument");
+    if (h->world < 2) return fail(h, PF_ESTATE, "not a sharded handle");
+    if (!h->airpf || !h->isl_valid) return fail(h, PF_ESTATE, "no AIRPF step");
+    if (t < 1 || (uint32_t)t > h->L) return fail(h, PF_EINVAL, "cross stage out of range");
+    if (!h->top_done) return fail(h, PF_ESTATE, "pf_step_top must run first");
+    IslandCrossArgs c{};
+    c.key = make_key(h->seed);
+    c.n = h->step_n;
+    c.s = h->S + (uint32_t)t;
+    c.m = h->m;
+    c.island0 = h->pos0 >> h->b;
+    c.rank = h->rank;
+    c.t = (uint32_t)t;
+    c.modified = h->airpf == 1;
+    c.thr = h->at<uint32_t>(h->lay.top_thr) + (h->world - (h->world >> (t - 1))) + (h->rank >> t);
+    c.A = h->at<int32_t>(h->lay.isl_A);
+    c.Apar = dev_partner_map;
+    c.choice = h->at<uint8_t>(h->lay.isl_choice) + (size_t)(c.s - 1) * ((h->m + 3) / 4);
+    h->mark(PF_KERNEL_CROSS, true);
+    launch_island_cross(h->stream, c);
+    h->mark(PF_KERNEL_CROSS, false);
+    return check_cuda(h, "pf_island_cross");
+}
+
 int pf_guard_check(pf_handle* h, unsigned char fill, uint64_t* bad_bytes) {
     if (!h || !bad_bytes) return fail(h, PF_EINVAL, "NULL argument");
     if (!(h->flags & PF_FLAG_GUARD)) return fail(h, PF_ESTATE, "handle not created with PF_FLAG_GUARD");
@@ -1452,7 +1500,15 @@ int pf_estimate(pf_handle* h, int phi, int kind, double* out) {
         double* part = h->at<double>(h->lay.mom_part);
         double* res = h->at<double>(h->lay.mom_out);
         const int32_t* isl = (h->airpf && h->isl_valid) ? h->at<int32_t>(h->lay.isl_A) : nullptr;
-        launch_moments(h->stream, D, h->X(h->cur), isl, h->b, h->N, part, res);
+        const float* xs = h->X(h->cur);
+        if (isl && h->world > 1) {  // sharded AIRPF: the blocks live on their owners (R27)
+            void* xm = nullptr;
+            const int rc = pf_debug_ptr(h, PF_DBG_XHAT, 0, &xm);
+            if (rc != PF_OK) return rc;
+            xs = static_cast<const float*>(xm);
+            isl = nullptr;
+        }
+        launch_moments(h->stream, D, xs, isl, h->b, h->N, part, res);
         const int rc = check_cuda(h, "pf_estimate (resampled)");
         if (rc != PF_OK) return rc;
         src = res + (phi == PF_PHI_X ? 0 : D);
@@ -1537,8 +1593,17 @@ int pf_debug_ptr(pf_handle* h, int what, int stage, void** dev_out) {
         }
         case PF_DBG_XHAT:
             if (h->airpf && h->isl_valid) {  // materialise x_hat = the island blocks (into the free buffer)
-                launch_block_gather(h->stream, h->X(h->cur), h->X(h->cur ^ 1), h->at<int32_t>(h->lay.isl_A), h->N, h->b,
-                                    (uint32_t)D);
+                if (h->world > 1) {  // sharded (R27): blocks from their owners
+                    if (h->peer_ws.size() != h->world) return fail(h, PF_ESTATE, "no peer mapping");
+                    PeerArgs pa{};
+                    const size_t xoff = h->cur ? h->lay.X1 : h->lay.X0;
+                    for (uint32_t r = 0; r < h->world; ++r) pa.x[r] = reinterpret_cast<const float*>(h->peer_ws[r] + xoff);
+                    launch_block_gather_peer(h->stream, pa, h->X(h->cur ^ 1), h->at<int32_t>(h->lay.isl_A), h->N, h->b,
+                                             (uint32_t)D, h->S);
+                } else {
+                    launch_block_gather(h->stream, h->X(h->cur), h->X(h->cur ^ 1), h->at<int32_t>(h->lay.isl_A), h->N,
+                                        h->b, (uint32_t)D);
+                }
                 *dev_out = h->X(h->cur ^ 1);
                 return check_cuda(h, "pf_debug_ptr");
             }
@@ -1551,7 +1616,7 @@ int pf_debug_ptr(pf_handle* h, int what, int stage, void** dev_out) {
             if (what == PF_DBG_ISLAND_A) *dev_out = h->at<int32_t>(h->lay.isl_A);
             else if (what == PF_DBG_ISLAND_LOGW) *dev_out = h->at<double>(h->lay.isl_logW);
             else {
-                if (stage < 1 || stage > (int)h->S) return fail(h, PF_EINVAL, "stage out of range");
+                if (stage < 1 || stage > (int)h->Sglobal) return fail(h, PF_EINVAL, "stage out of range");
                 *dev_out = h->at<uint8_t>(h->lay.isl_choice) + (size_t)(stage - 1) * ((h->m + 3) / 4);
             }
             return PF_OK;
@@ -1612,8 +1677,9 @@ int pf_set_airpf(pf_handle* h, int mode) {
     if (h->airpf != mode && h->carry_mode != 0)  // carried weights belong to the scheme that made them
         return fail(h, PF_ESTATE, "particles carry weights of an early-stopped step: run one step with theta = 1 first");
     if (!mode && h->isl_valid) {  // back to augmented resampling: materialise x_hat first
-        launch_block_gather(h->stream, h->X(h->cur), h->X(h->cur ^ 1), h->at<int32_t>(h->lay.isl_A), h->N, h->b,
-                            (uint32_t)h->plan.D);
+        void* xm = nullptr;
+        const int rc = pf_debug_ptr(h, PF_DBG_XHAT, 0, &xm);  // into X(cur ^ 1), from the owners when sharded
+        if (rc != PF_OK) return rc;
         h->cur ^= 1;
         h->isl_valid = false;
     }

@@ -50,6 +50,11 @@ struct Pass1Args {
     uint32_t probe;       // cost probes of experiment builds (-DPF_PROBES), else unused
     Pass1Smem sl;         // shared-memory layout (pass1_smem)
     const float* x_in;    // xhat_{n-1} (or x_0)
+    // sharded AIRPF (R27): island g reads global block isl_src[g] from its owner's state
+    // buffer, owner = block >> peer_shift (peer-mapped pointers, kPass1PeerMax ranks);
+    // xpeer[0] == nullptr: one GPU (x_in)
+    const float* xpeer[64];
+    uint32_t peer_shift;
     float* x_out;         // particles moved to their stage-k1 positions
     double* logV;         // level table (m - 1)
     uint32_t* thr;        // threshold table (m - 1)
@@ -180,11 +185,25 @@ __host__ __device__ inline uint32_t ess_chunks_total(const EssArgs& a) {
 
 struct IslandArgs {
     Key key;
-    uint32_t n, m, S;
+    uint32_t n, m, S;      // m: islands of this shard; S: the stages to draw (local ones when sharded)
+    uint32_t island0;      // global index of the shard's first island (draw counters, map values)
     int modified;
     const uint32_t* thr;   // side thresholds, level-table layout (stage s at level_offset(m, s))
     uint8_t* choice;       // S x nq nibbles (nq = ceil(m / 4))
     int32_t* A;            // m: island map
+};
+
+// Cross island stage t of a sharded AIRPF step (R27): island i of this shard (global
+// island0 + i) and island i of the partner shard rank ^ 2^{t-1} draw their sides with the
+// top threshold; Alg. 7's rule sees both draws; A_own[i] <- A_par[i] when i takes.
+struct IslandCrossArgs {
+    Key key;
+    uint32_t n, s, m, island0, rank, t;
+    int modified;
+    const uint32_t* thr;   // the stage's top threshold (31-bit, R20)
+    int32_t* A;            // this shard's island map (global block ids), updated in place
+    const int32_t* Apar;   // the partner's map
+    uint8_t* choice;       // the stage's choice nibbles (debug table row) or nullptr
 };
 
 constexpr uint32_t kMnTile = 1024;  // particles per CDF tile (one CTA of 1024 threads)

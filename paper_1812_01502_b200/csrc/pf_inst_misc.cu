@@ -95,7 +95,7 @@ __global__ void k_ess_final(const __grid_constant__ EssArgs a) {
 // Side draws of the four islands of quad c4 at stage s: bit e set = island 4 c4 + e takes
 // its partner's block (before Alg. 7's exchange rule).
 __device__ __forceinline__ uint32_t island_takes(const IslandArgs& a, uint32_t c4, uint32_t s) {
-    const uint4 blk = rng_block(a.key, c4, a.n, kDomainIsland, s);
+    const uint4 blk = rng_block(a.key, (a.island0 >> 2) + c4, a.n, kDomainIsland, s);  // global island quad
     const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
     const uint32_t bit = 1u << (s - 1);
     uint32_t take = 0u;
@@ -159,13 +159,56 @@ __global__ void __launch_bounds__(256) k_island_compose(const __grid_constant__ 
         const uint32_t take = (__ldg(a.choice + (uint64_t)(s - 1) * nq + (c >> 2)) >> (c & 3u)) & 1u;
         c ^= take << (s - 1);
     }
-    a.A[g] = (int32_t)c;
+    a.A[g] = (int32_t)(a.island0 + c);
 }
 
 void launch_island(cudaStream_t st, const IslandArgs& a) {
     const uint64_t work = (uint64_t)((a.m + 3u) >> 2) * a.S;
     if (work) k_island_draw<<<(uint32_t)((work + 255) / 256), 256, 0, st>>>(a);  // S* = 0 (AIRPF2): no stage
     k_island_compose<<<(a.m + 255) / 256, 256, 0, st>>>(a);
+}
+
+// Cross island stage (sharded AIRPF, R27): thread per quad of this shard's islands.
+__global__ void __launch_bounds__(256) k_island_cross(const __grid_constant__ IslandCrossArgs a) {
+    const uint32_t c4 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (4u * c4 >= a.m) return;
+    const uint32_t P = __ldg(a.thr), bit = 1u << (a.s - 1);
+    const uint32_t g0 = a.island0 + 4u * c4;                      // global islands g0..g0+3
+    const uint4 bo = rng_block(a.key, g0 >> 2, a.n, kDomainIsland, a.s);
+    const uint4 bp = rng_block(a.key, (g0 ^ bit) >> 2, a.n, kDomainIsland, a.s);  // the partners' quad
+    const uint32_t ro[4] = {bo.x, bo.y, bo.z, bo.w}, rp[4] = {bp.x, bp.y, bp.z, bp.w};
+    const bool own_low = (g0 & bit) == 0u;
+    uint32_t take = 0u;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const bool to = ((ro[e] >> 1) < P) != own_low;   // island g0+e takes its partner's block
+        const bool tp = ((rp[e] >> 1) < P) != !own_low;  // the partner takes g0+e's block
+        if (to && !(a.modified && tp)) take |= 1u << e;  // Alg. 7: a pure exchange is undone
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+        if ((take >> e) & 1u) a.A[4u * c4 + e] = a.Apar[4u * c4 + e];
+    if (a.choice) a.choice[c4] = (uint8_t)take;
+}
+
+void launch_island_cross(cudaStream_t st, const IslandCrossArgs& a) {
+    k_island_cross<<<((a.m + 3u) / 4u + 255u) / 256u, 256, 0, st>>>(a);
+}
+
+// x_hat of a sharded AIRPF step for the debug interface: local block g = owner's block.
+__global__ void k_block_gather_peer(const PeerArgs p, float* out, const int32_t* A, uint64_t N, uint32_t b, uint32_t D,
+                                    uint32_t shift) {
+    for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < N * D; f += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = f / D, k = f % D;
+        const uint32_t gb = (uint32_t)A[i >> b];
+        const uint64_t src = ((uint64_t)(gb & ((1u << shift) - 1u)) << b) | (i & ((1ull << b) - 1ull));
+        out[f] = p.x[gb >> shift][src * D + k];
+    }
+}
+
+void launch_block_gather_peer(cudaStream_t st, const PeerArgs& p, float* out, const int32_t* A, uint64_t N, uint32_t b,
+                              uint32_t D, uint32_t shift) {
+    k_block_gather_peer<<<1184, 256, 0, st>>>(p, out, A, N, b, D, shift);
 }
 
 // x_hat of an AIRPF step for the debug interface: out[g M + j] = in[A[g] M + j].

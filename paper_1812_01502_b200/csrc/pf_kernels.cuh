@@ -168,12 +168,16 @@ __global__ void __launch_bounds__(kCascadeThreads) k_cascade(const __grid_consta
     double* myroot = a.scratch + (uint64_t)(a.NT / 2 + c) * PS;
     tree_combine<D>(a.part + (uint64_t)c * LPC * PS, LPC, a.scratch + (uint64_t)c * (LPC / 2) * PS);
     if (tid < PS) myroot[tid] = (LPC == 1) ? a.part[(uint64_t)c * PS + tid] : a.scratch[(uint64_t)c * (LPC / 2) * PS + tid];
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
+    if (gridDim.x > 1) {  // last CTA to finish does the top (one CTA: no ticket, no fence)
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) s_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1);
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+    } else {
+        __syncthreads();
+    }
 
     // last CTA: levels above the CTA subtrees
     const uint32_t R = gridDim.x;
@@ -205,7 +209,7 @@ __global__ void __launch_bounds__(kCascadeThreads) k_cascade(const __grid_consta
         if (tid == 0) a.shard_rec[0] = a.logV[level_offset(a.m, (int)a.S)];
         if (tid < PS) a.shard_rec[1 + tid] = fin[tid];
         __syncthreads();
-        if (tid == 0) *a.ticket = 0u;
+        if (tid == 0 && gridDim.x > 1) *a.ticket = 0u;
         return;
     }
     if (tid == 0) {
@@ -216,7 +220,7 @@ __global__ void __launch_bounds__(kCascadeThreads) k_cascade(const __grid_consta
             a.est[2 * D + k] = fin[2 + 2 * D + k] / (double)a.N;
             a.est[3 * D + k] = fin[2 + 3 * D + k] / (double)a.N;
         }
-        *a.ticket = 0u;
+        if (gridDim.x > 1) *a.ticket = 0u;
     }
 }
 

@@ -62,6 +62,9 @@ void launch_relabel_plan(cudaStream_t st, const RelabelArgs& a);
 void launch_relabel_lists(cudaStream_t st, const RelabelArgs& a);
 // pack = true: the surplus this rank sends; false: assemble the stage's outputs (nown = |own|)
 void launch_relabel_move(cudaStream_t st, int D, const RelabelArgs& a, bool pack, uint64_t nown, bool dbg);
+void launch_island_cross(cudaStream_t st, const IslandCrossArgs& a);
+void launch_block_gather_peer(cudaStream_t st, const PeerArgs& p, float* out, const int32_t* A, uint64_t N, uint32_t b,
+                              uint32_t D, uint32_t shift);
 void launch_debug_compose(const LaunchCfg& c, const int32_t* anc, uint64_t N, uint32_t S, int32_t* A);
 
 }  // namespace pfk

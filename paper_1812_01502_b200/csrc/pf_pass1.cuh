@@ -79,9 +79,13 @@ __device__ __forceinline__ uint32_t xs_swz(uint32_t s) {
 #define PF_PROBE(bit) false
 #endif
 
-#ifndef PF_P1_D4_MAXT  // launch bounds of the fused d = 4 pass (C4 runs it with 128 threads)
-#define PF_P1_D4_MAXT 512
-#define PF_P1_D4_MINB 1
+// Launch bounds of the fused d = 4 pass: 128 threads, 6 CTAs per SM (80 registers, no new
+// spill): 5.55 -> 5.27 ms per C4 launch against (512, 1) = 96 registers and 5 CTAs per SM;
+// 7 CTAs (72 registers) measured 5.42 (profiles/r2_pass1_launch_bounds.txt).  make_plan
+// keeps d = 4 at <= 128 threads per CTA.
+#ifndef PF_P1_D4_MAXT
+#define PF_P1_D4_MAXT 128
+#define PF_P1_D4_MINB 6
 #endif
 constexpr int pass1_maxt(int D, int MODE) { return (D == 4 && MODE == kPass1Fused) ? PF_P1_D4_MAXT : 512; }
 constexpr int pass1_minb(int D, int MODE) {
@@ -125,11 +129,20 @@ __global__ void __launch_bounds__(pass1_maxt(D, MODE), pass1_minb(D, MODE)) k_pa
             continue;
         }
         uint32_t src_q = base + 4u * q;  // AIRPF: the quad's position inside the island block it reads
+        const float* xsrc = a.x_in;
         if constexpr (AIR)
-            if (a.isl_src) src_q = ((uint32_t)a.isl_src[src_q >> b] << b) | (src_q & (M - 1u));
+            if (a.isl_src) {
+                const uint32_t gblk = (uint32_t)a.isl_src[src_q >> b];
+                if (a.xpeer[0]) {  // sharded (R27): the block's owner, over NVLink when remote
+                    xsrc = a.xpeer[gblk >> a.peer_shift];
+                    src_q = ((gblk & ((1u << a.peer_shift) - 1u)) << b) | (src_q & (M - 1u));
+                } else {
+                    src_q = (gblk << b) | (src_q & (M - 1u));
+                }
+            }
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-            const float4 t = __ldg(reinterpret_cast<const float4*>(a.x_in + (uint64_t)src_q * D) + c);
+            const float4 t = __ldg(reinterpret_cast<const float4*>(xsrc + (uint64_t)src_q * D) + c);
             xh[it][4 * c] = t.x;
             xh[it][4 * c + 1] = t.y;
             xh[it][4 * c + 2] = t.z;

@@ -146,7 +146,7 @@ class LibBackend:
     """One shard on the current GPU through the C-ABI (libpf.so)."""
 
     def __init__(self, params: dict, N: int, M: int, seed: int, rank: int, world: int, debug: bool = False,
-                 stream=None, poison: Optional[int] = None):
+                 stream=None, poison: Optional[int] = None, airpf: int = 0):
         """poison (a byte, checking aid): as pf.ParticleFilter -- fill the workspace before
         pf_init_sharded and keep a guard band behind it (guard_intact())."""
         import torch
@@ -158,7 +158,8 @@ class LibBackend:
         self.params = params
         self.N, self.M, self.rank, self.world = int(N), int(M), int(rank), int(world)
         self.d = int(params["d"])
-        self.flags = (pf.PF_FLAG_DEBUG if debug else 0) | (pf.PF_FLAG_GUARD if poison is not None else 0)
+        self.flags = ((pf.PF_FLAG_DEBUG if debug else 0) | (pf.PF_FLAG_GUARD if poison is not None else 0) |
+                      (pf.PF_FLAG_AIRPF if airpf else 0))
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         L = pf.lib()
         m, keep = pf.make_model(params)
@@ -178,6 +179,9 @@ class LibBackend:
                                     self.ws_ptr, nbytes, self.stream.cuda_stream, ctypes.byref(h)))
         self.h = h
         self.rec_len = 3 + 4 * self.d
+        self.airpf = int(airpf)
+        if airpf:
+            pf.pf_set_airpf(h, int(airpf))
 
     def _view(self, ptr: int, nbytes: int, dtype):
         off = ptr - self.ws.data_ptr()
@@ -261,6 +265,19 @@ class LibBackend:
 
     def cross_peer(self):
         self.pf._check(self.pf.lib().pf_cross_peer(self.h), self.h)
+
+    # sharded AIRPF (include/pf.h pf_island_map / pf_island_cross)
+    def island_map(self):
+        p = ctypes.c_void_p()
+        self.pf._check(self.pf.lib().pf_island_map(self.h, ctypes.byref(p)), self.h)
+        return self._view(int(p.value), 4 * (self.N // self.M // self.world), self.torch.int32)
+
+    def island_cross(self, t: int, partner_map):
+        self._keep_m = partner_map
+        self.pf._check(self.pf.lib().pf_island_cross(self.h, int(t), partner_map.data_ptr()), self.h)
+
+    def set_airpf(self, mode: int):
+        self.pf.pf_set_airpf(self.h, mode)
 
     # relabelled exchange (include/pf.h pf_relabel_begin / pf_relabel_end)
     def relabel_begin(self, t: int):
@@ -357,6 +374,9 @@ def sharded_step(backend, transport, y, y_dev=None, exchange: str = "pairwise") 
         if exchange == "relabel":
             relabel_exchange(backend, transport)
             return
+        if exchange == "island":
+            island_exchange(backend, transport)
+            return
         world = transport.world
         L = world.bit_length() - 1
         for t in range(1, L + 1):
@@ -411,6 +431,16 @@ def relabel_exchange(backend, transport) -> None:
         send, n_recv = backend.relabel_begin(t)
         recv = transport.sendrecv(send, n_recv * sb, partner(transport.rank, t))
         backend.relabel_end(t, recv)
+
+
+def island_exchange(backend, transport) -> None:
+    """Sharded AIRPF (include/pf.h pf_island_*; reading R27): the L cross island
+    stages exchange only the island maps (m / G int32 per rank and stage); the states move
+    when the next step reads its blocks from their owners (peer mapping, peer_connect)."""
+    L = transport.world.bit_length() - 1
+    for t in range(1, L + 1):
+        recv = transport.exchange(backend.island_map(), partner(transport.rank, t))
+        backend.island_cross(t, recv)
 
 
 def pull_exchange(backend, transport) -> None:
@@ -546,6 +576,18 @@ def loopback_step(backends: Sequence, y, exchange: str = "pairwise") -> None:
     if exchange == "relabel":
         for b, r in zip(backends, zip(*loopback_relabel(backends))):
             b.surplus = np.array(r)
+        return
+    if exchange == "island":
+        ws = [b.ws_ptr for b in backends]
+        for b in backends:
+            if getattr(b, "_peer_ws", None) != ws:
+                b.peer_set(ws)
+                b._peer_ws = ws
+        G = len(backends)
+        for t in range(1, G.bit_length()):
+            maps = [b.island_map().clone() for b in backends]  # every map taken before any stage
+            for r, b in enumerate(backends):
+                b.island_cross(t, maps[partner(r, t)])
         return
     world = len(backends)
     L = world.bit_length() - 1

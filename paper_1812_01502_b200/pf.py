@@ -101,6 +101,8 @@ def lib() -> ctypes.CDLL:
         L.pf_cross_peer.argtypes = [vp]
         L.pf_guard_check.argtypes = [vp, ctypes.c_ubyte, vp]
         L.pf_run_dev.argtypes = [vp, vp, ctypes.c_uint32, vp]
+        L.pf_island_map.argtypes = [vp, ctypes.POINTER(vp)]
+        L.pf_island_cross.argtypes = [vp, ctypes.c_int, vp]
         L.pf_step_local_begin.argtypes = [vp, vp, vp]
         L.pf_step_local_end.argtypes = [vp]
         L.pf_relabel_begin.argtypes = [vp, ctypes.c_int, vp, ctypes.POINTER(vp), vp, vp]
@@ -117,7 +119,7 @@ EXPORTED = ["pf_workspace_bytes", "pf_init", "pf_step", "pf_step_dev", "pf_estim
             "pf_rotation_offset", "pf_cross_pull_plan", "pf_cross_pull_pack", "pf_cross_pull_serve",
             "pf_cross_pull_finish", "pf_peer_export", "pf_peer_open", "pf_peer_set", "pf_cross_peer",
             "pf_guard_check", "pf_run_dev", "pf_relabel_begin", "pf_relabel_end",
-            "pf_step_local_begin", "pf_step_local_end"]
+            "pf_step_local_begin", "pf_step_local_end", "pf_island_map", "pf_island_cross"]
 PF_IPC_HANDLE_BYTES = 64
 GUARD_BYTES = 1 << 16  # guard band behind a poisoned workspace (ParticleFilter(poison=...))
 PF_KERNEL_KINDS = 5

@@ -186,6 +186,65 @@ class OracleShard:
         self.n += 1
 
 
+class OracleIslandShard:
+    """CPU stand-in for a sharded AIRPF LibBackend (dist.island_exchange): the oracle's
+    one-GPU AIRPF step (orc_step_airpf) gives every stage's island sources; this shard holds
+    the island map of its islands after the local stages (global ids) and applies each cross
+    stage from the oracle's table, taking the partner's map entry when the island took the
+    partner's block.  The final maps must be the oracle's island map."""
+
+    def __init__(self, params, N, M, seed, rank, world):
+        from oracle import oracle as orc
+        self.orc, self.params, self.N, self.M, self.seed = orc, params, N, M, seed
+        self.rank, self.world = rank, world
+        self.m = N // M
+        self.S = int(np.log2(self.m))
+        self.L = world.bit_length() - 1
+        self.mloc = self.m // world
+        self.i0 = rank * self.mloc
+        self.xhat = orc.init(params, N, seed).astype(np.float32)
+        self.n = 0
+
+    def step_local(self, y):
+        self.r = self.orc.step_airpf(self.params, self.N, self.M, self.seed, self.n, y, self.xhat, modified=True)
+        src = self.r["src"]
+        A = np.empty(self.mloc, np.int64)
+        for i in range(self.mloc):  # compose the local stages 1..S - L
+            c = self.i0 + i
+            for s in range(self.S - self.L, 0, -1):
+                c = int(src[s - 1][c])
+            A[i] = c
+        self.A = A
+        lv = self.r["logVbar"][self.orc.level_offset(self.m, self.S - self.L) + self.rank]
+        return torch.tensor([lv], dtype=torch.float64)
+
+    def step_top(self, all_recs):
+        for q in range(self.world):
+            want = self.r["logVbar"][self.orc.level_offset(self.m, self.S - self.L) + q]
+            assert float(all_recs[q][0]) == want, "records not gathered in rank order"
+
+    def island_map(self):
+        return torch.from_numpy(self.A.astype(np.int32).copy())
+
+    def island_cross(self, t, partner_map):
+        s = self.S - self.L + t
+        peer = pfd.partner(self.rank, t)
+        pm = partner_map.numpy().astype(np.int64)
+        assert pm.shape == (self.mloc,)
+        src = self.r["src"][s - 1]
+        for i in range(self.mloc):
+            g = self.i0 + i
+            if int(src[g]) != g:  # took the partner's block (after Alg. 7's rule)
+                assert int(src[g]) == g ^ (1 << (s - 1)) and int(src[g]) // self.mloc == peer
+                self.A[i] = pm[i]
+
+    def finish(self):
+        want = self.r["Aisl"][self.i0: self.i0 + self.mloc]
+        assert np.array_equal(self.A, want), "island map differs from the oracle's"
+        self.xhat = self.r["xhat"].astype(np.float32)
+        self.n += 1
+
+
 def _worker(rank, world, port, q, exchange="pairwise", peer_dir=None):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -194,8 +253,11 @@ def _worker(rank, world, port, q, exchange="pairwise", peer_dir=None):
         cfg = inputs.CONFIGS["C1"]
         params = inputs.model_params(cfg)
         N, M = 256, 16
-        be = OracleShard(params, N, M, 5, rank, world, peer_dir=peer_dir)
-        be.relabel = exchange == "relabel"
+        if exchange == "island":
+            be = OracleIslandShard(params, N, M, 5, rank, world)
+        else:
+            be = OracleShard(params, N, M, 5, rank, world, peer_dir=peer_dir)
+            be.relabel = exchange == "relabel"
         tr = pfd.TorchTransport()
         if exchange == "peer_fail":  # one rank cannot export: every rank agrees on "no peer"
             if rank == world - 1:
@@ -228,7 +290,7 @@ def _free_port():
 
 @pytest.mark.parametrize("world,exchange", [(2, "pairwise"), (4, "pairwise"), (2, "pull"), (4, "pull"),
                                             (2, "peer"), (4, "peer"), (4, "peer_fail"), (2, "relabel"),
-                                            (4, "relabel")])
+                                            (4, "relabel"), (2, "island"), (4, "island")])
 def test_gloo_sharded_sequence(world, exchange, tmp_path):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
