@@ -360,8 +360,14 @@ def sharded_step(backend, transport, y, y_dev=None, exchange: str = "pairwise") 
     the states each rank's outputs read) or "peer" (one kernel reads them straight from
     the owners' memory over NVLink; peer_connect first)."""
     with _on_stream(backend):  # every transport call is ordered on the backend's stream
-        if hasattr(backend, "step_local_begin") and getattr(transport, "nccl", False):
+        if hasattr(backend, "step_local_begin") and getattr(transport, "nccl", False) and not getattr(
+                backend, "airpf", 0):
             _local_overlapped(backend, transport, y, y_dev)
+            if exchange == "peer":
+                # the records were gathered BEFORE the stage passes: the owners' states are
+                # final only once every rank has passed this barrier (the peer gather reads
+                # them in place)
+                transport.device_barrier(backend.stream)
         else:
             rec = backend.step_local(y) if y_dev is None else backend.step_local_dev(y_dev)
             backend.step_top(transport.allgather(rec))

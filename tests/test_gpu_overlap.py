@@ -3,7 +3,8 @@ pf_step_local_begin / pf_step_local_end): the shard records are gathered on a si
 while the k_stages passes run, and k_top waits for both through stream events.  G ranks are
 host threads on one GPU with a transport that gathers device records through a host
 barrier (nothing on the GPU waits for another rank); the result must be bitwise the one-GPU
-run, for the pairwise, pull and relabel-free exchanges."""
+run, for the pairwise, pull and peer exchanges (the peer gather reads the owners' states in
+place, so the overlapped path adds a device barrier after the local stage passes)."""
 import threading
 
 import numpy as np
@@ -64,7 +65,7 @@ class ThreadTransport:
         self.sh["bar"].wait()
 
 
-@pytest.mark.parametrize("exchange", ["pairwise", "pull"])
+@pytest.mark.parametrize("exchange", ["pairwise", "pull", "peer"])
 @pytest.mark.parametrize("name,N,M,G", [("C4", 1 << 16, 64, 2), ("C3", 1 << 15, 32, 4)])
 def test_overlapped_local_phase_is_bitwise(name, N, M, G, exchange):
     cfg = inputs.CONFIGS[name]
@@ -86,6 +87,9 @@ def test_overlapped_local_phase_is_bitwise(name, N, M, G, exchange):
             st = torch.cuda.Stream()
             b = pfd.LibBackend(p, N, M, 13, r, G, stream=st)
             tr = ThreadTransport(r, G, shared)
+            if exchange == "peer":  # every rank's workspace is addressable on this GPU
+                got = tr._swap("ws", b.ws_ptr)
+                b.peer_set([got[q] for q in range(G)])
             res = []
             for y in ys:
                 pfd.sharded_step(b, tr, y, exchange=exchange)
