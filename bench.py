@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--exchange", default="peer", choices=["peer", "pull", "pairwise"],
                     help="N > 1: cross stages as one peer-memory gather over NVLink (default; the pull "
                          "exchange if a rank cannot map its peers), one all-to-all pull, or L pairwise rounds")
+    ap.add_argument("--graph", type=int, default=-1, choices=[-1, 0, 1],
+                    help="one GPU: the K timed steps as one CUDA graph (pf_graph_capture, untimed) launched "
+                         "once (pf_graph_launch, timed); -1 (default): when N <= 2^16 and the scheme allows")
     ap.add_argument("--multinomial", action="store_true",
                     help="the plain BPF (Alg. 2, multinomial resampling) instead of augmented resampling")
     return ap.parse_args()
@@ -321,17 +324,31 @@ def run_ours(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         stages = []
+        use_graph = world == 1 and args.theta <= 0 and (args.graph == 1 or (args.graph == -1 and cfg.N <= (1 << 16)))
+        if use_graph:  # K steps captured (untimed); the timed region is their one launch
+            f.timing_enable(False)
+            ks = (args.warmup + np.arange(args.steps)) % T
+            f.graph_capture(y_dev[torch.as_tensor(ks, device=dev)].contiguous())
+            stream.synchronize()
         e0.record(stream)
-        for k in range(args.steps):
-            step(args.warmup + k)
-            if args.theta > 0:
-                stages.append(f.last_stages())  # the adaptive step has synchronised already
+        if use_graph:
+            f.graph_launch()
+        else:
+            for k in range(args.steps):
+                step(args.warmup + k)
+                if args.theta > 0:
+                    stages.append(f.last_stages())  # the adaptive step has synchronised already
         e1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         clk = clocks.stop()
         ms = e0.elapsed_time(e1)
+        if use_graph:  # per-kernel device times from K eager steps after the timed graph
+            f.timing_enable(True)
+            for k in range(args.steps):
+                step(args.warmup + args.steps + k)
+            stream.synchronize()
         kt = f.timing_read()
         f.timing_enable(False)
         if world > 1:
@@ -433,6 +450,8 @@ def run_ours(args):
                                   if args.airpf else {}),
                                **({"algorithm": "plain BPF (Alg. 1 + 2, multinomial)"} if args.multinomial else {})),
                 "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+                **({"timed_as": "one CUDA graph of the K steps (pf_graph_launch); kernels: K eager steps after it"}
+                   if use_graph else {}),
                 "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line))
     if world > 1:

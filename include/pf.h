@@ -110,6 +110,16 @@ int pf_step_dev(pf_handle* h, const float* y_dev);
  * scheme reads S* back).  Errors as pf_step_dev; steps before a failing one stay done. */
 int pf_run_dev(pf_handle* h, const float* y_dev, uint32_t T, double* est_dev);
 
+/* The same T steps captured into one CUDA graph, launched later by pf_graph_launch (one
+ * launch; the graph is freed after it).  The handle's state advances at capture (as if
+ * the steps had run), so pf_graph_launch must follow before any other step, estimate or
+ * debug read.  For small problems whose step is a few microsecond-long kernels, the graph
+ * removes the per-launch gaps.  Not for the fully adapted scheme (it synchronises) or
+ * sharded handles.  Errors: PF_EINVAL, PF_ESTATE (adaptive, sharded, graph pending),
+ * PF_ECUDA. */
+int pf_graph_capture(pf_handle* h, const float* y_dev, uint32_t T, double* est_dev);
+int pf_graph_launch(pf_handle* h);
+
 /* --- fully adapted augmented resampling (AIRPF2) ---
  * With theta in (0, 1], every later pf_step evaluates the ESS of the stage weights
  *   E_s = (N^-1 sum_i V_s^i)^2 / (N^-1 sum_i (V_s^i)^2),  s = 0 (V_0 = the weights), 1..S

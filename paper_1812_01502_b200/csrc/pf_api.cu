@@ -383,9 +383,12 @@ struct pf_handle {
             cudaEventRecord(recs.back().b, stream);
         }
     }
+    // CUDA graph of T captured steps (pf_graph_capture -> pf_graph_launch)
+    cudaGraphExec_t gexec = nullptr;
     ~pf_handle() {
         for (cudaEvent_t e : pool) cudaEventDestroy(e);
         for (void* p : peer_ipc) cudaIpcCloseMemHandle(p);
+        if (gexec) cudaGraphExecDestroy(gexec);
     }
     float* X(int i) { return reinterpret_cast<float*>(ws + (i ? lay.X1 : lay.X0)); }
     template <typename T>
@@ -948,6 +951,10 @@ static int run_step_plain(pf_handle* h, const float* y_host, const float* y_dev,
 }
 
 static int run_step(pf_handle* h, const float* y_host, const float* y_dev) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(h->stream, &cs);
+    if (h->gexec && cs == cudaStreamCaptureStatusNone)
+        return fail(h, PF_ESTATE, "a captured graph is pending: pf_graph_launch first");
     if (h->airpf) return run_step_airpf(h, y_host, y_dev);  // AIRPF, or AIRPF2 with theta > 0
     if (h->theta > 0.0) return run_step_adaptive(h, y_host, y_dev);
     if (h->multinomial) return run_step_multinomial(h, y_host, y_dev);
@@ -1485,6 +1492,48 @@ int pf_run_dev(pf_handle* h, const float* y_dev, uint32_t T, double* est_dev) {
             if (e != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_run_dev: ") + cudaGetErrorString(e));
         }
     }
+    return PF_OK;
+}
+
+// T steps captured into one CUDA graph (launched by pf_graph_launch): for small problems
+// whose step is a few short kernels, the inter-kernel gaps of stream launches dominate.
+int pf_graph_capture(pf_handle* h, const float* y_dev, uint32_t T, double* est_dev) {
+    if (!h || !T || !y_dev) return fail(h, PF_EINVAL, "NULL argument or T = 0");
+    if (h->world > 1) return fail(h, PF_ESTATE, "sharded handle");
+    if (h->theta > 0.0) return fail(h, PF_ESTATE, "the fully adapted step synchronises (S*): not capturable");
+    if (h->gexec) return fail(h, PF_ESTATE, "a captured graph is pending: pf_graph_launch first");
+    const bool timing = h->timing;
+    h->timing = false;  // no event records inside the graph
+    cudaError_t e = cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+        h->timing = timing;
+        return fail(h, PF_ECUDA, std::string("pf_graph_capture: ") + cudaGetErrorString(e));
+    }
+    const int rc = pf_run_dev(h, y_dev, T, est_dev);
+    cudaGraph_t g = nullptr;
+    e = cudaStreamEndCapture(h->stream, &g);
+    h->timing = timing;
+    if (rc != PF_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&h->gexec, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+        h->gexec = nullptr;
+        return fail(h, PF_ECUDA, std::string("pf_graph_capture: ") + cudaGetErrorString(e));
+    }
+    h->last_launches *= (int)T;  // kernels in the graph (pf_run_dev's last step x T)
+    return PF_OK;
+}
+
+int pf_graph_launch(pf_handle* h) {
+    if (!h) return fail(h, PF_EINVAL, "NULL handle");
+    if (!h->gexec) return fail(h, PF_ESTATE, "no captured graph");
+    const cudaError_t e = cudaGraphLaunch(h->gexec, h->stream);
+    cudaGraphExecDestroy(h->gexec);  // freed once the launch completes
+    h->gexec = nullptr;
+    if (e != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_graph_launch: ") + cudaGetErrorString(e));
     return PF_OK;
 }
 

@@ -101,6 +101,8 @@ def lib() -> ctypes.CDLL:
         L.pf_cross_peer.argtypes = [vp]
         L.pf_guard_check.argtypes = [vp, ctypes.c_ubyte, vp]
         L.pf_run_dev.argtypes = [vp, vp, ctypes.c_uint32, vp]
+        L.pf_graph_capture.argtypes = [vp, vp, ctypes.c_uint32, vp]
+        L.pf_graph_launch.argtypes = [vp]
         L.pf_island_map.argtypes = [vp, ctypes.POINTER(vp)]
         L.pf_island_cross.argtypes = [vp, ctypes.c_int, vp]
         L.pf_step_local_begin.argtypes = [vp, vp, vp]
@@ -119,7 +121,8 @@ EXPORTED = ["pf_workspace_bytes", "pf_init", "pf_step", "pf_step_dev", "pf_estim
             "pf_rotation_offset", "pf_cross_pull_plan", "pf_cross_pull_pack", "pf_cross_pull_serve",
             "pf_cross_pull_finish", "pf_peer_export", "pf_peer_open", "pf_peer_set", "pf_cross_peer",
             "pf_guard_check", "pf_run_dev", "pf_relabel_begin", "pf_relabel_end",
-            "pf_step_local_begin", "pf_step_local_end", "pf_island_map", "pf_island_cross"]
+            "pf_step_local_begin", "pf_step_local_end", "pf_island_map", "pf_island_cross",
+            "pf_graph_capture", "pf_graph_launch"]
 PF_IPC_HANDLE_BYTES = 64
 GUARD_BYTES = 1 << 16  # guard band behind a poisoned workspace (ParticleFilter(poison=...))
 PF_KERNEL_KINDS = 5
@@ -358,6 +361,20 @@ class ParticleFilter:
         _check(lib().pf_run_dev(self.h, y.data_ptr(), T, out.data_ptr() if out is not None else None), self.h)
         self._keep_y = y
         return out
+
+    def graph_capture(self, y_dev, estimates: bool = False):
+        """Capture len(y_dev) steps into one CUDA graph (pf_graph_capture); launch it with
+        graph_launch().  Returns the device estimate rows tensor (or None)."""
+        torch = self.torch
+        y = y_dev.contiguous()
+        T = int(y.shape[0])
+        out = torch.empty((T, 4, self.d), dtype=torch.float64, device=self.device) if estimates else None
+        _check(lib().pf_graph_capture(self.h, y.data_ptr(), T, out.data_ptr() if out is not None else None), self.h)
+        self._keep_gy = (y, out)
+        return out
+
+    def graph_launch(self):
+        _check(lib().pf_graph_launch(self.h), self.h)
 
     def set_state(self, xhat: np.ndarray, n: int):
         pf_debug_set_state(self.h, np.asarray(xhat, np.float32).reshape(self.N, self.d), n)

@@ -13,6 +13,8 @@
 //       replicated over each halfword by PRMT's sign-extension, entries assembled by LOP3
 //       two at a time
 //   D8: byte entries with the same sign trick
+//   D9: D7 with the sign extension done by inline-PTX prmt (CUDA's __byte_perm drops the
+//       selector's sign-extension bit)
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o draw_bench draw_bench.cu
 #include <cstdint>
 #include <cstdio>
@@ -64,6 +66,17 @@ __device__ __forceinline__ uint2 draw(const uint4 blk, uint32_t Praw, uint32_t j
         for (int e = 0; e < 4; ++e) dd[e] = (int32_t)(rw[e] >> b) - (int32_t)Praw;  // < 0: the lower side
         const uint32_t s01 = __byte_perm((uint32_t)dd[0], (uint32_t)dd[1], 0xFFBBu);  // 0xffff where lower
         const uint32_t s23 = __byte_perm((uint32_t)dd[2], (uint32_t)dd[3], 0xFFBBu);
+        const uint32_t w01 = __byte_perm(rw[0], rw[1], 0x5410u), w23 = __byte_perm(rw[2], rw[3], 0x5410u);
+        return make_uint2(((w01 & mask2) | blo2) | (~s01 & bitb2), ((w23 & mask2) | blo2) | (~s23 & bitb2));
+    } else if constexpr (V == 9) {
+        const uint32_t blo = (j & ~bit) << b, bitb = bit << b;
+        const uint32_t blo2 = blo | (blo << 16), bitb2 = bitb | (bitb << 16), mask2 = mask | (mask << 16);
+        uint32_t dd[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dd[e] = (uint32_t)((int32_t)(rw[e] >> b) - (int32_t)Praw);  // < 0: lower side
+        uint32_t s01, s23;
+        asm("prmt.b32 %0, %1, %2, 0xFFBB;" : "=r"(s01) : "r"(dd[0]), "r"(dd[1]));  // 0xffff where lower
+        asm("prmt.b32 %0, %1, %2, 0xFFBB;" : "=r"(s23) : "r"(dd[2]), "r"(dd[3]));
         const uint32_t w01 = __byte_perm(rw[0], rw[1], 0x5410u), w23 = __byte_perm(rw[2], rw[3], 0x5410u);
         return make_uint2(((w01 & mask2) | blo2) | (~s01 & bitb2), ((w23 & mask2) | blo2) | (~s23 & bitb2));
     } else if constexpr (V == 8) {
@@ -147,7 +160,9 @@ __global__ void check(uint32_t b, uint32_t* bad) {
         const uint32_t j = t & 63u, st = t % 6u;
         const uint2 r0 = draw<0>(blk, Pr, j, st, b), r7 = draw<7>(blk, Pr, j, st, b);
         const uint2 r6 = draw<6>(blk, Pr, j, st, b), r8 = draw<8>(blk, Pr, j, st, b);
+        const uint2 r9 = draw<9>(blk, Pr, j, st, b);
         if (r0.x != r7.x || r0.y != r7.y) atomicAdd(bad, 1u);
+        if (r0.x != r9.x || r0.y != r9.y) atomicAdd(bad + 2, 1u);
         const uint32_t m4 = ((1u << b) - 1u) * 0x01010101u | 0x80808080u;
         if ((r6.x & m4) != (r8.x & m4)) atomicAdd(bad + 1, 1u);
     }
@@ -156,12 +171,12 @@ __global__ void check(uint32_t b, uint32_t* bad) {
 int main() {
     {
         uint32_t* bad;
-        cudaMalloc(&bad, 8);
-        cudaMemset(bad, 0, 8);
+        cudaMalloc(&bad, 12);
+        cudaMemset(bad, 0, 12);
         for (uint32_t b = 1; b <= 7; ++b) check<<<256, 256>>>(b, bad);
-        uint32_t hb[2];
-        cudaMemcpy(hb, bad, 8, cudaMemcpyDeviceToHost);
-        printf("sign-trick exactness: %u (16-bit) / %u (byte) mismatches\n", hb[0], hb[1]);
+        uint32_t hb[3];
+        cudaMemcpy(hb, bad, 12, cudaMemcpyDeviceToHost);
+        printf("sign-trick exactness: %u (16-bit) / %u (byte) / %u (16-bit, PTX prmt) mismatches\n", hb[0], hb[1], hb[2]);
     }
     const int blocks = 148, threads = 1024, tiles = 400;
     uint32_t* out;
@@ -176,8 +191,8 @@ int main() {
     cudaEventCreate(&e);
     const char* names[] = {"D0 shift-compare", "P  Philox only", "D2 (r|mask)>T", "D3 carry on FMA pipe",
                            "D4 D2 x2 interleaved", "D5 pinned bases+PRMT", "D6 byte entries", "D7 sign trick 16-bit",
-                           "D8 sign trick bytes"};
-    for (int v = 0; v < 9; ++v) {
+                           "D8 sign trick bytes", "D9 sign trick 16-bit PTX"};
+    for (int v = 0; v < 10; ++v) {
         for (int rep = 0; rep < 3; ++rep) {
             cudaEventRecord(a);
             switch (v) {
@@ -189,7 +204,8 @@ int main() {
                 case 5: bench<5><<<blocks, threads>>>(ks, tiles, 6, out); break;
                 case 6: bench<6><<<blocks, threads>>>(ks, tiles, 6, out); break;
                 case 7: bench<7><<<blocks, threads>>>(ks, tiles, 6, out); break;
-                default: bench<8><<<blocks, threads>>>(ks, tiles, 6, out); break;
+                case 8: bench<8><<<blocks, threads>>>(ks, tiles, 6, out); break;
+                default: bench<9><<<blocks, threads>>>(ks, tiles, 6, out); break;
             }
             cudaEventRecord(e);
             cudaEventSynchronize(e);

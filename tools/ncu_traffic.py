@@ -23,7 +23,7 @@ acc = {}
 inst = {}
 for row in r:
     d = dict(zip(hdr, row))
-    name = d["Kernel Name"].replace("void ", "").split("<")[0].split("(")[0]
+    name = d["Kernel Name"].replace("void ", "").split("<")[0].split("(")[0].replace("k_stages_ws", "k_stages")
     tot = sum(float(d[m].replace(",", "")) * scale[units[m]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     acc.setdefault(name, []).append(tot)
     if "smsp__inst_executed.sum" in d:
