@@ -1487,9 +1487,10 @@ int pf_run_dev(pf_handle* h, const float* y_dev, uint32_t T, double* est_dev) {
         const int rc = dispatch_step(h, nullptr, y_dev + (size_t)k * h->mp.dy);
         if (rc != PF_OK) return rc;
         if (est_dev) {  // rows: filter x, filter x^2, predict x, predict x^2 (d doubles each)
-            const cudaError_t e = cudaMemcpy2DAsync(est_dev + (size_t)k * 4 * d, (size_t)d * 8, h->at<double>(h->lay.est),
-                                                    (size_t)D * 8, (size_t)d * 8, 4, cudaMemcpyDeviceToDevice, h->stream);
-            if (e != cudaSuccess) return fail(h, PF_ECUDA, std::string("pf_run_dev: ") + cudaGetErrorString(e));
+            // a kernel, not a 2-D memcpy: capturable into pf_graph_capture's graph
+            launch_rows_copy(h->stream, h->at<double>(h->lay.est), (uint32_t)D, est_dev + (size_t)k * 4 * d, (uint32_t)d, 4u);
+            const int rc2 = check_cuda(h, "pf_run_dev");
+            if (rc2 != PF_OK) return rc2;
         }
     }
     return PF_OK;

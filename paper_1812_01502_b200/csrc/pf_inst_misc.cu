@@ -225,6 +225,17 @@ void launch_block_gather(cudaStream_t st, const float* in, float* out, const int
     k_block_gather<<<1184, 256, 0, st>>>(in, out, A, N, b, D);
 }
 
+// rows x cols doubles from a pitch-sp array to a pitch-dp array (pf_run_dev's estimate rows)
+__global__ void k_rows_copy(const double* __restrict__ src, uint32_t sp, double* __restrict__ dst, uint32_t dp,
+                            uint32_t rows) {
+    const uint32_t i = threadIdx.x, r = i / dp, c = i % dp;
+    if (r < rows) dst[r * dp + c] = src[r * sp + c];
+}
+
+void launch_rows_copy(cudaStream_t st, const double* src, uint32_t sp, double* dst, uint32_t dp, uint32_t rows) {
+    k_rows_copy<<<1, rows * dp, 0, st>>>(src, sp, dst, dp, rows);
+}
+
 // ---- PF_EST_RESAMPLED: N^-1 sum_i phi(x_hat^i), phi in {x, x^2} ----------
 // Computed on demand from the step's output buffer (through the island map of an AIRPF
 // step, whose x_hat is never materialised).  Fixed grid, fixed order: thread partials in

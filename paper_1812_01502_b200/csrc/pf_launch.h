@@ -65,6 +65,7 @@ void launch_relabel_move(cudaStream_t st, int D, const RelabelArgs& a, bool pack
 void launch_island_cross(cudaStream_t st, const IslandCrossArgs& a);
 void launch_block_gather_peer(cudaStream_t st, const PeerArgs& p, float* out, const int32_t* A, uint64_t N, uint32_t b,
                               uint32_t D, uint32_t shift);
+void launch_rows_copy(cudaStream_t st, const double* src, uint32_t sp, double* dst, uint32_t dp, uint32_t rows);
 void launch_debug_compose(const LaunchCfg& c, const int32_t* anc, uint64_t N, uint32_t S, int32_t* A);
 
 }  // namespace pfk

@@ -45,17 +45,19 @@ def test_c1_vs_kalman():
     assert np.all(np.abs(z) < 5.0), z
 
 
-@pytest.mark.parametrize("name,N,M", [("C4", 1 << 20, 64), ("C2", 1 << 18, 256)])
+@pytest.mark.parametrize("name,N,M", [("C4", 1 << 18, 64), ("C2", 1 << 16, 256)])
 def test_lg_large_vs_kalman(name, N, M):
-    """A single large-N run: per-step filter-mean error below 6 x the posterior sd / sqrt(N/S)."""
+    """16 independent runs: the per-step filter mean of the runs within 5 standard errors
+    (their spread) of the exact Kalman mean, every coordinate (as test_c1_vs_kalman)."""
     cfg = inputs.CONFIGS[name]
     p = inputs.model_params(cfg)
     _, ys = inputs.simulate(cfg, T=20)
-    km, kc = kalman.kalman_filter(p["A"], p["Q"], p["H"], p["R"], p["m0"], p["P0"], ys)
-    means, _ = _run(p, N, M, 3, ys)
-    S = np.log2(N // M)
-    sd = np.sqrt(np.diagonal(kc, axis1=1, axis2=2))
-    assert np.all(np.abs(means - km) < 6 * sd * np.sqrt(S / N) * 10 + 1e-6)
+    km, _ = kalman.kalman_filter(p["A"], p["Q"], p["H"], p["R"], p["m0"], p["P0"], ys)
+    J = 16
+    runs = np.array([_run(p, N, M, 40 + j, ys)[0] for j in range(J)])  # J x T x d
+    se = runs.std(axis=0, ddof=1) / np.sqrt(J)
+    z = (runs.mean(axis=0) - km) / np.maximum(se, 1e-12)
+    assert np.all(np.abs(z) < 5.0), np.abs(z).max()
 
 
 def test_determinism_and_step_dev():
@@ -149,23 +151,33 @@ def test_variant_rates_on_gpu(kw):
 
 def test_c4_full_size_filter_vs_kalman():
     """The bench's workload end to end: C4 at N = 2^28 over its T = 50 observations through
-    pf_step_dev (as bench.py), filter means against the exact Kalman means at every step
-    (same error model as test_lg_large_vs_kalman)."""
+    pf_step_dev (as bench.py), two independent runs.  Their difference estimates the Monte
+    Carlo error: with rho^2 = mean over steps and coordinates of (a - b)^2 / (2 sd^2) (sd the
+    Kalman posterior sd; the relative error of a stable filter has a step-independent
+    scale), the mean of the two runs must lie within 6 rho sd / sqrt(2) of the Kalman mean at
+    every (step, coordinate) -- 200 tests at 6 sigma."""
     cfg = inputs.CONFIGS["C4"]
     p = inputs.model_params(cfg)
     _, ys = inputs.simulate(cfg)
     km, kc = kalman.kalman_filter(p["A"], p["Q"], p["H"], p["R"], p["m0"], p["P0"], ys)
-    f = pfb.ParticleFilter(p, cfg.N, cfg.M, 1)
     yd = torch.tensor(np.asarray(ys, np.float32), device="cuda")
-    means = np.zeros((len(ys), cfg.d))
-    for n in range(len(ys)):
-        f.step_dev(yd[n])
-        means[n] = f.estimate(pfb.PF_PHI_X, pfb.PF_EST_FILTER)
-    f.close()
-    S = np.log2(cfg.N // cfg.M)
+    runs = []
+    for seed in (1, 2):
+        f = pfb.ParticleFilter(p, cfg.N, cfg.M, seed)
+        means = np.zeros((len(ys), cfg.d))
+        for n in range(len(ys)):
+            f.step_dev(yd[n])
+            means[n] = f.estimate(pfb.PF_PHI_X, pfb.PF_EST_FILTER)
+        f.close()
+        runs.append(means)
+    a, b = runs
     sd = np.sqrt(np.diagonal(kc, axis1=1, axis2=2))
-    err = np.abs(means - km) / (sd * np.sqrt(S / cfg.N))
-    assert np.all(err < 60), err.max()
+    rho = np.sqrt(np.mean((a - b) ** 2 / (2 * sd ** 2)))
+    err = np.abs(0.5 * (a + b) - km) / sd
+    assert np.all(err < 6 * rho / np.sqrt(2) + 1e-6), (err.max(), rho)
+    # and the Monte Carlo scale itself is that of N = 2^28 particles: rho <= a few sqrt(S/N)
+    S = np.log2(cfg.N // cfg.M)
+    assert rho < 10 * np.sqrt(S / cfg.N), rho
 
 
 @pytest.mark.parametrize("kw", [{}, {"theta": 0.5}, {"airpf": 1}, {"multinomial": True}])
