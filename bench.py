@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--graph", type=int, default=-1, choices=[-1, 0, 1],
                     help="one GPU: the K timed steps as one CUDA graph (pf_graph_capture, untimed) launched "
                          "once (pf_graph_launch, timed); -1 (default): when N <= 2^16 and the scheme allows")
+    ap.add_argument("--y-dev", action="store_true",
+                    help="timed loop through pf_step_dev (observations read from device memory) instead of "
+                         "the north_star pf_step(h, y_host) (observation in the launch parameters)")
     ap.add_argument("--multinomial", action="store_true",
                     help="the plain BPF (Alg. 2, multinomial resampling) instead of augmented resampling")
     return ap.parse_args()
@@ -334,8 +337,9 @@ def run_ours(args):
         if use_graph:
             f.graph_launch()
         else:
+            timed_step = step if args.y_dev else step_host
             for k in range(args.steps):
-                step(args.warmup + k)
+                timed_step(args.warmup + k)
                 if args.theta > 0:
                     stages.append(f.last_stages())  # the adaptive step has synchronised already
         e1.record(stream)
@@ -450,8 +454,9 @@ def run_ours(args):
                                   if args.airpf else {}),
                                **({"algorithm": "plain BPF (Alg. 1 + 2, multinomial)"} if args.multinomial else {})),
                 "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
-                **({"timed_as": "one CUDA graph of the K steps (pf_graph_launch); kernels: K eager steps after it"}
-                   if use_graph else {}),
+                "timed_as": ("one CUDA graph of the K steps (pf_graph_launch); kernels: K eager steps after it"
+                             if use_graph else ("pf_step_dev (y in device memory)" if args.y_dev
+                                                else "pf_step(h, y_host) (y in the launch parameters)")),
                 "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line))
     if world > 1:

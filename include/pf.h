@@ -115,7 +115,8 @@ int pf_run_dev(pf_handle* h, const float* y_dev, uint32_t T, double* est_dev);
  * the steps had run), so pf_graph_launch must follow before any other step, estimate or
  * debug read.  For small problems whose step is a few microsecond-long kernels, the graph
  * removes the per-launch gaps.  Not for the fully adapted scheme (it synchronises) or
- * sharded handles.  Errors: PF_EINVAL, PF_ESTATE (adaptive, sharded, graph pending),
+ * sharded handles; the handle's stream must not be the legacy default stream (capture).
+ * Errors: PF_EINVAL, PF_ESTATE (adaptive, sharded, graph pending, default stream),
  * PF_ECUDA. */
 int pf_graph_capture(pf_handle* h, const float* y_dev, uint32_t T, double* est_dev);
 int pf_graph_launch(pf_handle* h);

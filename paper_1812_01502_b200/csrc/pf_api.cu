@@ -1503,6 +1503,7 @@ int pf_graph_capture(pf_handle* h, const float* y_dev, uint32_t T, double* est_d
     if (h->world > 1) return fail(h, PF_ESTATE, "sharded handle");
     if (h->theta > 0.0) return fail(h, PF_ESTATE, "the fully adapted step synchronises (S*): not capturable");
     if (h->gexec) return fail(h, PF_ESTATE, "a captured graph is pending: pf_graph_launch first");
+    if (h->stream == nullptr) return fail(h, PF_ESTATE, "stream capture needs a non-default stream");
     const bool timing = h->timing;
     h->timing = false;  // no event records inside the graph
     cudaError_t e = cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal);

@@ -13,7 +13,7 @@ constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kPass1MaxGroups = 64;  // T1 <= 64: the V tree of a tile fits one warp's lanes
 
 struct Pass1Smem {
-    uint32_t xs, w, L1, tab, chunk, lv1, red, ess, total;
+    uint32_t xs, w, qe, L1, tab, chunk, lv1, red, ess, total;
 };
 __host__ __device__ inline Pass1Smem pass1_smem(int D, uint32_t P1, uint32_t M, uint32_t k1, uint32_t threads,
                                                 uint32_t tb) {
@@ -27,6 +27,7 @@ __host__ __device__ inline Pass1Smem pass1_smem(int D, uint32_t P1, uint32_t M, 
     const uint32_t T1 = P1 / M;
     s.xs = take(P1 * 4u * (uint32_t)D);
     s.w = take(P1 * 4u);
+    s.qe = take(P1);  // quad ends of the CDF (P1 / 4 floats): the first search level
     s.L1 = take(P1 * tb);
     s.tab = take(k1 >= 2 ? (k1 - 1u) * P1 * tb : 0u);
     s.chunk = take(M > 64 ? (P1 / 128u) * 4u : 0u);  // per-warp-chunk maxima / totals

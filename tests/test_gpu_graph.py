@@ -22,14 +22,19 @@ def test_graph_equals_eager(name, N, M, kw):
     p = inputs.model_params(cfg)
     _, ys = inputs.simulate(cfg, T=12)
     yd = torch.tensor(np.asarray(ys, np.float32), device="cuda")
+    st = torch.cuda.Stream()  # capture needs a non-default stream
     a = pfb.ParticleFilter(p, N, M, 5, **kw)
     est_a = a.run_dev(yd)
-    b = pfb.ParticleFilter(p, N, M, 5, **kw)
+    b = pfb.ParticleFilter(p, N, M, 5, stream=st, **kw)
     est_b = b.graph_capture(yd, estimates=True)
     with pytest.raises(pfb.PFError):  # pending graph: no other step
         b.step(ys[0])
     b.graph_launch()
     torch.cuda.synchronize()
+    c = pfb.ParticleFilter(p, N, M, 5, **kw)  # the legacy default stream cannot be captured
+    with pytest.raises(pfb.PFError):
+        c.graph_capture(yd)
+    c.close()
     assert torch.equal(est_a, est_b)
     assert np.array_equal(a.debug_get(pfb.PF_DBG_XHAT), b.debug_get(pfb.PF_DBG_XHAT))
     b.step(ys[0])  # usable again
@@ -40,7 +45,7 @@ def test_graph_equals_eager(name, N, M, kw):
 def test_graph_refuses_adaptive():
     cfg = inputs.CONFIGS["C1"]
     p = inputs.model_params(cfg)
-    f = pfb.ParticleFilter(p, 1024, 64, 1, theta=0.5)
+    f = pfb.ParticleFilter(p, 1024, 64, 1, theta=0.5, stream=torch.cuda.Stream())
     yd = torch.zeros((3, 1), dtype=torch.float32, device="cuda")
     with pytest.raises(pfb.PFError):
         f.graph_capture(yd)
