@@ -575,7 +575,7 @@ static void launch_stages_k(pf_handle* h, const StagePass& cp, const void* pin, 
     a.lowbits = cp.s0 - 1;
     a.pipe = cp.pipe;
     // k_stages_ws: walkers = the given fraction (in 32ths) of the CTA, whole warps
-    a.ws_walkers = std::max<uint32_t>(32u, (cp.threads * env_u32("PF_STAGE_WS_WALK32", 12u) / 32u) & ~31u);
+    a.ws_walkers = std::max<uint32_t>(32u, (cp.threads * env_u32("PF_STAGE_WS_WALK32", 16u) / 32u) & ~31u);
     a.out_rot = out_rot;
     a.out_S = h->S;
     a.pin = pin;

@@ -391,7 +391,7 @@ __device__ __forceinline__ void ws_draws(const StageArgs& a, const StageTile& g,
         const uint32_t gp1 = ((tlo | (j1 << lowbits) | thi) << b) | (l1 & mask);
         const uint32_t c0 = (a.pos0 + gp0) >> 2, c1 = (a.pos0 + gp1) >> 2;
         uint32_t toff = 0;
-        for (uint32_t st = 0; st < k; ++st) {
+        for (uint32_t st = 0; st + 1u < k; ++st) {  // the last stage: in the walk (ws_walk)
             const uint32_t s = a.s0 + st;
             const uint4 b0 = rng_block(a.key, c0, a.n, kDomainResample, s);
             const uint4 b1 = rng_block(a.key, c1, a.n, kDomainResample, s);
@@ -420,15 +420,33 @@ __device__ __forceinline__ void ws_draws(const StageArgs& a, const StageTile& g,
     }
 }
 
-template <typename T, int TB>
+// The walkers' share: quads tid, tid + nthr, ...  The pass's LAST stage is drawn here from
+// the output quad's own Philox block (its 4 words are exactly these 4 outputs' draws, and
+// the walk starts at the output), so the drawers skip it and no table holds it: 1/k of the
+// draw work moves to the walkers, which wait on the drawers otherwise (ncu, round 2).
+template <typename T, int TB, bool DBG>
 __device__ __forceinline__ void ws_walk(const StageArgs& a, const StageTile& g, const T* xs, const unsigned char* tabs,
-                                        uint32_t tid, uint32_t nthr) {
+                                        const uint32_t* ths, uint32_t tid, uint32_t nthr) {
     const uint32_t M = a.M, b = a.b, k = a.k, P = a.P, mask = M - 1u, nq = P >> 2, lowbits = a.lowbits;
+    const uint32_t stl = k - 1u, sl = a.s0 + stl, bitl = 1u << stl;
+    const uint32_t Pl = ths[(1u << k) - 2u];  // the last stage pairs the tile's two halves: one threshold
     T* pout = reinterpret_cast<T*>(a.pout);
     for (uint32_t q = tid; q < nq; q += nthr) {
         const uint32_t l0 = 4u * q;
-        uint32_t tp[4] = {l0, l0 + 1u, l0 + 2u, l0 + 3u};
-        for (int st = (int)k - 1; st >= 0; --st) {
+        const uint32_t j = l0 >> b;
+        const uint32_t gp = ((g.tlo | (j << lowbits) | g.thi) << b) | (l0 & mask);
+        const uint4 blk = rng_block(a.key, (a.pos0 + gp) >> 2, a.n, kDomainResample, sl);
+        const uint32_t rw[4] = {blk.x, blk.y, blk.z, blk.w};
+        uint32_t tp[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t jj = ((rw[e] >> b) >= Pl) ? (j | bitl) : (j & ~bitl);
+            tp[e] = (jj << b) | (rw[e] & mask);
+            if constexpr (DBG)
+                a.dbg_anc[(uint64_t)(sl - 1) * a.N + gp + e] =
+                    (int32_t)(a.pos0 + (((g.tlo | (jj << lowbits) | g.thi) << b) | (rw[e] & mask)));
+        }
+        for (int st = (int)k - 2; st >= 0; --st) {
             if constexpr (TB == 1) {
                 const unsigned char* Ts = tabs + (uint32_t)st * P;
                 const uint32_t sh = (uint32_t)st + b;
@@ -447,8 +465,7 @@ __device__ __forceinline__ void ws_walk(const StageArgs& a, const StageTile& g, 
         Vec4<T> v;
 #pragma unroll
         for (int e = 0; e < 4; ++e) v.v[e] = xs[tp[e]];
-        const uint32_t j = l0 >> b;
-        uint32_t gp0 = ((g.tlo | (j << lowbits) | g.thi) << b) | (l0 & mask);
+        uint32_t gp0 = gp;
         if (a.out_rot) gp0 = (rotr_group(gp0 >> b, a.out_rot, a.out_S) << b) | (gp0 & mask);
         *reinterpret_cast<Vec4<T>*>(pout + gp0) = v;
     }
@@ -496,7 +513,7 @@ __global__ void __launch_bounds__(1024, 1) k_stages_ws(const __grid_constant__ S
             const uint32_t sl = i & 1u, par = (i >> 1) & 1u;
             mbar_wait_sleep(st_full + sl, par);
             mbar_wait_sleep(tab_full + sl, par);
-            ws_walk<T, TB>(a, stage_tile_geom(a, t0 + i * gridDim.x), xbuf(sl), tbuf(sl), rt, nwalk);
+            ws_walk<T, TB, DBG>(a, stage_tile_geom(a, t0 + i * gridDim.x), xbuf(sl), tbuf(sl), thbuf(sl), rt, nwalk);
             mbar_arrive(slot_free + sl);
             if (i + 2u < nt && threadIdx.x < 32u) {  // refill the slot once every walker has left it
                 mbar_wait_sleep(slot_free + sl, par);
@@ -515,14 +532,14 @@ __global__ void __launch_bounds__(1024, 1) k_stages_ws(const __grid_constant__ S
             const uint32_t s = a.s0 + st;
             return __ldg(a.thr + level_offset(a.m, (int)s) + (g.thi >> s) + (e - off));
         };
-        if (rt < E) thbuf(0)[rt] = thr_of(0);
+        uint32_t nxt = rt < E ? thr_of(0) : 0u;
         for (uint32_t i = 0; i < nt; ++i) {
             const uint32_t sl = i & 1u, par = (i >> 1) & 1u;
-            if (i >= 2u) mbar_wait_sleep(slot_free + sl, par ^ 1u);  // tile i-2 walked
+            if (i >= 2u) mbar_wait_sleep(slot_free + sl, par ^ 1u);  // tile i-2 walked: the slot is free
+            if (rt < E) thbuf(sl)[rt] = nxt;                         // (the walkers read its threshold too)
             named_bar_sync(1u, ndraw);                               // tile i's thresholds stored
-            const uint32_t nxt = (rt < E && i + 1u < nt) ? thr_of(i + 1u) : 0u;  // in flight during the draws
+            nxt = (rt < E && i + 1u < nt) ? thr_of(i + 1u) : 0u;     // in flight during the draws
             ws_draws<TB, DBG>(a, stage_tile_geom(a, t0 + i * gridDim.x), thbuf(sl), tbuf(sl), rt, ndraw);
-            if (rt < E && i + 1u < nt) thbuf(sl ^ 1u)[rt] = nxt;
             mbar_arrive(tab_full + sl);
         }
     }
