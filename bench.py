@@ -53,7 +53,7 @@ def parse():
                          "exchange if a rank cannot map its peers), one all-to-all pull, or L pairwise rounds")
     ap.add_argument("--graph", type=int, default=-1, choices=[-1, 0, 1],
                     help="one GPU: the K timed steps as one CUDA graph (pf_graph_capture, untimed) launched "
-                         "once (pf_graph_launch, timed); -1 (default): when N <= 2^16 and the scheme allows")
+                         "once (pf_graph_launch, timed); -1 (default): when N <= 2^22 and the scheme allows")
     ap.add_argument("--y-dev", action="store_true",
                     help="timed loop through pf_step_dev (observations read from device memory) instead of "
                          "the north_star pf_step(h, y_host) (observation in the launch parameters)")
@@ -327,7 +327,7 @@ def run_ours(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         stages = []
-        use_graph = world == 1 and args.theta <= 0 and (args.graph == 1 or (args.graph == -1 and cfg.N <= (1 << 16)))
+        use_graph = world == 1 and args.theta <= 0 and (args.graph == 1 or (args.graph == -1 and cfg.N <= (1 << 22)))
         if use_graph:  # K steps captured (untimed); the timed region is their one launch
             f.timing_enable(False)
             ks = (args.warmup + np.arange(args.steps)) % T

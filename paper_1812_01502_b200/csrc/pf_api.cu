@@ -221,7 +221,7 @@ struct Layout {
     size_t pull_src, pull_rank, pull_counts, pull_fill, pull_off, pull_req, pull_outpos, pull_serve;  // world > 1
     size_t dbg_x, dbg_lw, dbg_anc, dbg_A;
     size_t mom_part, mom_out;          // PF_EST_RESAMPLED (k_moments)
-    size_t rl_cnt, rl_off, rl_own, rl_par, rl_send;  // relabelled exchange (world > 1)
+    size_t rl_cnt, rl_off, rl_own, rl_par, rl_kidx, rl_send;  // relabelled exchange (world > 1)
     size_t guard_count;                // PF_FLAG_GUARD
     std::vector<size_t> gaps;          // PF_FLAG_GUARD: offsets of the PF_GUARD_BYTES gaps
     size_t total;
@@ -298,6 +298,7 @@ Layout make_layout(const Plan& p, uint64_t N, uint32_t M, uint32_t flags, uint32
         L.rl_off = take(sh ? (2 * nch + 2) * 4 : 0);
         L.rl_own = take(sh ? N * 4 : 0);
         L.rl_par = take(sh ? N * 4 : 0);
+        L.rl_kidx = take(sh ? N * 4 : 0);
         L.rl_send = take(sh ? xb : 0);
     }
     L.mom_part = take((size_t)kMomPartDoubles * 8);
@@ -1362,6 +1363,7 @@ static RelabelArgs relabel_args(pf_handle* h, int t) {
     a.off = h->at<uint32_t>(h->lay.rl_off);
     a.own = h->at<uint32_t>(h->lay.rl_own);
     a.par = h->at<uint32_t>(h->lay.rl_par);
+    a.kidx = h->at<uint32_t>(h->lay.rl_kidx);
     a.x = h->X(h->cur);
     a.out = h->X(h->cur ^ 1);
     a.send = h->at<float>(h->lay.rl_send);

@@ -280,6 +280,7 @@ struct RelabelArgs {
     uint32_t* off;               // 2 x nchunks + 2: exclusive offsets, then the totals
     uint32_t* own;               // Nloc: list own
     uint32_t* par;               // Nloc: list par (local source index in this shard)
+    uint32_t* kidx;              // Nloc: the rank of an own output in list own (valid where it wants r')
     const void* x;               // stage s-1 states of this shard (Nloc x d)
     void* out;                   // stage s states
     void* send;                  // packed surplus this rank sends (par[k], k >= kmin)

@@ -537,6 +537,8 @@ __global__ void __launch_bounds__(pass1_maxt(D, MODE), pass1_minb(D, MODE)) k_pa
         const uint32_t q = tid + it * threads;
         if (q >= nq) continue;
         uint32_t tp[4] = {4u * q, 4u * q + 1u, 4u * q + 2u, 4u * q + 3u};
+        // (keeping stage k1's own entries in registers instead of the table measured 3%
+        // slower: the extra live registers of the fused d = 4 kernel, profiles/r2_bench_C4_z.json)
         for (uint32_t s = AIR ? 1u : k1; s >= 2u && !PF_PROBE(3); --s) {  // AIRPF: the within-island draw only
             const unsigned char* Ts = tab + (s - 2u) * P1 * TB;
             if constexpr (TB == 1) {

@@ -8,8 +8,9 @@
 //                own position wanting r', par[k] = the source (in this shard) of the k-th
 //                r' output wanting this shard
 //   k_rl_pack    the surplus this rank sends: x[par[k]] for k in [kmin, |par|)
-//   k_rl_apply   outputs: an own-shard draw reads it; own[k] reads x[par[k]] (k < kmin, the
-//                swapped draw) or the received surplus (k >= kmin)
+//   k_rl_apply   every output once, coalesced: an own-shard draw reads it; the k-th output
+//                of list own (kidx) reads x[par[k]] (k < kmin, the swapped draw) or the
+//                received surplus (k >= kmin)
 // Every draw is the Alg. 3 draw of DESIGN.md §3 (word (i & 3) of Philox block (i >> 2, n,
 // RESAMPLE<<24 | s), side low iff (r >> b) < P, index r & (M-1)), on GLOBAL positions.
 #include "pf_launch.h"
@@ -130,7 +131,10 @@ __global__ void __launch_bounds__(kRlThreads) k_rl_lists(const __grid_constant__
     uint32_t ko = bo + io - no, kp = bp + ip - np;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-        if (wo[e]) a.own[ko++] = (uint32_t)(4u * q) + (uint32_t)e;
+        if (wo[e]) {
+            a.own[ko] = (uint32_t)(4u * q) + (uint32_t)e;
+            a.kidx[4u * q + e] = ko++;  // the output's rank in list own (k_rl_apply)
+        }
         if (wp[e]) a.par[kp++] = sp[e];
     }
 }
@@ -143,44 +147,45 @@ __global__ void __launch_bounds__(256) k_rl_pack(const __grid_constant__ Relabel
         snd[k] = x[a.par[a.kmin + k]];
 }
 
-// outputs whose draw stays in this shard
+// every output of this shard in one pass, written once and coalesced (4 consecutive
+// outputs per thread): a draw inside the shard reads its source; an output of list own
+// reads the swapped draw's source (rank k < kmin) or the received surplus (k >= kmin)
 template <typename T, bool DBG>
-__global__ void __launch_bounds__(256) k_rl_apply_stay(const __grid_constant__ RelabelArgs a) {
+__global__ void __launch_bounds__(256) k_rl_apply(const __grid_constant__ RelabelArgs a) {
     const T* x = reinterpret_cast<const T*>(a.x);
+    const T* rcv = reinterpret_cast<const T*>(a.recv);
     T* out = reinterpret_cast<T*>(a.out);
     const uint32_t P = __ldg(a.thr);
     for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; 4u * q < a.Nloc; q += (uint64_t)gridDim.x * blockDim.x) {
         bool w[4];
         uint32_t src[4];
         rl_quad(a, a.rank, q, P, w, src);
+        Vec4<T> v;
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t l = (uint32_t)(4u * q) + (uint32_t)e;
+            int64_t g;  // global source (debug)
             if (!w[e]) {
-                out[4u * q + e] = x[src[e]];
-                if constexpr (DBG) a.dbg_anc[4u * q + e] = (int32_t)((uint64_t)a.rank * a.Nloc + src[e]);
+                v.v[e] = x[src[e]];
+                g = (int64_t)a.rank * (int64_t)a.Nloc + src[e];
+            } else {
+                const uint32_t k = __ldg(a.kidx + l);
+                if (k < a.kmin) {
+                    const uint32_t ps = __ldg(a.par + k);
+                    v.v[e] = x[ps];
+                    g = (int64_t)a.rank * (int64_t)a.Nloc + ps;
+                } else {
+                    v.v[e] = rcv[k - a.kmin];
+                    g = (int64_t)a.partner * (int64_t)a.Nloc + src[e];
+                }
             }
-    }
-}
-
-// outputs of list own: the swapped draw (local) or the received surplus
-template <typename T, bool DBG>
-__global__ void __launch_bounds__(256) k_rl_apply_list(const __grid_constant__ RelabelArgs a, uint64_t nown) {
-    const T* x = reinterpret_cast<const T*>(a.x);
-    const T* rcv = reinterpret_cast<const T*>(a.recv);
-    T* out = reinterpret_cast<T*>(a.out);
-    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nown; k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t l = a.own[k];
-        if (k < a.kmin) {
-            out[l] = x[a.par[k]];
-            if constexpr (DBG) a.dbg_anc[l] = (int32_t)((uint64_t)a.rank * a.Nloc + a.par[k]);
+            if constexpr (DBG) a.dbg_anc[l] = (int32_t)g;
+        }
+        if (a.M >= 4u) {
+            *reinterpret_cast<Vec4<T>*>(out + 4u * q) = v;
         } else {
-            out[l] = rcv[k - a.kmin];
-            if constexpr (DBG) {  // the surplus output keeps its own draw (a source in r')
-                const uint64_t gpos = (uint64_t)a.rank * a.Nloc + l;
-                const uint4 blk = rng_block(a.key, (uint32_t)(gpos >> 2), a.n, kDomainResample, a.s);
-                const uint32_t r = word_of(blk, (int)(gpos & 3u));
-                a.dbg_anc[l] = (int32_t)((uint64_t)a.partner * a.Nloc + (((l >> a.b) << a.b) | (r & (a.M - 1u))));
-            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) out[4u * q + e] = v.v[e];
         }
     }
 }
@@ -199,13 +204,9 @@ static void rl_pack_apply(cudaStream_t st, const RelabelArgs& a, bool pack, uint
         if (a.nsend) k_rl_pack<T><<<g, 256, 0, st>>>(a);
         return;
     }
-    if (dbg) {
-        k_rl_apply_stay<T, true><<<g, 256, 0, st>>>(a);
-        if (nown) k_rl_apply_list<T, true><<<g, 256, 0, st>>>(a, nown);
-    } else {
-        k_rl_apply_stay<T, false><<<g, 256, 0, st>>>(a);
-        if (nown) k_rl_apply_list<T, false><<<g, 256, 0, st>>>(a, nown);
-    }
+    (void)nown;
+    if (dbg) k_rl_apply<T, true><<<g, 256, 0, st>>>(a);
+    else k_rl_apply<T, false><<<g, 256, 0, st>>>(a);
 }
 
 void launch_relabel_move(cudaStream_t st, int D, const RelabelArgs& a, bool pack, uint64_t nown, bool dbg) {

@@ -4,9 +4,12 @@ mkdir -p gpurun_out
 T=${TAG:-sw}
 out=gpurun_out/${T}_sweep.txt
 : > $out
-while read -r name envs; do
+while read -r name rest; do
   [ -z "$name" ] && continue
-  env $envs timeout 300 python bench.py --steps 6 --warmup 3 --no-cpu-baseline --no-e2e ${BENCH_ARGS} > gpurun_out/${T}_${name}.json 2> gpurun_out/${T}_${name}.err
+  envs=""; args=""
+  for tok in $rest; do case $tok in *=*) envs="$envs $tok";; *) args="$args $tok";; esac; done
+  case $name in *_nows) envs="$envs PF_STAGE_WS=0";; esac
+  env $envs timeout 300 python bench.py --steps 6 --warmup 3 --no-cpu-baseline --no-e2e ${BENCH_ARGS} $args > gpurun_out/${T}_${name}.json 2> gpurun_out/${T}_${name}.err
   python - "$name" "gpurun_out/${T}_${name}.json" >> $out <<'PY'
 import json, sys
 name, f = sys.argv[1], sys.argv[2]
