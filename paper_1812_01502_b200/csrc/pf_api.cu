@@ -194,8 +194,10 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, uint64
         sp.threads = pick_threads(sp.P / 4, env_u32("PF_STAGE_THREADS", kStageThreadsDefault), &sp.qpt);
         // warp-specialised pass (k_stages_ws): half the CTA walks, half draws, each on QPT
         // quads per thread; needs whole-quad groups (M >= 4), bulk-copied groups and a CTA
-        // of 2 x P/4/QPT <= 1024 threads
+        // of 2 x P/4/QPT <= 1024 threads; deep passes over tiny groups (k > 7 with M < 16,
+        // d = 1) run faster on the plain pipelined kernel (profiles/r2_ws_kmax.txt)
         if (pipe && env_u32("PF_STAGE_WS", 1u) && M >= 4u && (uint64_t)M * sb >= 16u && sp.P / 4u >= 64u &&
+            k <= env_u32("PF_STAGE_WS_KMAX", M >= 16u ? 16u : 7u) &&
             stages_smem(sp.P, sb, k, sp.tb, 2u) <= budget &&
             (1u << k) <= std::min<uint32_t>(1024u, sp.P / 4u * 2u) / 2u) {  // one threshold per drawer
             sp.pipe = 2u;

@@ -196,18 +196,28 @@ __device__ __forceinline__ float log_potential(const ModelParams& mp, const floa
             v = fmaf(mp.rdiag[k] * r, r, v);
         }
     } else {
+        // static trip counts with dy guards: y and r stay in registers (a dynamic index
+        // would put them, and the kernel's y, in local memory); same summation order
         float r[8];
-        for (int k = 0; k < mp.dy; ++k) {
-            float hx = 0.0f;
 #pragma unroll
-            for (int j = 0; j < D; ++j) hx = fmaf(mp.H[k * D + j], x[j], hx);
+        for (int k = 0; k < 8; ++k) {
+            float hx = 0.0f;
+            if (k < mp.dy) {
+#pragma unroll
+                for (int j = 0; j < D; ++j) hx = fmaf(mp.H[k * D + j], x[j], hx);
+            }
             r[k] = y[k] - hx;
         }
         float q = 0.0f;
-        for (int k = 0; k < mp.dy; ++k) {
-            float t = 0.0f;
-            for (int j = 0; j < mp.dy; ++j) t = fmaf(mp.Rinv[k * mp.dy + j], r[j], t);
-            q = fmaf(r[k], t, q);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (k < mp.dy) {
+                float t = 0.0f;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < mp.dy) t = fmaf(mp.Rinv[k * mp.dy + j], r[j], t);
+                q = fmaf(r[k], t, q);
+            }
         }
         v = -0.5f * q;
     }
