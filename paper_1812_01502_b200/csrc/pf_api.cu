@@ -92,9 +92,12 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, uint64
     // pass-1 tile: the largest 2^k1 <= 64 groups (k1 <= S) whose shared memory fits the budget
     uint32_t P1 = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(N, (uint64_t)kPass1MaxGroups * M),
                                                std::max<uint64_t>(2ull * M, Nglobal / kMaxShards));
-    const uint32_t maxthr1 = d == 4 ? kPass1ThreadsD4 : 512u;  // the kernels' launch bounds
+    // the kernels' launch bounds: 512 threads, except the fused d = 4 pass below 8 quads per
+    // thread (128); a d = 4 tile too large for 128 x 8 quads (M >= 4096) takes more threads
+    // at 8 quads each, which that kernel's QPT = 8 instantiation allows
+    const uint32_t maxthr1 = 512u;
     auto threads_for = [&](uint32_t P, uint32_t* q) {
-        uint32_t t = std::min(pick_threads(P / 4, threads1, q), maxthr1);
+        uint32_t t = std::min(pick_threads(P / 4, threads1, q), d == 4 ? kPass1ThreadsD4 : maxthr1);
         *q = std::max(1u, (P / 4) / t);
         while (*q > maxqpt1 && t < maxthr1) {  // k_pass1 is instantiated for up to 8 quads per thread
             t *= 2;

@@ -82,18 +82,20 @@ __device__ __forceinline__ uint32_t xs_swz(uint32_t s) {
 // Launch bounds of the fused d = 4 pass: 128 threads, 6 CTAs per SM (80 registers, no new
 // spill): 5.55 -> 5.27 ms per C4 launch against (512, 1) = 96 registers and 5 CTAs per SM;
 // 7 CTAs (72 registers) measured 5.42 (profiles/r2_pass1_launch_bounds.txt).  make_plan
-// keeps d = 4 at <= 128 threads per CTA.
+// keeps d = 4 at <= 128 threads per CTA below 8 quads per thread; the QPT = 8 instance
+// (tiles of M >= 4096 only) keeps the general 512-thread bound.
 #ifndef PF_P1_D4_MAXT
 #define PF_P1_D4_MAXT 128
 #define PF_P1_D4_MINB 6
 #endif
-constexpr int pass1_maxt(int D, int MODE) { return (D == 4 && MODE == kPass1Fused) ? PF_P1_D4_MAXT : 512; }
-constexpr int pass1_minb(int D, int MODE) {
-    return (MODE == kPass1Airpf && D >= 4) ? 2 : ((D == 4 && MODE == kPass1Fused) ? PF_P1_D4_MINB : PF_P1_MINB);
+constexpr bool pass1_d4_fused(int D, int MODE, int QPT) { return D == 4 && MODE == kPass1Fused && QPT < 8; }
+constexpr int pass1_maxt(int D, int MODE, int QPT) { return pass1_d4_fused(D, MODE, QPT) ? PF_P1_D4_MAXT : 512; }
+constexpr int pass1_minb(int D, int MODE, int QPT) {
+    return (MODE == kPass1Airpf && D >= 4) ? 2 : (pass1_d4_fused(D, MODE, QPT) ? PF_P1_D4_MINB : PF_P1_MINB);
 }
 
 template <int D, int KIND, bool DBG, int QPT, int TB, int MODE = kPass1Fused>
-__global__ void __launch_bounds__(pass1_maxt(D, MODE), pass1_minb(D, MODE)) k_pass1(const __grid_constant__ Pass1Args a) {
+__global__ void __launch_bounds__(pass1_maxt(D, MODE, QPT), pass1_minb(D, MODE, QPT)) k_pass1(const __grid_constant__ Pass1Args a) {
     constexpr int PS = 2 + 4 * D;  // partial: max, sw, s1[D], s2[D], p1[D], p2[D]
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t threads = blockDim.x;
