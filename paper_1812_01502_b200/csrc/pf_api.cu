@@ -213,6 +213,13 @@ bool make_plan(int d, uint64_t N, uint32_t M, Plan* pl, std::string* err, uint64
         p.passes.push_back(sp);
         s += k;
     }
+    if (env_u32("PF_PLAN_VERBOSE", 0u)) {
+        fprintf(stderr, "[pf plan] N=%llu M=%u d=%d tb=%u pass1: P1=%u k1=%u threads=%u qpt=%u smem=%u tiles=%u\n",
+                (unsigned long long)N, M, p.D, p.tb, p.P1, p.k1, p.pass1_threads, p.pass1_qpt, p.pass1_smem, p.NT);
+        for (const StagePass& sp : p.passes)
+            fprintf(stderr, "[pf plan]   pass s0=%u k=%u P=%u tb=%u pipe=%u threads=%u qpt=%u smem=%u grid=%u\n", sp.s0,
+                    sp.k, sp.P, sp.tb, sp.pipe, sp.threads, sp.qpt, sp.smem, sp.grid);
+    }
     *pl = p;
     return true;
 }
@@ -582,6 +589,7 @@ static void launch_stages_k(pf_handle* h, const StagePass& cp, const void* pin, 
     a.pipe = cp.pipe;
     // k_stages_ws: walkers = the given fraction (in 32ths) of the CTA, whole warps
     a.ws_walkers = std::max<uint32_t>(32u, (cp.threads * env_u32("PF_STAGE_WS_WALK32", 16u) / 32u) & ~31u);
+    a.spec = env_u32("PF_STAGE_SPEC", 1u);
     a.out_rot = out_rot;
     a.out_S = h->S;
     a.pin = pin;
@@ -636,6 +644,7 @@ static void fill_pass1(pf_handle* h, Pass1Args& a, const float* y_host, const fl
     a.P1 = p.P1;
     a.T1 = p.P1 / h->M;
     a.probe = env_u32("PF_PASS1_PROBE", 0u);
+    a.spec = env_u32("PF_PASS1_SPEC", 1u);
     a.sl = pass1_smem(p.D, p.P1, h->M, p.k1, p.pass1_threads, p.tb);
     a.logV = h->at<double>(h->lay.logV);
     a.thr = h->at<uint32_t>(h->lay.thr);
@@ -1022,13 +1031,6 @@ static int init_core(const pf_model* model, uint64_t N, uint32_t M, uint64_t see
     Layout L = make_layout(p, Nloc, M, flags, (uint32_t)world, Sglobal);
     if (!dev_ws || ws_bytes < L.total) return fail(nullptr, PF_EWORKSPACE, "workspace too small");
     if (reinterpret_cast<uintptr_t>(dev_ws) & 255u) return fail(nullptr, PF_EWORKSPACE, "workspace not 256-byte aligned");
-    if (env_u32("PF_PLAN_VERBOSE", 0u)) {
-        fprintf(stderr, "[pf plan] N=%llu M=%u d=%d tb=%u pass1: P1=%u k1=%u threads=%u qpt=%u smem=%u tiles=%u\n",
-                (unsigned long long)Nloc, M, p.D, p.tb, p.P1, p.k1, p.pass1_threads, p.pass1_qpt, p.pass1_smem, p.NT);
-        for (const StagePass& sp : p.passes)
-            fprintf(stderr, "[pf plan]   pass s0=%u k=%u P=%u tb=%u pipe=%u threads=%u qpt=%u smem=%u grid=%u\n", sp.s0,
-                    sp.k, sp.P, sp.tb, sp.pipe, sp.threads, sp.qpt, sp.smem, sp.grid);
-    }
     pf_handle* h = new pf_handle();
     h->mp = to_params(model);
     h->N = Nloc;

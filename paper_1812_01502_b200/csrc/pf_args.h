@@ -13,7 +13,7 @@ constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kPass1MaxGroups = 64;  // T1 <= 64: the V tree of a tile fits one warp's lanes
 
 struct Pass1Smem {
-    uint32_t xs, w, qe, L1, tab, chunk, lv1, red, ess, total;
+    uint32_t xs, w, qe, L1, tab, chunk, lv1, red, ess, thr, total;
 };
 __host__ __device__ inline Pass1Smem pass1_smem(int D, uint32_t P1, uint32_t M, uint32_t k1, uint32_t threads,
                                                 uint32_t tb) {
@@ -34,6 +34,7 @@ __host__ __device__ inline Pass1Smem pass1_smem(int D, uint32_t P1, uint32_t M, 
     s.lv1 = take(T1 * 8u);  // pair (or, AIRPF, island) log-means
     s.red = take((threads / 32u) * (2u + 4u * (uint32_t)D) * 4u);
     s.ess = take((threads / 32u) * 4u);  // per-warp sum of squared weights (kPass1Weigh)
+    s.thr = take(k1 >= 2 ? (k1 - 1u) * (T1 / 4u) * 4u : 0u);  // k_pass1c: stage 2..k1 thresholds from warp 0
     s.total = off;
     return s;
 }
@@ -49,6 +50,7 @@ struct Pass1Args {
     uint32_t pos0;        // global index of the shard's first particle (RNG counters)
     uint32_t m, M, b, S, k1, P1, T1;
     uint32_t probe;       // cost probes of experiment builds (-DPF_PROBES), else unused
+    uint32_t spec;        // 1: a compile-time (B, K1, QPT) instance of the fused pass may run (k_pass1c)
     Pass1Smem sl;         // shared-memory layout (pass1_smem)
     const float* x_in;    // xhat_{n-1} (or x_0)
     // sharded AIRPF (R27): island g reads global block isl_src[g] from its owner's state
@@ -120,6 +122,7 @@ struct StageArgs {
     uint32_t out_rot;     // stage rotation (R23): outputs go to group rotr_S(g, out_rot)
     uint32_t out_S;       //   of the next layout (0: no move; needs M >= 4)
     uint32_t ws_walkers;  // k_stages_ws: walker threads (the rest of the CTA draws)
+    uint32_t spec;        // 1: a compile-time (k, b) instance of k_stages_ws may run (k_stages_wsc)
     const void* pin;      // states at stage s0-1 (packed AoS, shard-local)
     void* pout;           // states at stage s0+k-1
     const uint32_t* thr;  // side thresholds, level-table layout (level_offset)

@@ -108,10 +108,11 @@ __device__ __forceinline__ float neg2_log_u1(uint32_t a) {
 // 2^-10 per pair) the precise neg2_log_u1 runs.
 constexpr uint32_t kFastLogLimit = (1u << 24) - (1u << 14);  // u1 = n 2^-24 < 1 - 2^-10
 
+template <int FAST>  // 1: u1 < 1 - 2^-10 is known (the MUFU branch), 0: decide here
 __device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
     const uint32_t na = (a >> 8) + 1u;
     float r2;
-    if (na < kFastLogLimit) r2 = -1.3862943611198906f * __log2f((float)na * 0x1p-24f);  // -2 ln 2 lg2(u1)
+    if (FAST || na < kFastLogLimit) r2 = -1.3862943611198906f * __log2f((float)na * 0x1p-24f);  // -2 ln 2 lg2(u1)
     else r2 = neg2_log_u1(a);
     const float rad = r2 * rsqrtf(fmaxf(r2, 1e-30f));
     const float th = fmaf((float)(b >> 8), 6.28318530717958647692f * 0x1p-24f, -3.14159265358979323846f);
@@ -120,10 +121,17 @@ __device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
     return make_float2(-rad * c, -rad * s);
 }
 
-// Four normals of one block: coordinates 4j..4j+3.
+// Four normals of one block: coordinates 4j..4j+3.  One branch decides the radius path of
+// both pairs (each pair's value is the one box_muller<0> gives it).
 __device__ __forceinline__ void normals4(const uint4& v, float* z) {
-    const float2 p = box_muller(v.x, v.y);
-    const float2 q = box_muller(v.z, v.w);
+    float2 p, q;
+    if (max(v.x, v.z) < ((kFastLogLimit - 1u) << 8)) {  // both u1 below the limit: (a >> 8) + 1 < limit
+        p = box_muller<1>(v.x, v.y);
+        q = box_muller<1>(v.z, v.w);
+    } else {
+        p = box_muller<0>(v.x, v.y);
+        q = box_muller<0>(v.z, v.w);
+    }
     z[0] = p.x;
     z[1] = p.y;
     z[2] = q.x;

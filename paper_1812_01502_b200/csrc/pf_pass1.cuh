@@ -281,11 +281,11 @@ __global__ void __launch_bounds__(pass1_maxt(D, MODE, QPT), pass1_minb(D, MODE, 
         const uint32_t q = tid + it * threads;
         const bool valid = q < nq;
         const bool dead = pm[it] == -CUDART_INF_F;  // all of the pair's weights are zero
-        const float f = (dead || !valid) ? 0.0f : (QPT == 1 ? 1.0f : expf(pm[it] - mthr));
+        const float f = (dead || !valid) ? 0.0f : (QPT == 1 ? 1.0f : __expf(pm[it] - mthr));
         float r = 0.0f;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const float c = dead ? 1.0f : expf(lw[it][e] - pm[it]);
+            const float c = dead ? 1.0f : __expf(lw[it][e] - pm[it]);  // MUFU ex2: see DESIGN.md §3
             r += c;
             run[it][e] = r;
             const float wf = c * f;

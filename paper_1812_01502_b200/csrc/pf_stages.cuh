@@ -54,11 +54,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // The same wait with a suspend-time hint: a waiting warp sleeps until the phase completes
 // (or the hint elapses) instead of spinning -- in k_stages_ws the spinning waiters took
 // ~30% of the issued instructions from the working warps (ncu source page)
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t hint_ns = 1000000u) {
     asm volatile(
         "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra WAIT_%=;\n}\n" ::"r"(
             smem_u32(bar)),
-        "r"(parity), "r"(1000000u)
+        "r"(parity), "r"(hint_ns)
         : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -540,6 +540,162 @@ __global__ void __launch_bounds__(1024, 1) k_stages_ws(const __grid_constant__ S
             named_bar_sync(1u, ndraw);                               // tile i's thresholds stored
             nxt = (rt < E && i + 1u < nt) ? thr_of(i + 1u) : 0u;     // in flight during the draws
             ws_draws<TB, DBG>(a, stage_tile_geom(a, t0 + i * gridDim.x), thbuf(sl), tbuf(sl), rt, ndraw);
+            mbar_arrive(tab_full + sl);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// k_stages_wsc: k_stages_ws with the pass depth K and b = log2 M fixed at compile time
+// (16-bit tables, no debug tables), for the plans the benchmark configurations run (C4:
+// K = 6, b = 6).  Same draws, same outputs, bit for bit (tests/test_gpu_stage_spec.py);
+// what changes is the instruction count per particle:
+//   * the stage loop unrolls, so every stage's bit, table offset and threshold offset is
+//     an immediate and the Philox counter's (n, stage) words fold where uniform;
+//   * table entries hold the source's BYTE offset in the previous stage's table (tile
+//     position x 2): a walk step is one LDS.U16 at [entry + stage offset], no address
+//     arithmetic (the drawers pay one shift per pair of entries for it);
+//   * the drawers compose two entries with three LOP3-class operations after the sign
+//     trick of ws_entries.
+// Entries of one stage for one quad: e = ((r & mask) << 1) | (side ? hi : lo) << (b + 1),
+// two per 32-bit word (outputs 4q, 4q+1 | 4q+2, 4q+3).
+template <int B>
+__device__ __forceinline__ uint2 wsc_pair_entries(const uint4 blk, uint32_t Pt, uint32_t blo2, uint32_t bitb2) {
+    constexpr uint32_t mask2s = (((1u << B) - 1u) << 1) * 0x10001u;
+    const int32_t ip = (int32_t)Pt;
+    const uint32_t d0 = (uint32_t)((int32_t)(blk.x >> B) - ip), d1 = (uint32_t)((int32_t)(blk.y >> B) - ip);
+    const uint32_t d2 = (uint32_t)((int32_t)(blk.z >> B) - ip), d3 = (uint32_t)((int32_t)(blk.w >> B) - ip);
+    uint32_t s01, s23;  // 0xffff per entry where the lower side is drawn
+    asm("prmt.b32 %0, %1, %2, 0xFFBB;" : "=r"(s01) : "r"(d0), "r"(d1));
+    asm("prmt.b32 %0, %1, %2, 0xFFBB;" : "=r"(s23) : "r"(d2), "r"(d3));
+    const uint32_t w01 = __byte_perm(blk.x, blk.y, 0x5410u) << 1, w23 = __byte_perm(blk.z, blk.w, 0x5410u) << 1;
+    return make_uint2(((w01 & mask2s) | blo2) | (~s01 & bitb2), ((w23 & mask2s) | blo2) | (~s23 & bitb2));
+}
+
+template <int K, int B>
+__device__ __forceinline__ void wsc_draws(const StageArgs& a, const StageTile& g, const uint32_t* ths, uint16_t* tabs,
+                                          uint32_t rt, uint32_t nthr) {
+    constexpr uint32_t M = 1u << B, P = M << K, nq = P >> 2, mask = M - 1u;
+    const uint32_t lowbits = a.lowbits;
+    for (uint32_t q0 = rt; q0 < nq; q0 += 2u * nthr) {
+        const uint32_t q1 = q0 + nthr;
+        const bool two = q1 < nq;
+        const uint32_t l0 = 4u * q0, l1 = 4u * (two ? q1 : q0);
+        const uint32_t j0 = l0 >> B, j1 = l1 >> B;
+        const uint32_t c0 = (a.pos0 + (((g.tlo | (j0 << lowbits) | g.thi) << B) | (l0 & mask))) >> 2;
+        const uint32_t c1 = (a.pos0 + (((g.tlo | (j1 << lowbits) | g.thi) << B) | (l1 & mask))) >> 2;
+        const uint32_t jb0 = (j0 << (B + 1)) * 0x10001u, jb1 = (j1 << (B + 1)) * 0x10001u;
+#pragma unroll
+        for (int st = 0; st + 1 < K; ++st) {  // the last stage: in the walk (wsc_walk)
+            const uint32_t s = a.s0 + (uint32_t)st;
+            const uint32_t bitb2 = ((1u << st) << (B + 1)) * 0x10001u;
+            const uint32_t toff = (1u << K) - (1u << (K - st));
+            const uint4 b0 = rng_block(a.key, c0, a.n, kDomainResample, s);
+            const uint4 b1 = rng_block(a.key, c1, a.n, kDomainResample, s);
+            const uint32_t P0 = ths[toff + (j0 >> (st + 1))], P1 = ths[toff + (j1 >> (st + 1))];
+            *reinterpret_cast<uint2*>(tabs + st * P + l0) = wsc_pair_entries<B>(b0, P0, jb0 & ~bitb2, bitb2);
+            if (two) *reinterpret_cast<uint2*>(tabs + st * P + l1) = wsc_pair_entries<B>(b1, P1, jb1 & ~bitb2, bitb2);
+        }
+    }
+}
+
+template <typename T, int K, int B>
+__device__ __forceinline__ void wsc_walk(const StageArgs& a, const StageTile& g, const T* xs, const uint16_t* tabs,
+                                         const uint32_t* ths, uint32_t tid, uint32_t nthr) {
+    constexpr uint32_t M = 1u << B, P = M << K, nq = P >> 2, mask = M - 1u;
+    constexpr uint32_t bitlb = (1u << (K - 1)) << (B + 1);  // the last stage's bit, as a byte offset
+    const uint32_t lowbits = a.lowbits, sl = a.s0 + (uint32_t)K - 1u;
+    const uint32_t Pl = ths[(1u << K) - 2u];  // the last stage pairs the tile's two halves: one threshold
+    const unsigned char* tb = reinterpret_cast<const unsigned char*>(tabs);
+    T* pout = reinterpret_cast<T*>(a.pout);
+    for (uint32_t q = tid; q < nq; q += nthr) {
+        const uint32_t l0 = 4u * q;
+        const uint32_t j = l0 >> B;
+        const uint32_t gp = ((g.tlo | (j << lowbits) | g.thi) << B) | (l0 & mask);
+        const uint4 blk = rng_block(a.key, (a.pos0 + gp) >> 2, a.n, kDomainResample, sl);
+        const uint32_t rw[4] = {blk.x, blk.y, blk.z, blk.w};
+        const uint32_t jlo = (j << (B + 1)) & ~bitlb;
+        uint32_t t2[4];  // byte offsets (tile position x 2)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) t2[e] = ((rw[e] & mask) << 1) | jlo | (((rw[e] >> B) >= Pl) ? bitlb : 0u);
+#pragma unroll
+        for (int st = K - 2; st >= 0; --st)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) t2[e] = *reinterpret_cast<const uint16_t*>(tb + st * (2u * P) + t2[e]);
+        Vec4<T> v;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v.v[e] = *reinterpret_cast<const T*>(reinterpret_cast<const unsigned char*>(xs) + t2[e] * (sizeof(T) / 2));
+        uint32_t gp0 = gp;
+        if (a.out_rot) gp0 = (rotr_group(gp0 >> B, a.out_rot, a.out_S) << B) | (gp0 & mask);
+        *reinterpret_cast<Vec4<T>*>(pout + gp0) = v;
+    }
+}
+
+template <typename T, int K, int B>
+__global__ void __launch_bounds__(1024, 1) k_stages_wsc(const __grid_constant__ StageArgs a) {
+    static_assert(B >= 2 && ((1u << B) * sizeof(T)) >= 16u && ((1u << (B + K)) * 2u) <= 65536u, "wsc: M >= 4, bulk groups, 16-bit byte offsets");
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr uint32_t P = (1u << B) << K;
+    constexpr uint32_t stb = (P * (uint32_t)sizeof(T) + 15u) & ~15u;
+    constexpr uint32_t ttb = (K * P * 2u + 15u) & ~15u;  // the layout of stages_smem(P, ., K, 2, 2)
+    const uint32_t ntiles = (uint32_t)(a.N / P);
+    unsigned char* tab0 = smem + 2u * stb;
+    uint32_t* th0 = reinterpret_cast<uint32_t*>(tab0 + 2u * ttb);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(th0 + (2u << K));
+    uint64_t* st_full = bars;        // [2]
+    uint64_t* tab_full = bars + 2;   // [2]
+    uint64_t* slot_free = bars + 4;  // [2]
+    auto xbuf = [&](uint32_t sl) { return reinterpret_cast<T*>(smem + sl * stb); };
+    auto tbuf = [&](uint32_t sl) { return reinterpret_cast<uint16_t*>(tab0 + sl * ttb); };
+    auto thbuf = [&](uint32_t sl) { return th0 + (sl << K); };
+
+    const uint32_t t0 = blockIdx.x;
+    if (t0 >= ntiles) return;
+    const uint32_t nt = (ntiles - t0 + gridDim.x - 1u) / gridDim.x;
+    const uint32_t nwalk = a.ws_walkers, ndraw = blockDim.x - nwalk;
+    const bool walker = threadIdx.x < nwalk;
+    const uint32_t rt = walker ? threadIdx.x : threadIdx.x - nwalk;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(st_full + i, 1u);
+            mbar_init(tab_full + i, ndraw);
+            mbar_init(slot_free + i, nwalk);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (walker) {
+        for (uint32_t i = 0; i < 2u && i < nt; ++i)
+            stage_states_load<T>(a, stage_tile_geom(a, t0 + i * gridDim.x), xbuf(i), st_full + i);
+        for (uint32_t i = 0; i < nt; ++i) {
+            const uint32_t sl = i & 1u, par = (i >> 1) & 1u;
+            mbar_wait_sleep(st_full + sl, par);
+            mbar_wait_sleep(tab_full + sl, par);
+            wsc_walk<T, K, B>(a, stage_tile_geom(a, t0 + i * gridDim.x), xbuf(sl), tbuf(sl), thbuf(sl), rt, nwalk);
+            mbar_arrive(slot_free + sl);
+            if (i + 2u < nt && threadIdx.x < 32u) {
+                mbar_wait_sleep(slot_free + sl, par);
+                stage_states_load<T>(a, stage_tile_geom(a, t0 + (i + 2u) * gridDim.x), xbuf(sl), st_full + sl);
+            }
+        }
+    } else {
+        constexpr uint32_t E = (1u << K) - 1u;
+        auto thr_of = [&](uint32_t tile_i) -> uint32_t {
+            const StageTile g = stage_tile_geom(a, t0 + tile_i * gridDim.x);
+            const uint32_t e = rt, u = (1u << K) - e;
+            const uint32_t st = K - (32u - __clz(u - 1u));
+            const uint32_t off = (1u << K) - (1u << (K - st));
+            const uint32_t s = a.s0 + st;
+            return __ldg(a.thr + level_offset(a.m, (int)s) + (g.thi >> s) + (e - off));
+        };
+        uint32_t nxt = rt < E ? thr_of(0) : 0u;
+        for (uint32_t i = 0; i < nt; ++i) {
+            const uint32_t sl = i & 1u, par = (i >> 1) & 1u;
+            if (i >= 2u) mbar_wait_sleep(slot_free + sl, par ^ 1u);
+            if (rt < E) thbuf(sl)[rt] = nxt;
+            named_bar_sync(1u, ndraw);
+            nxt = (rt < E && i + 1u < nt) ? thr_of(i + 1u) : 0u;
+            wsc_draws<K, B>(a, stage_tile_geom(a, t0 + i * gridDim.x), thbuf(sl), tbuf(sl), rt, ndraw);
             mbar_arrive(tab_full + sl);
         }
     }
