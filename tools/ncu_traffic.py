@@ -23,7 +23,12 @@ acc = {}
 inst = {}
 for row in r:
     d = dict(zip(hdr, row))
-    name = d["Kernel Name"].replace("void ", "").split("<")[0].split("(")[0].replace("k_stages_ws", "k_stages")
+    name = d["Kernel Name"].replace("void ", "").split("<")[0].split("(")[0].split("::")[-1]
+    # bench.py keys kernels by kind: the warp-specialised and compile-time instances of a pass
+    # (k_stages_ws, k_stages_wsc, k_pass1c) report under their pass's name
+    for kind in ("k_stages", "k_pass1"):
+        if name.startswith(kind):
+            name = kind
     tot = sum(float(d[m].replace(",", "")) * scale[units[m]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     acc.setdefault(name, []).append(tot)
     if "smsp__inst_executed.sum" in d:
