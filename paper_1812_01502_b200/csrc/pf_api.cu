@@ -46,6 +46,7 @@ constexpr uint32_t kLPCMin = 64u;   // min leaves per cascade CTA
 
 struct StagePass {
     uint32_t s0, k, P, threads, qpt, smem, tb, grid, pipe;
+    uint32_t kd = 0;  // stages drawn (0: k)
 };
 
 struct Plan {
@@ -584,6 +585,7 @@ static void launch_stages_k(pf_handle* h, const StagePass& cp, const void* pin, 
     a.b = h->b;
     a.s0 = cp.s0;
     a.k = cp.k;
+    a.kd = cp.kd ? cp.kd : cp.k;
     a.P = cp.P;
     a.lowbits = cp.s0 - 1;
     a.pipe = cp.pipe;
@@ -602,26 +604,10 @@ static void launch_stages_k(pf_handle* h, const StagePass& cp, const void* pin, 
 
 // A k_stages pass over stages s0..s0+k-1 (k <= the plan's pass), sized like make_plan.
 static StagePass stage_pass_for(const pf_handle* h, const StagePass& sp, uint32_t k) {
-    if (k == sp.k) return sp;
+    // the plan's pass (tile depth sp.k, geometry, launch size) drawing only its first k stages
     StagePass q = sp;
-    const uint32_t sb = (uint32_t)(4 * h->plan.D);
-    q.k = k;
-    q.P = h->M << k;
-    q.threads = pick_threads(q.P / 4, env_u32("PF_STAGE_THREADS", kStageThreadsDefault), &q.qpt);
-    if (q.pipe == 2u) {
-        if (q.P / 4u >= 64u) {
-            q.qpt = 1u;
-            q.threads = std::min<uint32_t>(1024u, q.P / 4u * 2u);
-        } else {
-            q.pipe = 1u;
-        }
-    }
-    q.smem = stages_smem(q.P, sb, k, q.tb, q.pipe);
-    int nsm = 148, dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-        nsm = 148;
-    const uint32_t per_sm = std::max(1u, std::min(kSmemPerSM / (q.smem + 1024u), 2048u / q.threads));
-    q.grid = (uint32_t)std::min<uint64_t>(h->N / q.P, (uint64_t)nsm * per_sm);
+    q.kd = k;
+    (void)h;
     return q;
 }
 
@@ -1760,6 +1746,9 @@ int pf_set_adaptive(pf_handle* h, double theta) {
     if (theta == 0.0 && h->carry_mode != 0)
         return fail(h, PF_ESTATE, "particles carry weights of an early-stopped step: run one step with theta = 1 first");
     h->theta = theta;
+    if (theta > 0.0) {  // truncated passes run the runtime-plan stage kernels: load them now
+        for (const StagePass& sp : h->plan.passes) preload_stages(h->plan.D, (int)sp.tb, (h->flags & PF_FLAG_DEBUG) != 0);
+    }
     return PF_OK;
 }
 

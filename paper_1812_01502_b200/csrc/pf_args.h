@@ -13,7 +13,7 @@ constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kPass1MaxGroups = 64;  // T1 <= 64: the V tree of a tile fits one warp's lanes
 
 struct Pass1Smem {
-    uint32_t xs, w, qe, L1, tab, chunk, lv1, red, ess, thr, total;
+    uint32_t xs, w, qe, ey, L1, tab, chunk, lv1, red, ess, thr, total;
 };
 __host__ __device__ inline Pass1Smem pass1_smem(int D, uint32_t P1, uint32_t M, uint32_t k1, uint32_t threads,
                                                 uint32_t tb) {
@@ -28,6 +28,7 @@ __host__ __device__ inline Pass1Smem pass1_smem(int D, uint32_t P1, uint32_t M, 
     s.xs = take(P1 * 4u * (uint32_t)D);
     s.w = take(P1 * 4u);
     s.qe = take(P1);  // quad ends of the CDF (P1 / 4 floats): the first search level
+    s.ey = take(M > 64u ? P1 : 0u);  // the same in BFS (Eytzinger) order per pool, pools of > 32 quads
     s.L1 = take(P1 * tb);
     s.tab = take(k1 >= 2 ? (k1 - 1u) * P1 * tb : 0u);
     s.chunk = take(M > 64 ? (P1 / 128u) * 4u : 0u);  // per-warp-chunk maxima / totals
@@ -117,6 +118,8 @@ struct StageArgs {
     uint64_t N;     // particles of this shard
     uint32_t pos0;  // global index of the shard's first particle (RNG counters)
     uint32_t m, M, b, s0, k, P, lowbits;
+    uint32_t kd;          // stages drawn, s0 .. s0+kd-1 (<= k, the tile depth; < k for a pass an
+                          // early-stopped adaptive step truncates: the tile keeps the plan's depth)
     uint32_t pipe;        // 2: warp-specialised (k_stages_ws); 1: software-pipelined (two buffers
                           // of everything); 0: one buffer
     uint32_t out_rot;     // stage rotation (R23): outputs go to group rotr_S(g, out_rot)

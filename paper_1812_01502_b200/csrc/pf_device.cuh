@@ -71,6 +71,26 @@ __device__ __forceinline__ uint32_t word_of(const uint4& v, int w) {
     return w == 0 ? v.x : (w == 1 ? v.y : (w == 2 ? v.z : v.w));
 }
 
+// MUFU approximations without the denormal fix-ups of __log2f / rsqrtf / __expf (the
+// .ftz PTX forms): for normal inputs and outputs the same MUFU results, three instructions
+// fewer each.  Every input below is normal by construction (u1 >= 2^-24, r2 >= 1e-30); the
+// stage-1 weights e^x (x = lw - max <= 0) flush to 0 below e^-87 instead of going denormal.
+__device__ __forceinline__ float lg2_ftz(float x) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float exp_ftz(float x) {  // e^x = 2^(x log2 e), as __expf
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x * 1.4426950408889634f));
+    return r;
+}
+
 // u in [0,1) from the 24 high bits (exact in fp32).
 __device__ __forceinline__ float u01f(uint32_t r) { return (float)(r >> 8) * 0x1p-24f; }
 
@@ -112,9 +132,9 @@ template <int FAST>  // 1: u1 < 1 - 2^-10 is known (the MUFU branch), 0: decide 
 __device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
     const uint32_t na = (a >> 8) + 1u;
     float r2;
-    if (FAST || na < kFastLogLimit) r2 = -1.3862943611198906f * __log2f((float)na * 0x1p-24f);  // -2 ln 2 lg2(u1)
+    if (FAST || na < kFastLogLimit) r2 = -1.3862943611198906f * lg2_ftz((float)na * 0x1p-24f);  // -2 ln 2 lg2(u1)
     else r2 = neg2_log_u1(a);
-    const float rad = r2 * rsqrtf(fmaxf(r2, 1e-30f));
+    const float rad = r2 * rsqrt_ftz(fmaxf(r2, 1e-30f));
     const float th = fmaf((float)(b >> 8), 6.28318530717958647692f * 0x1p-24f, -3.14159265358979323846f);
     float s, c;
     __sincosf(th, &s, &c);

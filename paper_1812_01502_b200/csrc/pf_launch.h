@@ -32,6 +32,21 @@ void launch_stages_f1(int tb, bool dbg, int qpt, const LaunchCfg& c, const Stage
 void launch_stages_f2(int tb, bool dbg, int qpt, const LaunchCfg& c, const StageArgs& a);
 void launch_stages_f4(int tb, bool dbg, int qpt, const LaunchCfg& c, const StageArgs& a);
 void launch_stages_f8(int tb, bool dbg, int qpt, const LaunchCfg& c, const StageArgs& a);
+// Force the (lazily loaded) runtime-plan stage kernels of a payload into the context, so a
+// pass the fully adapted scheme truncates (drawn by k_stages_ws / k_stages, not by the
+// compile-time instance the full pass uses) does not pay the module load inside a step.
+void preload_stages_f1(int tb, bool dbg);
+void preload_stages_f2(int tb, bool dbg);
+void preload_stages_f4(int tb, bool dbg);
+void preload_stages_f8(int tb, bool dbg);
+inline void preload_stages(int D, int tb, bool dbg) {
+    switch (D) {
+        case 1: preload_stages_f1(tb, dbg); break;
+        case 2: preload_stages_f2(tb, dbg); break;
+        case 4: preload_stages_f4(tb, dbg); break;
+        default: preload_stages_f8(tb, dbg); break;
+    }
+}
 inline void launch_stages(int D, int tb, bool dbg, int qpt, const LaunchCfg& c, const StageArgs& a) {
     switch (D) {
         case 1: launch_stages_f1(tb, dbg, qpt, c, a); break;

@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(pass1_maxt(D, MODE, QPT), pass1_minb(D, MODE, 
     float* xs = reinterpret_cast<float*>(smem + SL.xs);
     float* w = reinterpret_cast<float*>(smem + SL.w);
     float* qe = reinterpret_cast<float*>(smem + SL.qe);
+    float* ey = reinterpret_cast<float*>(smem + SL.ey);
     unsigned char* L1 = smem + SL.L1;
     unsigned char* tab = smem + SL.tab;
     float* chunk = reinterpret_cast<float*>(smem + SL.chunk);
@@ -281,11 +282,11 @@ __global__ void __launch_bounds__(pass1_maxt(D, MODE, QPT), pass1_minb(D, MODE, 
         const uint32_t q = tid + it * threads;
         const bool valid = q < nq;
         const bool dead = pm[it] == -CUDART_INF_F;  // all of the pair's weights are zero
-        const float f = (dead || !valid) ? 0.0f : (QPT == 1 ? 1.0f : __expf(pm[it] - mthr));
+        const float f = (dead || !valid) ? 0.0f : (QPT == 1 ? 1.0f : exp_ftz(pm[it] - mthr));
         float r = 0.0f;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const float c = dead ? 1.0f : __expf(lw[it][e] - pm[it]);  // MUFU ex2: see DESIGN.md §3
+            const float c = dead ? 1.0f : exp_ftz(lw[it][e] - pm[it]);  // MUFU ex2: see DESIGN.md §5
             r += c;
             run[it][e] = r;
             const float wf = c * f;
@@ -354,6 +355,17 @@ __global__ void __launch_bounds__(pass1_maxt(D, MODE, QPT), pass1_minb(D, MODE, 
         reinterpret_cast<float4*>(w)[q] =
             make_float4(excl[it] + run[it][0], excl[it] + run[it][1], excl[it] + run[it][2], excl[it] + run[it][3]);
         qe[q] = excl[it] + run[it][3];
+        if (Z > 32u && MODE != kPass1Weigh) {
+            // pools of > 32 quads: the quad ends again in BFS (Eytzinger) order of the search
+            // tree -- the probe of level L, node m (quad m 2 step + step - 1, step = Z >> (L+1))
+            // at pool offset 2^L - 1 + m -- so one level's probes are consecutive words (the
+            // flat order put every probe of a level with step >= 32 in one bank)
+            const uint32_t j = q & (Z - 1u);
+            if (j + 1u < Z) {
+                const uint32_t v = j + 1u, ls = __ffs(v) - 1u, lz = __ffs(Z) - 1u;
+                ey[(q - j) + (1u << (lz - 1u - ls)) - 1u + (v >> (ls + 1u))] = excl[it] + run[it][3];
+            }
+        }
         if (((4u * q) & ((1u << pool_sh) - 1u)) == 0u) {  // first quad of its pool: log mean of the pool
             const double lm = pm[it] == -CUDART_INF_F ? -CUDART_INF : (double)pm[it] + (double)(logf(tot[it]) - log2M);
             lv1[(4u * q) >> pool_sh] = lm;
@@ -393,12 +405,33 @@ __global__ void __launch_bounds__(pass1_maxt(D, MODE, QPT), pass1_minb(D, MODE, 
         for (int it = 0; it < QPT; ++it)
 #pragma unroll
             for (int e = 0; e < 4; ++e) jq[it][e] = lo[it][e] >> 2;  // the pool's first quad
-        for (uint32_t step = Z >> 1; step >= 1u && !PF_PROBE(1); step >>= 1) {
+        if (Z <= 32u) {
+            for (uint32_t step = Z >> 1; step >= 1u && !PF_PROBE(1); step >>= 1) {
+#pragma unroll
+                for (int it = 0; it < QPT; ++it)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (qe[jq[it][e] + step - 1u] <= tq[it][e]) jq[it][e] += step;
+            }
+        } else {  // the same probes, read from the BFS-ordered copy (level L, node jr >> (lz - L))
+            const uint32_t lz = __ffs(Z) - 1u;
+            uint32_t jr[QPT][4];
 #pragma unroll
             for (int it = 0; it < QPT; ++it)
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (qe[jq[it][e] + step - 1u] <= tq[it][e]) jq[it][e] += step;
+                for (int e = 0; e < 4; ++e) jr[it][e] = 0u;
+            for (uint32_t L = 0; L < lz && !PF_PROBE(1); ++L) {
+                const uint32_t step = Z >> (L + 1u), sh = lz - L, lvl = (1u << L) - 1u;
+#pragma unroll
+                for (int it = 0; it < QPT; ++it)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (ey[jq[it][e] + lvl + (jr[it][e] >> sh)] <= tq[it][e]) jr[it][e] += step;
+            }
+#pragma unroll
+            for (int it = 0; it < QPT; ++it)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) jq[it][e] += jr[it][e];
         }
 #pragma unroll
         for (int it = 0; it < QPT; ++it)

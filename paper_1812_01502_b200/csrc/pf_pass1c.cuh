@@ -144,11 +144,11 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
 #pragma unroll
     for (int it = 0; it < QPT; ++it) {
         const bool dead = pm[it] == -CUDART_INF_F;
-        const float f = dead ? 0.0f : (QPT == 1 ? 1.0f : __expf(pm[it] - mthr));
+        const float f = dead ? 0.0f : (QPT == 1 ? 1.0f : exp_ftz(pm[it] - mthr));
         float r = 0.0f;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const float c = dead ? 1.0f : __expf(lw[it][e] - pm[it]);  // MUFU ex2: see DESIGN.md §3
+            const float c = dead ? 1.0f : exp_ftz(lw[it][e] - pm[it]);  // MUFU ex2: see DESIGN.md §5
             r += c;
             run[it][e] = r;
             const float wf = c * f;

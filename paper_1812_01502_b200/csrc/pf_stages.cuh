@@ -121,7 +121,7 @@ __device__ __forceinline__ void stage_thresholds_load(const StageArgs& a, const 
 template <int TB, bool DBG, int QPT>
 __device__ __forceinline__ void stage_draws(const StageArgs& a, const StageTile& g, const uint32_t* ths,
                                             unsigned char* tabs) {
-    const uint32_t M = a.M, b = a.b, k = a.k, P = a.P, mask = M - 1u, nq = P >> 2, lowbits = a.lowbits;
+    const uint32_t M = a.M, b = a.b, k = a.k, kd = a.kd, P = a.P, mask = M - 1u, nq = P >> 2, lowbits = a.lowbits;
     const uint32_t tlo = g.tlo, thi = g.thi;
 #pragma unroll
     for (int it = 0; it < QPT; ++it) {
@@ -133,7 +133,7 @@ __device__ __forceinline__ void stage_draws(const StageArgs& a, const StageTile&
             const uint32_t gp0 = ((tlo | (j << lowbits) | thi) << b) | (l0 & mask);
             const uint32_t c0 = (a.pos0 + gp0) >> 2;
             uint32_t toff = 0;  // offset of stage st's thresholds
-            for (uint32_t st = 0; st < k; ++st) {
+            for (uint32_t st = 0; st < kd; ++st) {
                 const uint32_t s = a.s0 + st, bit = 1u << st;
                 const uint4 blk = rng_block(a.key, c0, a.n, kDomainResample, s);
                 const uint32_t Pt = ths[toff + (j >> (st + 1))];
@@ -170,7 +170,7 @@ __device__ __forceinline__ void stage_draws(const StageArgs& a, const StageTile&
                 c0[h] = (a.pos0 + gpa[h]) >> 2;
             }
             uint32_t toff = 0;
-            for (uint32_t st = 0; st < k; ++st) {
+            for (uint32_t st = 0; st < kd; ++st) {
                 const uint32_t s = a.s0 + st, bit = 1u << st;
                 uint32_t en[4];
 #pragma unroll
@@ -208,7 +208,7 @@ __device__ __forceinline__ void stage_draws(const StageArgs& a, const StageTile&
 template <typename T, int TB, int QPT>
 __device__ __forceinline__ void stage_walk(const StageArgs& a, const StageTile& g, const T* xs,
                                            const unsigned char* tabs) {
-    const uint32_t M = a.M, b = a.b, k = a.k, P = a.P, mask = M - 1u, nq = P >> 2, lowbits = a.lowbits;
+    const uint32_t M = a.M, b = a.b, kd = a.kd, P = a.P, mask = M - 1u, nq = P >> 2, lowbits = a.lowbits;
     T* pout = reinterpret_cast<T*>(a.pout);
 #pragma unroll
     for (int it = 0; it < QPT; ++it) {
@@ -216,7 +216,7 @@ __device__ __forceinline__ void stage_walk(const StageArgs& a, const StageTile& 
         if (q >= nq) break;
         const uint32_t l0 = 4u * q;
         uint32_t tp[4] = {l0, l0 + 1u, l0 + 2u, l0 + 3u};
-        for (int st = (int)k - 1; st >= 0; --st) {
+        for (int st = (int)kd - 1; st >= 0; --st) {
             if constexpr (TB == 1) {
                 const unsigned char* Ts = tabs + (uint32_t)st * P;
                 const uint32_t sh = (uint32_t)st + b;
@@ -380,7 +380,7 @@ __device__ __forceinline__ void ws_entries(const StageArgs& a, const uint4 blk, 
 template <int TB, bool DBG>
 __device__ __forceinline__ void ws_draws(const StageArgs& a, const StageTile& g, const uint32_t* ths,
                                          unsigned char* tabs, uint32_t rt, uint32_t nthr) {
-    const uint32_t b = a.b, k = a.k, nq = a.P >> 2, lowbits = a.lowbits, mask = a.M - 1u;
+    const uint32_t b = a.b, k = a.k, kd = a.kd, nq = a.P >> 2, lowbits = a.lowbits, mask = a.M - 1u;
     const uint32_t tlo = g.tlo, thi = g.thi;
     for (uint32_t q0 = rt; q0 < nq; q0 += 2u * nthr) {
         const uint32_t q1 = q0 + nthr;
@@ -391,7 +391,7 @@ __device__ __forceinline__ void ws_draws(const StageArgs& a, const StageTile& g,
         const uint32_t gp1 = ((tlo | (j1 << lowbits) | thi) << b) | (l1 & mask);
         const uint32_t c0 = (a.pos0 + gp0) >> 2, c1 = (a.pos0 + gp1) >> 2;
         uint32_t toff = 0;
-        for (uint32_t st = 0; st + 1u < k; ++st) {  // the last stage: in the walk (ws_walk)
+        for (uint32_t st = 0; st + 1u < kd; ++st) {  // the last stage: in the walk (ws_walk)
             const uint32_t s = a.s0 + st;
             const uint4 b0 = rng_block(a.key, c0, a.n, kDomainResample, s);
             const uint4 b1 = rng_block(a.key, c1, a.n, kDomainResample, s);
@@ -428,12 +428,14 @@ template <typename T, int TB, bool DBG>
 __device__ __forceinline__ void ws_walk(const StageArgs& a, const StageTile& g, const T* xs, const unsigned char* tabs,
                                         const uint32_t* ths, uint32_t tid, uint32_t nthr) {
     const uint32_t M = a.M, b = a.b, k = a.k, P = a.P, mask = M - 1u, nq = P >> 2, lowbits = a.lowbits;
-    const uint32_t stl = k - 1u, sl = a.s0 + stl, bitl = 1u << stl;
-    const uint32_t Pl = ths[(1u << k) - 2u];  // the last stage pairs the tile's two halves: one threshold
+    const uint32_t stl = a.kd - 1u, sl = a.s0 + stl, bitl = 1u << stl;
+    // the last drawn stage's thresholds (one when kd = k: the tile's two halves pair)
+    const uint32_t* thl = ths + ((1u << k) - (1u << (k - stl)));
     T* pout = reinterpret_cast<T*>(a.pout);
     for (uint32_t q = tid; q < nq; q += nthr) {
         const uint32_t l0 = 4u * q;
         const uint32_t j = l0 >> b;
+        const uint32_t Pl = thl[j >> (stl + 1u)];
         const uint32_t gp = ((g.tlo | (j << lowbits) | g.thi) << b) | (l0 & mask);
         const uint4 blk = rng_block(a.key, (a.pos0 + gp) >> 2, a.n, kDomainResample, sl);
         const uint32_t rw[4] = {blk.x, blk.y, blk.z, blk.w};
@@ -446,7 +448,7 @@ __device__ __forceinline__ void ws_walk(const StageArgs& a, const StageTile& g, 
                 a.dbg_anc[(uint64_t)(sl - 1) * a.N + gp + e] =
                     (int32_t)(a.pos0 + (((g.tlo | (jj << lowbits) | g.thi) << b) | (rw[e] & mask)));
         }
-        for (int st = (int)k - 2; st >= 0; --st) {
+        for (int st = (int)stl - 1; st >= 0; --st) {
             if constexpr (TB == 1) {
                 const unsigned char* Ts = tabs + (uint32_t)st * P;
                 const uint32_t sh = (uint32_t)st + b;

@@ -23,7 +23,9 @@ from paper_1812_01502_b200 import pf as pfb  # noqa: E402
 
 
 def _run(name, N, M, spec, T=3, **kw):
-    os.environ["PF_STAGE_SPEC"] = os.environ["PF_PASS1_SPEC"] = "1" if spec else "0"
+    """spec: 0 runtime-plan kernels, 1 compile-time instances."""
+    os.environ["PF_STAGE_SPEC"] = str(int(spec))
+    os.environ["PF_PASS1_SPEC"] = "1" if spec else "0"
     try:
         cfg = inputs.CONFIGS[name]
         p = inputs.model_params(cfg)
@@ -46,20 +48,22 @@ def _run(name, N, M, spec, T=3, **kw):
 # (config, N, M): plans with compile-time instances -- C4 (k_pass1c B = 6, K1 = 4; k_stages_wsc
 # K = 6, b = 6; one CTA wave and several tiles per CTA), C2 (k_stages_wsc K = 3 and 2, b = 8,
 # d = 8), C3 at full size (k_pass1c SV, B = 5, K1 = 6; k_stages_wsc K = 7 and 6, b = 5)
+@pytest.mark.parametrize("spec", [1])
 @pytest.mark.parametrize("name,N,M", [("C4", 1 << 16, 64), ("C4", 1 << 22, 64), ("C2", 1 << 18, 256),
                                       ("C3", 1 << 24, 32)])
-def test_spec_equals_generic(name, N, M):
-    xa, ea = _run(name, N, M, True)
-    xb, eb = _run(name, N, M, False)
+def test_spec_equals_generic(name, N, M, spec):
+    xa, ea = _run(name, N, M, spec)
+    xb, eb = _run(name, N, M, 0)
     assert np.isfinite(xa).all()
     assert np.array_equal(xa, xb)
     assert np.array_equal(ea, eb)
 
 
-def test_spec_equals_generic_rotation():
+@pytest.mark.parametrize("spec", [1])
+def test_spec_equals_generic_rotation(spec):
     """The fully adapted scheme with stage rotation (theta = 1: every stage, the last pass
     writes the next layout through out_rot)."""
-    xa, ea = _run("C4", 1 << 16, 64, True, theta=1.0, rotate=True)
-    xb, eb = _run("C4", 1 << 16, 64, False, theta=1.0, rotate=True)
+    xa, ea = _run("C4", 1 << 16, 64, spec, theta=1.0, rotate=True)
+    xb, eb = _run("C4", 1 << 16, 64, 0, theta=1.0, rotate=True)
     assert np.array_equal(xa, xb)
     assert np.array_equal(ea, eb)
