@@ -13,7 +13,8 @@
 //     position x 2), so a walk step is a single LDS.U16, and the stage 2..K1 entries are
 //     built two per word with the sign trick of k_stages_ws (pf_stages.cuh).
 // Restrictions (the launcher falls back to k_pass1 otherwise): 16-bit tables (TB = 2), a
-// stage-1 pool of at most 32 quads (B <= 6), no debug tables, no AIRPF / adaptive modes.
+// stage-1 pool of at most 32 quads (B <= 6), no debug tables, no adaptive modes; the AIRPF
+// mode has an instance of its own (MODE = kPass1Airpf).
 #pragma once
 #include <cstdint>
 
@@ -47,13 +48,18 @@ __device__ __forceinline__ float log_potential_lg_diag(const ModelParams& mp, co
     return (v == v && v != INFINITY && v != -INFINITY) ? v : -INFINITY;
 }
 
-// DIAG: the LG model takes the diagonal paths (the launcher checks mp.diag_lq && mp.diag_obs)
-template <int D, int KIND, int B, int K1, int QPT, int MINB, bool DIAG>
+// DIAG: the LG model takes the diagonal paths (the launcher checks mp.diag_lq && mp.diag_obs).
+// MODE: kPass1Fused (the step's pass 1) or kPass1Airpf (AIRPF, k_pass1's AIRPF mode: island
+// blocks read through the previous island map, carried island weights (AIRPF2), the
+// within-island resample with pools of one island, island levels 1..K1 with 31-bit
+// thresholds (R20), no stage tables: the tile is written in natural order).
+template <int D, int KIND, int B, int K1, int QPT, int MINB, bool DIAG, int MODE = kPass1Fused>
 __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(const __grid_constant__ Pass1Args a) {
+    constexpr bool AIR = MODE == kPass1Airpf;
     constexpr uint32_t M = 1u << B, P1 = M << K1, T1 = 1u << K1, nq = P1 / 4u;
     constexpr uint32_t NTHR = nq / QPT, NWARP = NTHR / 32u;
-    constexpr uint32_t Z = M >> 1;  // quads per stage-1 pool (2M positions)
-    constexpr uint32_t pool_sh = B + 1u;
+    constexpr uint32_t Z = AIR ? (M >> 2) : (M >> 1);  // quads per stage-1 pool (2M positions; AIRPF: one island)
+    constexpr uint32_t pool_sh = AIR ? B : B + 1u;
     constexpr int PS = 2 + 4 * D;
     static_assert(B >= 2 && B <= 6 && K1 >= 1 && K1 <= 6 && NTHR % 32u == 0u && 2u * P1 <= 65536u, "k_pass1c plan");
     extern __shared__ __align__(16) unsigned char smem[];
@@ -76,9 +82,21 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
 #pragma unroll
     for (int it = 0; it < QPT; ++it) {
         const uint32_t q = tid + it * NTHR;
+        uint32_t src_q = base + 4u * q;  // AIRPF: the quad's position inside the island block it reads
+        const float* xsrc = a.x_in;
+        if constexpr (AIR)
+            if (a.isl_src) {
+                const uint32_t gblk = (uint32_t)a.isl_src[src_q >> B];
+                if (a.xpeer[0]) {  // sharded (R27): the block's owner, over NVLink when remote
+                    xsrc = a.xpeer[gblk >> a.peer_shift];
+                    src_q = ((gblk & ((1u << a.peer_shift) - 1u)) << B) | (src_q & (M - 1u));
+                } else {
+                    src_q = (gblk << B) | (src_q & (M - 1u));
+                }
+            }
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-            const float4 t = __ldg(reinterpret_cast<const float4*>(a.x_in + (uint64_t)(base + 4u * q) * D) + c);
+            const float4 t = __ldg(reinterpret_cast<const float4*>(xsrc + (uint64_t)src_q * D) + c);
             xh[it][4 * c] = t.x;
             xh[it][4 * c + 1] = t.y;
             xh[it][4 * c + 2] = t.z;
@@ -117,6 +135,25 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
         for (int e = 0; e < 4; ++e) {
             if constexpr (KIND == 1 && DIAG) lw[it][e] = log_potential_lg_diag<D>(a.mp, y, x + e * D);
             else lw[it][e] = log_potential<D, KIND>(a.mp, y, x + e * D);
+        }
+        if constexpr (AIR) {  // carried island weight (AIRPF2, R26; k_pass1 section 2)
+            if (a.carry_mode != 0) {
+                float cw[4];
+                if (a.carry_mode == 1) {
+                    const float4 t = __ldg(reinterpret_cast<const float4*>(a.carry_lw + i0));
+                    cw[0] = (float)((double)t.x - a.carry_c);
+                    cw[1] = (float)((double)t.y - a.carry_c);
+                    cw[2] = (float)((double)t.z - a.carry_c);
+                    cw[3] = (float)((double)t.w - a.carry_c);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        cw[e] = (float)(__ldg(a.carry_lv + (((((uint64_t)a.pos0 + i0 + e) >> B) >> a.carry_shift) &
+                                                            a.carry_mask)) - a.carry_c);
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) lw[it][e] += cw[e];
+            }
         }
 #pragma unroll
         for (int k = 0; k < 4 * D; ++k) xr[it][k] = x[k];
@@ -187,6 +224,7 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
         if (((4u * q) & ((1u << pool_sh) - 1u)) == 0u) {
             const double lm = pm[it] == -CUDART_INF_F ? -CUDART_INF : (double)pm[it] + (double)(logf(tot[it]) - log2M);
             lv1[(4u * q) >> pool_sh] = lm;
+            if constexpr (AIR) a.logW[((uint64_t)base >> B) + ((4u * q) >> B)] = lm;
         }
     }
     __syncwarp();
@@ -196,7 +234,8 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
 #pragma unroll
         for (int it = 0; it < QPT; ++it) {
             const uint32_t q = tid + it * NTHR;
-            const uint4 blk = rng_block(a.key, c0t + q, a.n, kDomainResample, 1u);
+            const uint4 blk = AIR ? rng_block(a.key, c0t + q, a.n, kDomainWithin, 0u)
+                                  : rng_block(a.key, c0t + q, a.n, kDomainResample, 1u);
             const uint32_t pq = ((4u * q) >> pool_sh) << (pool_sh - 2u);  // the pool's first quad
             const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
             const float totc = w[4u * pq + 4u * Z - 1u];  // the pool total as stored (reading R3)
@@ -249,15 +288,25 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
     }
     __syncthreads();  // L1, lv1, red complete
 
-    // ---- 4. V levels 2..K1 and thresholds (k_pass1 section 4) ---------------------------
-    // by warp 0 alone (k_pass1 has every warp build them redundantly), the thresholds
-    // handed to the other warps in shared memory: 4.30 -> 4.12 ms per C4 launch
-    uint32_t thr[K1 + 1];
+    // ---- 4. V levels 2..K1 and thresholds (k_pass1 section 4), by warp 0 alone (k_pass1
+    // has every warp build them redundantly), the thresholds handed to the other warps in
+    // shared memory: 4.30 -> 4.12 ms per C4 launch.  AIRPF: level 1 = pair means of the
+    // island log-means, every level with 31-bit thresholds (R20), nothing handed over.
     uint32_t* thr_s = reinterpret_cast<uint32_t*>(smem + SL.thr);
     if (warp == 0) {
         constexpr uint32_t npair = T1 >> 1;
-        double v = lane < npair ? lv1[lane] : -CUDART_INF;
-        if (warp == 0 && lane < npair) a.logV[level_offset(a.m, 1) + (uint64_t)tile * npair + lane] = v;
+        constexpr int tb_bits = AIR ? 1 : B;
+        double v;
+        if constexpr (AIR) {
+            double nv = -CUDART_INF;
+            uint32_t Pt = 0u;
+            if (lane < npair) pair_level_fast(lv1[2u * lane], lv1[2u * lane + 1u], 1, &nv, &Pt);
+            v = nv;
+            if (lane < npair) a.thr[level_offset(a.m, 1) + (uint64_t)tile * npair + lane] = Pt;
+        } else {
+            v = lane < npair ? lv1[lane] : -CUDART_INF;
+        }
+        if (lane < npair) a.logV[level_offset(a.m, 1) + (uint64_t)tile * npair + lane] = v;
 #pragma unroll
         for (int s = 2; s <= K1; ++s) {
             const uint32_t stp = 1u << (s - 2);
@@ -265,22 +314,20 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
             const bool act = (lane & (2u * stp - 1u)) == 0u && lane < npair;
             uint32_t Pt;
             double nv;
-            pair_level_fast(v, vr, B, &nv, &Pt);
-            thr[s] = Pt;
+            pair_level_fast(v, vr, tb_bits, &nv, &Pt);
             if (act) {
                 v = nv;
-                if (warp == 0) {
-                    const uint64_t at = level_offset(a.m, s) + (uint64_t)tile * (T1 >> s) + (lane >> (s - 1));
-                    a.logV[at] = nv;
-                    a.thr[at] = Pt;
-                    thr_s[(s - 2) * (T1 / 4u) + (lane >> (s - 1))] = Pt;
-                }
+                const uint64_t at = level_offset(a.m, s) + (uint64_t)tile * (T1 >> s) + (lane >> (s - 1));
+                a.logV[at] = nv;
+                a.thr[at] = Pt;
+                if constexpr (!AIR) thr_s[(s - 2) * (T1 / 4u) + (lane >> (s - 1))] = Pt;
             }
         }
     }
-    __syncthreads();  // thresholds ready
+    if constexpr (!AIR) __syncthreads();  // thresholds ready
 
     // ---- 5. stages 2..K1: entries = source byte offsets, two per word ----------------------
+    if constexpr (!AIR) {
 #pragma unroll
     for (int it = 0; it < QPT; ++it) {
         const uint32_t q = tid + it * NTHR;
@@ -297,16 +344,19 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
         }
     }
     __syncthreads();  // all stage tables ready
+    }  // !AIR
 
     // ---- 6. compose backwards (byte offsets) and write the tile at its stage-K1 positions
 #pragma unroll
     for (int it = 0; it < QPT; ++it) {
         const uint32_t q = tid + it * NTHR;
         uint32_t t2[4] = {8u * q, 8u * q + 2u, 8u * q + 4u, 8u * q + 6u};
+        if constexpr (!AIR) {  // AIRPF: the within-island draw only
 #pragma unroll
-        for (int s = K1; s >= 2; --s)
+            for (int s = K1; s >= 2; --s)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) t2[e] = *reinterpret_cast<const uint16_t*>(tab + (uint32_t)(s - 2) * 2u * P1 + t2[e]);
+                for (int e = 0; e < 4; ++e) t2[e] = *reinterpret_cast<const uint16_t*>(tab + (uint32_t)(s - 2) * 2u * P1 + t2[e]);
+        }
 #pragma unroll
         for (int e = 0; e < 4; ++e) t2[e] = *reinterpret_cast<const uint16_t*>(L1 + t2[e]);
         float v[4 * D];
@@ -331,7 +381,7 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
             }
         }
         uint32_t dst = base + 4u * q;
-        if (a.out_rot) dst = (rotr_group(dst >> B, a.out_rot, a.S) << B) | (dst & (M - 1u));
+        if (!AIR && a.out_rot) dst = (rotr_group(dst >> B, a.out_rot, a.S) << B) | (dst & (M - 1u));
 #pragma unroll
         for (int c = 0; c < D; ++c)
             reinterpret_cast<float4*>(a.x_out + (uint64_t)dst * D)[c] =
@@ -357,6 +407,9 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
                 }
             }
             a.part[(uint64_t)tile * PS + k] = v;
+        }
+        if constexpr (AIR) {  // AIRPF2: the running max of lw shifts the island ESS sums
+            if (lane == 0 && a.ess_lmax) atomicMax(a.ess_lmax, float_order_bits(tmax));
         }
     }
 }

@@ -36,6 +36,7 @@ def _run(name, N, M, spec, T=3, **kw):
             f.step(np.asarray(ys[t], np.float32))
             est.append(f.estimate(pfb.PF_PHI_X, pfb.PF_EST_FILTER))
             est.append(f.estimate(pfb.PF_PHI_X2, pfb.PF_EST_PREDICT))
+            est.append(f.estimate(pfb.PF_PHI_X, pfb.PF_EST_RESAMPLED))
         torch.cuda.synchronize()
         x = f.debug_get(pfb.PF_DBG_XHAT)
         f.close()
@@ -65,5 +66,17 @@ def test_spec_equals_generic_rotation(spec):
     writes the next layout through out_rot)."""
     xa, ea = _run("C4", 1 << 16, 64, spec, theta=1.0, rotate=True)
     xb, eb = _run("C4", 1 << 16, 64, 0, theta=1.0, rotate=True)
+    assert np.array_equal(xa, xb)
+    assert np.array_equal(ea, eb)
+
+
+@pytest.mark.parametrize("kw", [{"airpf": 1}, {"airpf": 2}, {"airpf": 1, "theta": 0.5}])
+def test_spec_equals_generic_airpf(kw):
+    """k_pass1c's AIRPF instance (Alg. 7 / Alg. 6, and AIRPF2 with carried island weights)
+    against k_pass1's AIRPF mode: the within-resampled sample, the island map (through the
+    resampled estimate) and every estimate, bitwise, over four steps."""
+    xa, ea = _run("C4", 1 << 18, 64, 1, T=4, **kw)
+    xb, eb = _run("C4", 1 << 18, 64, 0, T=4, **kw)
+    assert np.isfinite(xa).all()
     assert np.array_equal(xa, xb)
     assert np.array_equal(ea, eb)
