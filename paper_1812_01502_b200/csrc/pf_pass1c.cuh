@@ -55,7 +55,7 @@ __device__ __forceinline__ float log_potential_lg_diag(const ModelParams& mp, co
 // thresholds (R20), no stage tables: the tile is written in natural order).
 template <int D, int KIND, int B, int K1, int QPT, int MINB, bool DIAG, int MODE = kPass1Fused>
 __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(const __grid_constant__ Pass1Args a) {
-    constexpr bool AIR = MODE == kPass1Airpf;
+    constexpr bool AIR = MODE == kPass1Airpf, WEIGH = MODE == kPass1Weigh, RES = MODE == kPass1Resample;
     constexpr uint32_t M = 1u << B, P1 = M << K1, T1 = 1u << K1, nq = P1 / 4u;
     constexpr uint32_t NTHR = nq / QPT, NWARP = NTHR / 32u;
     constexpr uint32_t Z = AIR ? (M >> 2) : (M >> 1);  // quads per stage-1 pool (2M positions; AIRPF: one island)
@@ -71,6 +71,10 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
     unsigned char* tab = smem + SL.tab;
     double* lv1 = reinterpret_cast<double*>(smem + SL.lv1);
     float* red = reinterpret_cast<float*>(smem + SL.red);
+    float* essw = reinterpret_cast<float*>(smem + SL.ess);
+    // stages drawn: K1 (the tile depth) except in the resample half of an early-stopped
+    // adaptive step, which draws stages 1..min(K1, S*) of the same tile
+    const uint32_t kd = RES ? a.k1 : (uint32_t)K1;
 
     const uint32_t tile = blockIdx.x;
     const uint32_t base = tile * P1;
@@ -131,12 +135,20 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
 #pragma unroll
             for (int k = 0; k < 4 * D; ++k) x[k] = xh[it][k];
         }
+        if constexpr (RES) {  // the weigh half's log-weights, read back
+            const float4 t = __ldg(reinterpret_cast<const float4*>(a.lw_in + i0));
+            lw[it][0] = t.x;
+            lw[it][1] = t.y;
+            lw[it][2] = t.z;
+            lw[it][3] = t.w;
+        } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            if constexpr (KIND == 1 && DIAG) lw[it][e] = log_potential_lg_diag<D>(a.mp, y, x + e * D);
-            else lw[it][e] = log_potential<D, KIND>(a.mp, y, x + e * D);
+            for (int e = 0; e < 4; ++e) {
+                if constexpr (KIND == 1 && DIAG) lw[it][e] = log_potential_lg_diag<D>(a.mp, y, x + e * D);
+                else lw[it][e] = log_potential<D, KIND>(a.mp, y, x + e * D);
+            }
         }
-        if constexpr (AIR) {  // carried island weight (AIRPF2, R26; k_pass1 section 2)
+        if constexpr (AIR || WEIGH) {  // carried weight (R18; AIRPF2: R26; k_pass1 section 2)
             if (a.carry_mode != 0) {
                 float cw[4];
                 if (a.carry_mode == 1) {
@@ -155,11 +167,20 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
                 for (int e = 0; e < 4; ++e) lw[it][e] += cw[e];
             }
         }
+        if constexpr (WEIGH) {  // x_n and lw in natural order for the resample half
+            reinterpret_cast<float4*>(a.lw_out + i0)[0] = make_float4(lw[it][0], lw[it][1], lw[it][2], lw[it][3]);
+#pragma unroll
+            for (int c = 0; c < D; ++c)
+                reinterpret_cast<float4*>(a.x_out + (uint64_t)i0 * D)[c] =
+                    make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+        }
 #pragma unroll
         for (int k = 0; k < 4 * D; ++k) xr[it][k] = x[k];
+        if constexpr (!WEIGH) {
 #pragma unroll
-        for (int c = 0; c < D; ++c)
-            reinterpret_cast<float4*>(xs)[q * D + c] = make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+            for (int c = 0; c < D; ++c)
+                reinterpret_cast<float4*>(xs)[q * D + c] = make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+        }
     }
 
     // ---- 3. stage 1 (k_pass1 section 3, Z <= 32: one pool per warp segment) -------------
@@ -174,7 +195,7 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
     float mthr = -CUDART_INF_F;
 #pragma unroll
     for (int it = 0; it < QPT; ++it) mthr = fmaxf(mthr, pm[it]);
-    float acc[PS];
+    float acc[PS], accsq = 0.0f;
 #pragma unroll
     for (int k = 0; k < PS; ++k) acc[k] = 0.0f;
     float run[QPT][4], incl[QPT];
@@ -190,6 +211,7 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
             run[it][e] = r;
             const float wf = c * f;
             acc[1] += wf;
+            if constexpr (WEIGH) accsq = fmaf(wf, wf, accsq);
 #pragma unroll
             for (int k = 0; k < D; ++k) {
                 const float xv = xr[it][e * D + k];
@@ -218,9 +240,11 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
 #pragma unroll
     for (int it = 0; it < QPT; ++it) {
         const uint32_t q = tid + it * NTHR;
-        reinterpret_cast<float4*>(w)[q] =
-            make_float4(excl[it] + run[it][0], excl[it] + run[it][1], excl[it] + run[it][2], excl[it] + run[it][3]);
-        qe[q] = excl[it] + run[it][3];
+        if constexpr (!WEIGH) {
+            reinterpret_cast<float4*>(w)[q] =
+                make_float4(excl[it] + run[it][0], excl[it] + run[it][1], excl[it] + run[it][2], excl[it] + run[it][3]);
+            qe[q] = excl[it] + run[it][3];
+        }
         if (((4u * q) & ((1u << pool_sh) - 1u)) == 0u) {
             const double lm = pm[it] == -CUDART_INF_F ? -CUDART_INF : (double)pm[it] + (double)(logf(tot[it]) - log2M);
             lv1[(4u * q) >> pool_sh] = lm;
@@ -228,7 +252,7 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
         }
     }
     __syncwarp();
-    {
+    if constexpr (!WEIGH) {
         uint32_t jb[QPT][4];  // byte offset of the quad-end probe base (4 x quad index)
         float tq[QPT][4];
 #pragma unroll
@@ -285,6 +309,11 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
             red[warp * PS] = wmax;
             red[warp * PS + 1] = sw;
         }
+        if constexpr (WEIGH) {
+            float sq = accsq * f * f;
+            for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(kFull, sq, o);
+            if (lane == 0) essw[warp] = sq;
+        }
     }
     __syncthreads();  // L1, lv1, red complete
 
@@ -309,6 +338,7 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
         if (lane < npair) a.logV[level_offset(a.m, 1) + (uint64_t)tile * npair + lane] = v;
 #pragma unroll
         for (int s = 2; s <= K1; ++s) {
+            if ((uint32_t)s > kd) break;
             const uint32_t stp = 1u << (s - 2);
             const double vr = __shfl_down_sync(kFull, v, stp);
             const bool act = (lane & (2u * stp - 1u)) == 0u && lane < npair;
@@ -324,10 +354,10 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
             }
         }
     }
-    if constexpr (!AIR) __syncthreads();  // thresholds ready
+    if constexpr (!AIR && !WEIGH) __syncthreads();  // thresholds ready
 
     // ---- 5. stages 2..K1: entries = source byte offsets, two per word ----------------------
-    if constexpr (!AIR) {
+    if constexpr (!AIR && !WEIGH) {
 #pragma unroll
     for (int it = 0; it < QPT; ++it) {
         const uint32_t q = tid + it * NTHR;
@@ -336,6 +366,7 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
         const uint32_t jb2 = (j0 << (B + 1)) * 0x10001u;
 #pragma unroll
         for (int s = 2; s <= K1; ++s) {
+            if ((uint32_t)s > kd) break;
             const uint32_t P0 = thr_s[(s - 2) * (T1 / 4u) + (j0 >> s)];
             const uint32_t bitb2 = ((1u << (s - 1)) << (B + 1)) * 0x10001u;
             const uint4 blk = rng_block(a.key, c0t + q, a.n, kDomainResample, (uint32_t)s);
@@ -347,15 +378,18 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
     }  // !AIR
 
     // ---- 6. compose backwards (byte offsets) and write the tile at its stage-K1 positions
+    if constexpr (!WEIGH) {
 #pragma unroll
     for (int it = 0; it < QPT; ++it) {
         const uint32_t q = tid + it * NTHR;
         uint32_t t2[4] = {8u * q, 8u * q + 2u, 8u * q + 4u, 8u * q + 6u};
         if constexpr (!AIR) {  // AIRPF: the within-island draw only
 #pragma unroll
-            for (int s = K1; s >= 2; --s)
+            for (int s = K1; s >= 2; --s) {
+                if ((uint32_t)s > kd) continue;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) t2[e] = *reinterpret_cast<const uint16_t*>(tab + (uint32_t)(s - 2) * 2u * P1 + t2[e]);
+            }
         }
 #pragma unroll
         for (int e = 0; e < 4; ++e) t2[e] = *reinterpret_cast<const uint16_t*>(L1 + t2[e]);
@@ -387,6 +421,7 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
             reinterpret_cast<float4*>(a.x_out + (uint64_t)dst * D)[c] =
                 make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
     }
+    }  // !WEIGH
 
     // ---- 7. warp 0: the tile's estimate partial (k_pass1 section 7) -----------------------
     if (warp == 0) {
@@ -410,6 +445,22 @@ __global__ void __launch_bounds__(((1 << (B + K1)) / 4) / QPT, MINB) k_pass1c(co
         }
         if constexpr (AIR) {  // AIRPF2: the running max of lw shifts the island ESS sums
             if (lane == 0 && a.ess_lmax) atomicMax(a.ess_lmax, float_order_bits(tmax));
+        }
+        if constexpr (WEIGH) {  // ESS partial {max, sum w, sum w^2} (R17)
+            if (lane == 0) {
+                double sw = 0.0, sq = 0.0;
+#pragma unroll
+                for (uint32_t wv = 0; wv < NWARP; ++wv) {
+                    const float wm = red[wv * PS];
+                    const double f = (wm == -CUDART_INF_F) ? 0.0 : exp((double)wm - (double)tmax);
+                    sw += (double)red[wv * PS + 1] * f;
+                    sq += (double)essw[wv] * f * f;
+                }
+                a.ess_part[(uint64_t)tile * 3] = (double)tmax;
+                a.ess_part[(uint64_t)tile * 3 + 1] = sw;
+                a.ess_part[(uint64_t)tile * 3 + 2] = sq;
+                atomicMax(a.ess_lmax, float_order_bits(tmax));
+            }
         }
     }
 }

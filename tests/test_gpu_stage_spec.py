@@ -80,3 +80,15 @@ def test_spec_equals_generic_airpf(kw):
     assert np.isfinite(xa).all()
     assert np.array_equal(xa, xb)
     assert np.array_equal(ea, eb)
+
+
+@pytest.mark.parametrize("kw", [{"theta": 0.5}, {"theta": 0.9}, {"theta": 0.5, "rotate": True}])
+def test_spec_equals_generic_adaptive(kw):
+    """k_pass1c's weigh and resample instances (the two halves of a fully adapted step, with
+    early stops S* < K1 that draw fewer stages of the same tile, carried weights of both kinds
+    and stage rotation) against k_pass1's modes, bitwise, over six steps."""
+    xa, ea = _run("C4", 1 << 18, 64, 1, T=6, **kw)
+    xb, eb = _run("C4", 1 << 18, 64, 0, T=6, **kw)
+    assert np.isfinite(xa).all()
+    assert np.array_equal(xa, xb)
+    assert np.array_equal(ea, eb)
