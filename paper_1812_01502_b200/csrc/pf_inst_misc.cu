@@ -311,6 +311,19 @@ constexpr uint32_t kPullMaxG = 64;
 
 // Stage-S_loc source (owner rank c, local position lc) of output l: the L cross-stage
 // draws composed from the last stage back (counter-based, thresholds from pf_step_top).
+// Cross stages t0 .. 1 from (rank c, local position lc) at stage S_loc + t0.
+__device__ __forceinline__ void compose_cross_from(const PullArgs& a, uint32_t t0, uint32_t& c, uint32_t& lc) {
+    for (uint32_t t = t0; t >= 1u; --t) {  // the stage S_loc + t draw at the current position
+        const uint64_t gpos = (uint64_t)c * a.Nloc + lc;
+        const uint4 blk = rng_block(a.key, (uint32_t)(gpos >> 2), a.n, kDomainResample, a.S_loc + t);
+        const uint32_t r = word_of(blk, (int)(gpos & 3u));
+        const uint32_t P = __ldg(a.top_thr + (a.G - (a.G >> (t - 1))) + (c >> t));
+        const uint32_t bit = 1u << (t - 1);
+        c = ((r >> a.b) < P) ? (c & ~bit) : (c | bit);
+        lc = ((lc >> a.b) << a.b) | (r & (a.M - 1u));
+    }
+}
+
 __device__ __forceinline__ void compose_cross(const PullArgs& a, uint64_t l, uint32_t& c, uint32_t& lc) {
     c = a.rank;
     lc = (uint32_t)l;
@@ -436,51 +449,61 @@ __global__ void __launch_bounds__(256) k_pull_scatter(const float* __restrict__ 
 template <int D>
 __global__ void __launch_bounds__(256) k_peer_gather(const __grid_constant__ PullArgs a,
                                                      const __grid_constant__ PeerArgs p) {
-    constexpr int U = 4;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t l0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l0 < a.Nloc; l0 += stride * U) {
-        const float* src[U];
+    // one quad of consecutive outputs per thread: the last cross stage's draws of the four
+    // are the four words of ONE Philox block (the draw contract keys them by the output
+    // quad), so only the earlier cross stages, at the outputs' scattered positions, draw a
+    // block per output (L - 1 + 1/4 blocks per output instead of L)
+    const uint64_t nq = a.Nloc >> 2;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t l0 = 4u * q;
+        uint32_t c[4], lc[4];
+        {
+            const uint32_t t = a.L;
+            const uint64_t gpos = (uint64_t)a.rank * a.Nloc + l0;
+            const uint4 blk = rng_block(a.key, (uint32_t)(gpos >> 2), a.n, kDomainResample, a.S_loc + t);
+            const uint32_t r[4] = {blk.x, blk.y, blk.z, blk.w};
+            const uint32_t P = __ldg(a.top_thr + (a.G - (a.G >> (t - 1))) + (a.rank >> t));
+            const uint32_t bit = 1u << (t - 1);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint64_t l = l0 + (uint64_t)u * stride;
-            uint32_t c = 0u, lc = 0u;
-            if (l < a.Nloc) compose_cross(a, l, c, lc);
-            src[u] = p.x[c] + (uint64_t)lc * D;
+            for (int e = 0; e < 4; ++e) {
+                c[e] = ((r[e] >> a.b) < P) ? (a.rank & ~bit) : (a.rank | bit);
+                lc[e] = (((uint32_t)(l0 + e) >> a.b) << a.b) | (r[e] & (a.M - 1u));
+            }
         }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) compose_cross_from(a, a.L - 1u, c[e], lc[e]);
         if constexpr (D % 4 == 0) {
-            float4 v[U][D / 4];
+            float4 v[4][D / 4];  // (the four loads of a thread in flight together)
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (l0 + (uint64_t)u * stride < a.Nloc)
+            for (int e = 0; e < 4; ++e)
 #pragma unroll
-                    for (int q = 0; q < D / 4; ++q) v[u][q] = __ldg(reinterpret_cast<const float4*>(src[u]) + q);
+                for (int k = 0; k < D / 4; ++k) v[e][k] = __ldg(reinterpret_cast<const float4*>(p.x[c[e]] + (uint64_t)lc[e] * D) + k);
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint64_t l = l0 + (uint64_t)u * stride;
-                if (l < a.Nloc)
+            for (int e = 0; e < 4; ++e)
 #pragma unroll
-                    for (int q = 0; q < D / 4; ++q) reinterpret_cast<float4*>(p.out)[l * (D / 4) + q] = v[u][q];
-            }
+                for (int k = 0; k < D / 4; ++k) reinterpret_cast<float4*>(p.out)[(l0 + e) * (D / 4) + k] = v[e][k];
         } else {
-            float v[U][D];
+            float v[4][D];
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (l0 + (uint64_t)u * stride < a.Nloc)
+            for (int e = 0; e < 4; ++e)
 #pragma unroll
-                    for (int q = 0; q < D; ++q) v[u][q] = __ldg(src[u] + q);
+                for (int k = 0; k < D; ++k) v[e][k] = __ldg(p.x[c[e]] + (uint64_t)lc[e] * D + k);
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint64_t l = l0 + (uint64_t)u * stride;
-                if (l < a.Nloc)
+            for (int e = 0; e < 4; ++e)
 #pragma unroll
-                    for (int q = 0; q < D; ++q) p.out[l * D + q] = v[u][q];
-            }
+                for (int k = 0; k < D; ++k) p.out[(l0 + e) * D + k] = v[e][k];
         }
+    }
+    // a shard of fewer than 4 or a non-multiple of 4 outputs (not produced by the plans; kept exact)
+    for (uint64_t l = 4u * nq + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < a.Nloc; l += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t c, lc;
+        compose_cross(a, l, c, lc);
+        for (int k = 0; k < D; ++k) p.out[l * D + k] = __ldg(p.x[c] + (uint64_t)lc * D + k);
     }
 }
 
 void launch_peer_gather(cudaStream_t st, int D, const PullArgs& a, const PeerArgs& p, bool debug) {
-    const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((a.Nloc + 1023) / 1024, 148ull * 8));
+    const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((a.Nloc / 4 + 255) / 256, 148ull * 8));
     switch (D) {
         case 1: k_peer_gather<1><<<grid, 256, 0, st>>>(a, p); break;
         case 2: k_peer_gather<2><<<grid, 256, 0, st>>>(a, p); break;

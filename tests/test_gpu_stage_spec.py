@@ -47,11 +47,11 @@ def _run(name, N, M, spec, T=3, **kw):
 
 
 # (config, N, M): plans with compile-time instances -- C4 (k_pass1c B = 6, K1 = 4; k_stages_wsc
-# K = 6, b = 6; one CTA wave and several tiles per CTA), C2 (k_stages_wsc K = 3 and 2, b = 8,
+# K = 6 or 5, b = 6; one CTA wave and several tiles per CTA), C2 (k_stages_wsc K = 3 and 2, b = 8,
 # d = 8), C3 at full size (k_pass1c SV, B = 5, K1 = 6; k_stages_wsc K = 7 and 6, b = 5)
 @pytest.mark.parametrize("spec", [1])
-@pytest.mark.parametrize("name,N,M", [("C4", 1 << 16, 64), ("C4", 1 << 22, 64), ("C2", 1 << 18, 256),
-                                      ("C3", 1 << 24, 32)])
+@pytest.mark.parametrize("name,N,M", [("C4", 1 << 16, 64), ("C4", 1 << 20, 64), ("C4", 1 << 22, 64),
+                                      ("C2", 1 << 18, 256), ("C3", 1 << 24, 32)])
 def test_spec_equals_generic(name, N, M, spec):
     xa, ea = _run(name, N, M, spec)
     xb, eb = _run(name, N, M, 0)
