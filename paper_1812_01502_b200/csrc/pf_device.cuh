@@ -62,6 +62,30 @@ __device__ __forceinline__ uint4 philox10(uint4 c, const Key& key) {
     return c;
 }
 
+// NB independent blocks advanced round by round in lockstep: the same values as NB calls of
+// philox10, but the NB multiply chains are interleaved in program order, so a warp has
+// 2 NB independent IMAD.WIDE in flight per round instead of 2 (the drawers of k_stages_wsc
+// and the pass-1 noise are bound by the latency of that chain, not by its pipe).
+template <int NB>
+__device__ __forceinline__ void philox10_lockstep(uint4 (&c)[NB], const Key& key) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        uint64_t p0[NB], p1[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            p0[i] = (uint64_t)0xD2511F53u * c[i].x;
+            p1[i] = (uint64_t)0xCD9E8D57u * c[i].z;
+        }
+#pragma unroll
+        for (int i = 0; i < NB; ++i)
+            c[i] = make_uint4((uint32_t)(p1[i] >> 32) ^ c[i].y ^ key.k[2 * r], (uint32_t)p1[i],
+                              (uint32_t)(p0[i] >> 32) ^ c[i].w ^ key.k[2 * r + 1], (uint32_t)p0[i]);
+    }
+}
+__device__ __forceinline__ uint4 rng_counter(uint32_t c0, uint32_t n, uint32_t domain, uint32_t sub) {
+    return make_uint4(c0, n, (domain << 24) | sub, 0u);
+}
+
 // Block (c0, n, domain<<24 | sub, 0) of the draw contract.
 __device__ __forceinline__ uint4 rng_block(const Key& key, uint32_t c0, uint32_t n, uint32_t domain, uint32_t sub) {
     return philox10(make_uint4(c0, n, (domain << 24) | sub, 0u), key);

@@ -574,6 +574,45 @@ __device__ __forceinline__ uint2 wsc_pair_entries(const uint4 blk, uint32_t Pt, 
     return make_uint2(((w01 & mask2s) | blo2) | (~s01 & bitb2), ((w23 & mask2s) | blo2) | (~s23 & bitb2));
 }
 
+// The drawers' stages ST..K-2 of two quads (q0, q1), NS stages at a time: 2 NS Philox chains
+// in lockstep (philox10_lockstep: the drawers are bound by the latency of the multiply
+// chain, not by its pipe; one stage at a time, 2 chains, measured 2.056 ms per C4 pass,
+// two stages 1.972, three stages (-DPF_WSC_CHUNK=3) 1.975; profiles/r2_wsc_lockstep_s4.txt).
+// The last stage of the pass is drawn in the walk (wsc_walk).
+#ifndef PF_WSC_CHUNK
+#define PF_WSC_CHUNK 2
+#endif
+struct WscQuadPair {
+    uint32_t l0, l1, j0, j1, c0, c1, jb0, jb1;
+    bool two;
+};
+template <int K, int B, int ST>
+__device__ __forceinline__ void wsc_draw_from(const StageArgs& a, const WscQuadPair& w, const uint32_t* ths, uint16_t* tabs) {
+    constexpr uint32_t P = (1u << B) << K;
+    constexpr int rem = K - 1 - ST;
+    if constexpr (rem > 0) {
+        constexpr int NS = (PF_WSC_CHUNK == 3 && (rem == 3 || rem >= 5)) ? 3 : (rem >= 2 ? 2 : 1);
+        uint4 c[2 * NS];
+#pragma unroll
+        for (int h = 0; h < NS; ++h) {
+            c[2 * h] = rng_counter(w.c0, a.n, kDomainResample, a.s0 + (uint32_t)(ST + h));
+            c[2 * h + 1] = rng_counter(w.c1, a.n, kDomainResample, a.s0 + (uint32_t)(ST + h));
+        }
+        philox10_lockstep<2 * NS>(c, a.key);
+#pragma unroll
+        for (int h = 0; h < NS; ++h) {
+            constexpr uint32_t one = 1u;
+            const int sh = ST + h;
+            const uint32_t bitb2 = ((one << sh) << (B + 1)) * 0x10001u;
+            const uint32_t toff = (one << K) - (one << (K - sh));
+            const uint32_t P0 = ths[toff + (w.j0 >> (sh + 1))], P1 = ths[toff + (w.j1 >> (sh + 1))];
+            *reinterpret_cast<uint2*>(tabs + sh * P + w.l0) = wsc_pair_entries<B>(c[2 * h], P0, w.jb0 & ~bitb2, bitb2);
+            if (w.two) *reinterpret_cast<uint2*>(tabs + sh * P + w.l1) = wsc_pair_entries<B>(c[2 * h + 1], P1, w.jb1 & ~bitb2, bitb2);
+        }
+        wsc_draw_from<K, B, ST + NS>(a, w, ths, tabs);
+    }
+}
+
 template <int K, int B>
 __device__ __forceinline__ void wsc_draws(const StageArgs& a, const StageTile& g, const uint32_t* ths, uint16_t* tabs,
                                           uint32_t rt, uint32_t nthr) {
@@ -581,23 +620,17 @@ __device__ __forceinline__ void wsc_draws(const StageArgs& a, const StageTile& g
     const uint32_t lowbits = a.lowbits;
     for (uint32_t q0 = rt; q0 < nq; q0 += 2u * nthr) {
         const uint32_t q1 = q0 + nthr;
-        const bool two = q1 < nq;
-        const uint32_t l0 = 4u * q0, l1 = 4u * (two ? q1 : q0);
-        const uint32_t j0 = l0 >> B, j1 = l1 >> B;
-        const uint32_t c0 = (a.pos0 + (((g.tlo | (j0 << lowbits) | g.thi) << B) | (l0 & mask))) >> 2;
-        const uint32_t c1 = (a.pos0 + (((g.tlo | (j1 << lowbits) | g.thi) << B) | (l1 & mask))) >> 2;
-        const uint32_t jb0 = (j0 << (B + 1)) * 0x10001u, jb1 = (j1 << (B + 1)) * 0x10001u;
-#pragma unroll
-        for (int st = 0; st + 1 < K; ++st) {  // the last stage: in the walk (wsc_walk)
-            const uint32_t s = a.s0 + (uint32_t)st;
-            const uint32_t bitb2 = ((1u << st) << (B + 1)) * 0x10001u;
-            const uint32_t toff = (1u << K) - (1u << (K - st));
-            const uint4 b0 = rng_block(a.key, c0, a.n, kDomainResample, s);
-            const uint4 b1 = rng_block(a.key, c1, a.n, kDomainResample, s);
-            const uint32_t P0 = ths[toff + (j0 >> (st + 1))], P1 = ths[toff + (j1 >> (st + 1))];
-            *reinterpret_cast<uint2*>(tabs + st * P + l0) = wsc_pair_entries<B>(b0, P0, jb0 & ~bitb2, bitb2);
-            if (two) *reinterpret_cast<uint2*>(tabs + st * P + l1) = wsc_pair_entries<B>(b1, P1, jb1 & ~bitb2, bitb2);
-        }
+        WscQuadPair w;
+        w.two = q1 < nq;
+        w.l0 = 4u * q0;
+        w.l1 = 4u * (w.two ? q1 : q0);
+        w.j0 = w.l0 >> B;
+        w.j1 = w.l1 >> B;
+        w.c0 = (a.pos0 + (((g.tlo | (w.j0 << lowbits) | g.thi) << B) | (w.l0 & mask))) >> 2;
+        w.c1 = (a.pos0 + (((g.tlo | (w.j1 << lowbits) | g.thi) << B) | (w.l1 & mask))) >> 2;
+        w.jb0 = (w.j0 << (B + 1)) * 0x10001u;
+        w.jb1 = (w.j1 << (B + 1)) * 0x10001u;
+        wsc_draw_from<K, B, 0>(a, w, ths, tabs);
     }
 }
 
